@@ -1,0 +1,142 @@
+/*
+ * ttk.h — C ABI of the B200 (sm_100a) tensor-train hot path of arXiv:1906.06785
+ * ("Low-rank solvers for unsteady Navier–Stokes with stochastic viscosity").
+ *
+ * The path: apply the Kronecker-sum operator  A = sum_k T_k (x) G_k (x) K_k
+ * (time (x) stochastic (x) space; PAPER.md:157 eq:F, :239-244 eq:Xz) to a 3-core tensor
+ * train, TT-round the result back to low rank (Alg. 2 :259-273), and the
+ * TT dot / axpby used by low-rank GMRES (Alg. 3).  One GPU, fp64.
+ *
+ * Conventions (R1):
+ *   A TT is X(i_x,i_xi,i_t) = sum_{a,b} U1[i_x,a] U2[a,i_xi,b] U3[b,i_t].  vec(X) runs space
+ *   fastest.  Paper cores z^(1), z^(2), z^(3) (time, stoch, space) map to
+ *   U3^T, U2 with swapped bonds, U1^T.
+ *   All core buffers are DEVICE pointers, float64, compact row-major with the CURRENT ranks:
+ *     U1: n_x  x r1            element (i, a)    at U1[i*r1 + a]
+ *     U2: r1 x n_xi x r2       element (a, i, b) at U2[(a*n_xi + i)*r2 + b]
+ *     U3: r2 x n_t             element (b, t)    at U3[b*n_t + t]
+ *   cap1/cap2 give the rank capacity the buffers were allocated for: U1 holds >= n_x*cap1
+ *   doubles, U2 >= cap1*n_xi*cap2, U3 >= cap2*n_t.
+ *
+ * Ownership: the caller owns every tk_tt buffer (allocated with PyTorch in the binding).
+ * The library owns the context (stream, stream-ordered memory pool for temporaries) and the
+ * device copy of the operator descriptor.  Inputs are never modified except by tk_round,
+ * which rounds in place (ranks never grow).
+ *
+ * Errors: every call returns TK_OK (0) or a negative code; tk_last_error(ctx) returns a
+ * message.  No call falls back to the CPU.  All calls are asynchronous on the context stream
+ * except where noted (tk_round and tk_gmres_cycle block on the host to read the ranks they
+ * choose; tk_*_host variants block to return a host scalar).
+ */
+#ifndef TTK_H
+#define TTK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TK_OK = 0,
+  TK_ESHAPE = -1,    /* mode sizes disagree                        */
+  TK_ECAP = -2,      /* output rank exceeds the capacity of the caller's buffers           */
+  TK_EARG = -3,      /* invalid argument: tol < 0, T < 1, null pointer, rank < 1, ...      */
+  TK_ENUMERIC = -4,  /* non-finite singular values / norms                                 */
+  TK_ECUDA = -5      /* a CUDA runtime error (message in tk_last_error)                    */
+};
+
+typedef struct tk_ctx tk_ctx;
+typedef struct tk_op tk_op;
+
+typedef struct {
+  int64_t n_x, n_xi, n_t; /* mode sizes (space, stochastic, time)                          */
+  int64_t r1, r2;         /* current TT ranks (space bond, time bond), >= 1                */
+  int64_t cap1, cap2;     /* rank capacity of the buffers                                  */
+  double *U1, *U2, *U3;   /* device pointers, layouts above                                */
+} tk_tt;
+
+/* Library version string. */
+const char* tk_version(void);
+
+/* Create a context bound to `cuda_stream` (a cudaStream_t; NULL = legacy default stream).
+ * All work of the context is enqueued on that stream. */
+int tk_ctx_create(tk_ctx** ctx, void* cuda_stream);
+int tk_ctx_destroy(tk_ctx* ctx);
+const char* tk_last_error(const tk_ctx* ctx);
+/* Number of kernels this context has launched since creation (for the bench's
+ * "gpu_launches"). */
+int64_t tk_ctx_launch_count(const tk_ctx* ctx);
+
+/* Operator descriptor  A = sum_{k<T} T_k (x) G_k (x) K_k.
+ *   K_k : n_x x n_x CSR, HOST arrays: rowptr[n_x+1] (int32), col[nnz_k] (int32, 0-based),
+ *         val[nnz_k] (float64).
+ *   G_k : n_xi x n_xi dense, HOST, row-major.
+ *   T_k : n_t x n_t banded, HOST, LAPACK general band storage, column major with
+ *         ldab = kl+ku+1: T[i][j] = band[j*ldab + ku + i - j] for j-ku <= i <= j+kl.
+ * The descriptor is copied to the device; the host arrays may be freed afterwards.
+ * Synchronous (setup, not on the hot path). */
+int tk_op_create(tk_ctx* ctx, tk_op** op, int T, int64_t n_x, int64_t n_xi, int64_t n_t,
+                 const int32_t* const* K_rowptr, const int32_t* const* K_col,
+                 const double* const* K_val, const double* const* G, const int* T_kl,
+                 const int* T_ku, const double* const* T_band);
+int tk_op_destroy(tk_op* op);
+int tk_op_terms(const tk_op* op);
+
+/* y = A x   (PAPER.md:239-244 eq:Xz).  Per term k: K_k U1, G_k x_2 U2,
+ * U3 T_k^T; terms are concatenated: y ranks = (T*x.r1, T*x.r2), y.U1 = [K_0 U1 | ... ],
+ * y.U2 block diagonal (zeros off the diagonal blocks), y.U3 = [U3 T_0^T; U3 T_1^T; ...].
+ * y must have cap1 >= T*x.r1 and cap2 >= T*x.r2 (else TK_ECAP); on success y->r1, y->r2
+ * are set.  Asynchronous. */
+int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y);
+
+/* In-place TT rounding T_eps: on return ||x_new - x||_F <= tol ||x||_F
+ * unless rmax binds, with delta_1 = delta_2 = tol ||x||_F / sqrt(2) and the
+ * rank rule "smallest r >= 1 whose discarded tail (sum_{j>r} s_j^2)^{1/2} <= delta", capped
+ * at rmax when rmax > 0 (R2-R5).  Space bond first, then time bond (north-star
+ * direction).  Output cores: U1 and reshape(U2, r1 n_xi, r2) have orthonormal columns and
+ * ||U3||_F = ||x_new||_F.  The zero tensor canonicalises to ranks (1,1), zero cores.
+ * sigma1_out / sigma2_out (nullable HOST arrays of length >= x->r1 and >= x->r2 on entry)
+ * receive the singular values of the two bonds (descending; entries past the numerical
+ * dimension are 0); discarded_out (nullable HOST, 2 doubles) the discarded tail norms;
+ * norm_out (nullable HOST) ||x||_F of the input.  BLOCKS the host (reads the chosen ranks).
+ */
+int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+             double* sigma2_out, double* discarded_out, double* norm_out);
+
+/* <x, y>_F contracted core by core (Alg. 3 line 7):
+ * W1 = X1^T Y1, W2 = sum_i X2(:,i,:)^T W1 Y2(:,i,:), <x,y> = sum(W2 .* (X3 Y3^T)).
+ * out_dev: DEVICE pointer to one double.  Asynchronous. */
+int tk_dot(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out_dev);
+/* ||x||_F = sqrt(<x,x>) into a DEVICE double.  Asynchronous. */
+int tk_norm(tk_ctx* ctx, const tk_tt* x, double* out_dev);
+
+/* z = a x + b y by core concatenation: z.U1 = [x.U1 | y.U1],
+ * z.U2 = blockdiag(x.U2, y.U2), z.U3 = [a x.U3; b y.U3].  z ranks = sums (TK_ECAP if they
+ * exceed z's capacity).  a_dev / b_dev are DEVICE pointers to one double each (so GMRES
+ * coefficients never leave the device); tk_axpby_host takes host scalars.  Asynchronous.
+ * z must not alias x or y. */
+int tk_axpby(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
+             const tk_tt* y, tk_tt* z);
+int tk_axpby_host(tk_ctx* ctx, double a, const tk_tt* x, double b, const tk_tt* y, tk_tt* z);
+/* x <- s x (scales U3); s_dev DEVICE double; if invert != 0 uses 1/s.  Asynchronous. */
+int tk_scale(tk_ctx* ctx, tk_tt* x, const double* s_dev, int invert);
+
+/* One cycle of low-rank GMRES, Alg. 3 with P = I, z_0 = 0 and the
+ * c5 reading of DESIGN.md R15: x = T(A v_k); MGS with h_ik = <x, v_i>, x = T(x - h_ik v_i);
+ * h_{k+1,k} = ||x||; v_{k+1} = x / h_{k+1,k}; Givens least squares on the host.
+ *   history_out (HOST, steps+1 doubles): beta, then |g_{k+1}| after every step.
+ *   steps_done  (HOST): number of Arnoldi steps performed (< steps on breakdown).
+ *   explicit_out (HOST, nullable): ||T(b - A z)||_F for the returned iterate.
+ *   step_ms_out (HOST, nullable, steps doubles): wall time of each Krylov step (host clock
+ *   around a stream synchronisation).
+ * Blocking. */
+int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps, double tol,
+                   double* history_out, int* steps_done, double* explicit_out,
+                   double* step_ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTK_H */

@@ -1,0 +1,157 @@
+// Operator apply  y = sum_k (T_k (x) G_k (x) K_k) x  on TT cores (eq:Xz).
+//
+//  spmm_multi : Y1[:, k r1:(k+1) r1] = K_k U1 for ALL k in one sweep over the spatial rows.
+//               One warp per row; the row's T*r1 outputs are written once, contiguously
+//               (the write stream is 87% of the apply's HBM bytes at c4).  U1 rows are
+//               gathered through the read-only path (L1/L2 reuse across neighbouring rows
+//               of the stencil-like K_k).  CSR (col, val) pairs are fetched 32 at a time by
+//               the warp and broadcast by shuffles.
+//  stoch_apply: Y2 = blockdiag_k (G_k x_2 U2), written densely (zeros off the blocks).
+//  time_apply : Y3[k r2 + b, :] = U3[b, :] T_k^T with T_k in LAPACK band storage.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "ttk_internal.h"
+
+namespace {
+
+template <int RPL>
+__global__ void __launch_bounds__(256) spmm_multi_k(int64_t n_x, int T, int r,
+                                                    const int32_t* __restrict__ rowptr,
+                                                    const int32_t* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const int64_t* __restrict__ nnz_off,
+                                                    const double* __restrict__ U1,
+                                                    double* __restrict__ Y1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t R = (int64_t)T * r;
+  for (int64_t i = warp; i < n_x; i += nwarps) {
+    double* yrow = Y1 + i * R;
+    for (int k = 0; k < T; k++) {
+      const int32_t* rp = rowptr + (int64_t)k * (n_x + 1);
+      const int64_t base = nnz_off[k];
+      const int beg = rp[i], end = rp[i + 1];
+      double acc[RPL];
+#pragma unroll
+      for (int u = 0; u < RPL; u++) acc[u] = 0.0;
+      for (int e0 = beg; e0 < end; e0 += 32) {
+        int myc = 0;
+        double myv = 0.0;
+        if (e0 + lane < end) {
+          myc = __ldg(col + base + e0 + lane);
+          myv = __ldg(val + base + e0 + lane);
+        }
+        const int cnt = min(32, end - e0);
+        for (int q = 0; q < cnt; q++) {
+          const int c = __shfl_sync(0xffffffffu, myc, q);
+          const double v = __shfl_sync(0xffffffffu, myv, q);
+          const double* urow = U1 + (int64_t)c * r;
+#pragma unroll
+          for (int u = 0; u < RPL; u++) {
+            const int cc = lane + 32 * u;
+            if (cc < r) acc[u] = fma(v, __ldg(urow + cc), acc[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RPL; u++) {
+        const int cc = lane + 32 * u;
+        if (cc < r) yrow[(int64_t)k * r + cc] = acc[u];
+      }
+    }
+  }
+}
+
+__global__ void stoch_apply_k(int T, int r1, int n_xi, int r2, const double* __restrict__ G,
+                              const double* __restrict__ U2, double* __restrict__ Y2) {
+  const int64_t R2 = (int64_t)T * r2;
+  const int64_t rowlen = (int64_t)n_xi * R2;
+  for (int64_t row = blockIdx.x; row < (int64_t)T * r1; row += gridDim.x) {
+    const int k = (int)(row / r1), a = (int)(row % r1);
+    const double* g = G + (int64_t)k * n_xi * n_xi;
+    const double* u = U2 + (int64_t)a * n_xi * r2;
+    double* y = Y2 + row * rowlen;
+    for (int64_t e = threadIdx.x; e < rowlen; e += blockDim.x) {
+      const int i = (int)(e / R2);
+      const int64_t bb = e % R2;
+      double v = 0.0;
+      if (bb >= (int64_t)k * r2 && bb < (int64_t)(k + 1) * r2) {
+        const int b = (int)(bb - (int64_t)k * r2);
+        for (int j = 0; j < n_xi; j++) v = fma(g[(int64_t)i * n_xi + j], u[(int64_t)j * r2 + b], v);
+      }
+      y[e] = v;
+    }
+  }
+}
+
+__global__ void time_apply_k(int T, int r2, int n_t, const int* __restrict__ kl,
+                             const int* __restrict__ ku, const int64_t* __restrict__ band_off,
+                             const double* __restrict__ band, const double* __restrict__ U3,
+                             double* __restrict__ Y3) {
+  const int64_t n = (int64_t)T * r2 * n_t;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e % n_t);
+    const int64_t row = e / n_t;
+    const int k = (int)(row / r2), b = (int)(row % r2);
+    const int l = kl[k], u = ku[k], ld = l + u + 1;
+    const double* bd = band + band_off[k];
+    const double* x = U3 + (int64_t)b * n_t;
+    double v = 0.0;
+    const int s0 = max(0, t - l), s1 = min(n_t - 1, t + u);
+    for (int s = s0; s <= s1; s++) v = fma(bd[(int64_t)s * ld + u + t - s], x[s], v);
+    Y3[e] = v;
+  }
+}
+
+}  // namespace
+
+int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1) {
+  const int64_t n_x = op->n_x;
+  const int threads = 256;
+  int64_t blocks = (n_x * 32 + threads - 1) / threads;
+  blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
+  const int rpl = (r + 31) / 32;
+#define TK_SPMM(R)                                                                          \
+  spmm_multi_k<R><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                           \
+      n_x, op->T, r, op->rowptr, op->col, op->val, op->nnz_off, U1, Y1)
+  if (rpl <= 1)
+    TK_SPMM(1);
+  else if (rpl == 2)
+    TK_SPMM(2);
+  else if (rpl == 3)
+    TK_SPMM(3);
+  else if (rpl == 4)
+    TK_SPMM(4);
+  else if (rpl <= 8)
+    TK_SPMM(8);
+  else {
+    ctx->err = "tk_apply_op: r1 > 256 not supported by spmm_multi";
+    return TK_EARG;
+  }
+#undef TK_SPMM
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
+                          double* Y2) {
+  int64_t rows = (int64_t)op->T * r1;
+  int blocks = (int)std::min<int64_t>(rows, 16LL * ctx->num_sms);
+  stoch_apply_k<<<blocks, 256, 0, ctx->stream>>>(op->T, r1, (int)op->n_xi, r2, op->G, U2, Y2);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+int tk_launch_time_apply(tk_ctx* ctx, const tk_op* op, int r2, const double* U3, double* Y3) {
+  int64_t n = (int64_t)op->T * r2 * op->n_t;
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16LL * ctx->num_sms));
+  time_apply_k<<<blocks, 256, 0, ctx->stream>>>(op->T, r2, (int)op->n_t, op->band_kl,
+                                                op->band_ku, op->band_off, op->band, U3, Y3);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

@@ -1,0 +1,320 @@
+// fp64 GEMM / Gram on the FP64 tensor pipe (DMMA) for sm_100a.
+//
+// tcgen05 has no f64 kind, so fp64 tensor work on B200 is the warp-level
+// mma.sync.aligned.m8n8k4.row.col.f64 (SASS DMMA.8x8x4).  CTA tile 64x64x16, 4 warps each
+// owning a 32x32 sub-tile (4x4 DMMA fragments, 32 fp64 accumulators per thread), operands
+// staged through a 3-stage cp.async (LDGSTS) shared-memory pipeline with zero-filled ragged
+// edges.  Layout-generic: A may be M-major (row-major M x K) or K-major (stored K x M, the
+// Gram/"TN" case), B K-major (K x N) or N-major (stored N x K).  Shared-memory strides are
+// padded so every fragment load is bank-conflict free.
+//
+// Split-K (for the tall-skinny Grams Y^T Y where M, N << K) writes per-split partial tiles
+// that a second kernel reduces in a fixed order: results are deterministic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "ttk_internal.h"
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 128;
+constexpr int PADK = 4;   // stride BK+4 = 20 doubles for M/N-major tiles
+constexpr int PADM = 4;   // stride BM+4 = 68 doubles for K-major tiles
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int valid_elems) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid_elems * 8;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Shared-memory tile geometry
+template <bool KMAJOR, int BMN>
+struct TileGeom {
+  // KMAJOR: [BK][BMN + PADM];  else [BMN][BK + PADK]
+  static constexpr int SIZE = KMAJOR ? BK * (BMN + PADM) : BMN * (BK + PADK);
+  __device__ static __forceinline__ int idx(int k, int m) {
+    return KMAJOR ? k * (BMN + PADM) + m : m * (BK + PADK) + k;
+  }
+};
+
+// Load a BMN x BK tile of an operand into shared memory.
+//   KMAJOR: global element (k, m) at G[(k0+k)*ld + m0+m]   (contiguous in m)
+//   else  : global element (k, m) at G[(m0+m)*ld + k0+k]   (contiguous in k)
+template <bool KMAJOR, int BMN, bool VEC2>
+__device__ __forceinline__ void load_tile(double* sm, const double* __restrict__ G, int64_t ld,
+                                          int64_t m0, int64_t mlim, int64_t k0, int64_t klim,
+                                          int tid) {
+  using GEO = TileGeom<KMAJOR, BMN>;
+  if (VEC2) {
+    constexpr int PAIRS = BMN * BK / 2;
+#pragma unroll
+    for (int e = tid; e < PAIRS; e += NT) {
+      int k, m;
+      int64_t gk, gm;
+      const double* src;
+      int valid;
+      if (KMAJOR) {
+        k = e / (BMN / 2);
+        m = (e % (BMN / 2)) * 2;
+        gk = k0 + k;
+        gm = m0 + m;
+        valid = (gk < klim) ? (int)max((int64_t)0, min((int64_t)2, mlim - gm)) : 0;
+        src = G + (valid ? gk * ld + gm : 0);
+        cp_async16(sm + GEO::idx(k, m), src, valid);
+      } else {
+        m = e / (BK / 2);
+        k = (e % (BK / 2)) * 2;
+        gk = k0 + k;
+        gm = m0 + m;
+        valid = (gm < mlim) ? (int)max((int64_t)0, min((int64_t)2, klim - gk)) : 0;
+        src = G + (valid ? gm * ld + gk : 0);
+        cp_async16(sm + GEO::idx(k, m), src, valid);
+      }
+    }
+  } else {
+    constexpr int ELEMS = BMN * BK;
+#pragma unroll
+    for (int e = tid; e < ELEMS; e += NT) {
+      int k, m;
+      if (KMAJOR) {
+        k = e / BMN;
+        m = e % BMN;
+      } else {
+        m = e / BK;
+        k = e % BK;
+      }
+      int64_t gk = k0 + k, gm = m0 + m;
+      bool valid = gk < klim && gm < mlim;
+      const double* src = G + (valid ? (KMAJOR ? gk * ld + gm : gm * ld + gk) : 0);
+      cp_async8(sm + GEO::idx(k, m), src, valid);
+    }
+  }
+}
+
+// A_KMAJOR == transA ; B_KMAJOR == !transB
+template <bool A_KMAJOR, bool B_KMAJOR, bool VEC2>
+__global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t K,
+                                                   const double* __restrict__ A, int64_t lda,
+                                                   const double* __restrict__ B, int64_t ldb,
+                                                   double* __restrict__ C, int64_t ldc,
+                                                   double alpha, double beta, int64_t kchunk,
+                                                   int sym, double* __restrict__ partial) {
+  using GA = TileGeom<A_KMAJOR, BM>;
+  using GB = TileGeom<B_KMAJOR, BN>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * GA::SIZE;
+
+  const int tile_m = blockIdx.y, tile_n = blockIdx.x;
+  if (sym && tile_n < tile_m) return;
+  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = min(K, kbeg + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int lr = lane >> 2, lc = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int64_t ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  // prologue
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < ntiles) {
+      int64_t k0 = kbeg + (int64_t)s * BK;
+      load_tile<A_KMAJOR, BM, VEC2>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
+      load_tile<B_KMAJOR, BN, VEC2>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
+    }
+    cp_commit();
+  }
+
+  for (int64_t t = 0; t < ntiles; t++) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    // prefetch tile t + STAGES - 1
+    {
+      int64_t tn = t + STAGES - 1;
+      if (tn < ntiles) {
+        int s = (int)(tn % STAGES);
+        int64_t k0 = kbeg + tn * BK;
+        load_tile<A_KMAJOR, BM, VEC2>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
+        load_tile<B_KMAJOR, BN, VEC2>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
+      }
+      cp_commit();
+    }
+    const double* as = As + (int)(t % STAGES) * GA::SIZE;
+    const double* bs = Bs + (int)(t % STAGES) * GB::SIZE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) a[i] = as[GA::idx(kk + lc, wm * 32 + i * 8 + lr)];
+#pragma unroll
+      for (int j = 0; j < 4; j++) b[j] = bs[GB::idx(kk + lc, wn * 32 + j * 8 + lr)];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int64_t gm = m0 + wm * 32 + i * 8 + lr;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t gn = n0 + wn * 32 + j * 8 + 2 * lc + h;
+        if (gn >= N) continue;
+        if (sym && gn < gm) continue;
+        double v = acc[i][j][h];
+        if (partial) {
+          partial[((int64_t)blockIdx.z * M + gm) * N + gn] = v;
+        } else {
+          double o = alpha * v;
+          if (beta != 0.0) o += beta * C[gm * ldc + gn];
+          C[gm * ldc + gn] = o;
+          if (sym && gn != gm) {
+            double o2 = alpha * v;
+            if (beta != 0.0) o2 += beta * C[gn * ldc + gm];
+            C[gn * ldc + gm] = o2;
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ P,
+                              double* __restrict__ C, int64_t ldc, double alpha, double beta,
+                              int sym) {
+  int64_t total = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = e / N, n = e % N;
+    int64_t pm = m, pn = n;
+    if (sym && n < m) {
+      pm = n;
+      pn = m;
+    }
+    double s = 0.0;
+    for (int z = 0; z < splits; z++) s += P[((int64_t)z * M + pm) * N + pn];
+    double o = alpha * s;
+    if (beta != 0.0) o += beta * C[m * ldc + n];
+    C[m * ldc + n] = o;
+  }
+}
+
+template <bool AK, bool BK_, bool V2>
+int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
+             int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
+             double beta, int64_t kchunk, int sym, double* partial) {
+  using GA = TileGeom<AK, BM>;
+  using GB = TileGeom<BK_, BN>;
+  size_t smem = (size_t)STAGES * (GA::SIZE + GB::SIZE) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dgemm_kernel<AK, BK_, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  dgemm_kernel<AK, BK_, V2><<<grid, NT, smem, ctx->stream>>>(M, N, K, A, lda, B, ldb, C, ldc,
+                                                             alpha, beta, kchunk, sym, partial);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+}  // namespace
+
+int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+             double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+             double beta, double* C, int64_t ldc, bool sym) {
+  if (M <= 0 || N <= 0) return TK_OK;
+  if (sym && M != N) {
+    ctx->err = "tk_dgemm: sym requires M == N";
+    return TK_EARG;
+  }
+  if (K <= 0) {
+    if (beta != 0.0) {
+      ctx->err = "tk_dgemm: K == 0 with beta != 0 is not supported";
+      return TK_EARG;
+    }
+    for (int64_t m = 0; m < M; m++)
+      TK_CUDA_TRY(ctx, cudaMemsetAsync(C + m * ldc, 0, N * sizeof(double), ctx->stream));
+    return TK_OK;
+  }
+  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
+  // split-K: aim for >= 4 CTAs per SM when the output is small and K is long
+  int64_t target = 4LL * ctx->num_sms;
+  int64_t splits = 1;
+  if (tiles < target && K >= 8 * BK) {
+    splits = std::min<int64_t>((target + tiles - 1) / tiles, (K + 8 * BK - 1) / (8 * BK));
+    splits = std::max<int64_t>(splits, 1);
+  }
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = ((kchunk + BK - 1) / BK) * BK;
+  splits = (K + kchunk - 1) / kchunk;
+  double* partial = nullptr;
+  DevBuf pbuf;
+  if (splits > 1) {
+    TK_TRY(pbuf.get(ctx, (size_t)splits * M * N));
+    partial = pbuf.p;
+  }
+  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
+  const bool AK = transA, BKm = !transB;
+  // 16-byte vector path: contiguous dims even and 16-byte aligned bases
+  bool v2 = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
+            (((uintptr_t)B & 15) == 0);
+  int st;
+#define TK_GEMM_CASE(a, b, v)                                                             \
+  if (AK == a && BKm == b && v2 == v)                                                     \
+    st = launch_t<a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, \
+                           sym ? 1 : 0, partial);
+  TK_GEMM_CASE(false, false, false)
+  TK_GEMM_CASE(false, false, true)
+  TK_GEMM_CASE(false, true, false)
+  TK_GEMM_CASE(false, true, true)
+  TK_GEMM_CASE(true, false, false)
+  TK_GEMM_CASE(true, false, true)
+  TK_GEMM_CASE(true, true, false)
+  TK_GEMM_CASE(true, true, true)
+#undef TK_GEMM_CASE
+  if (st != TK_OK) return st;
+  if (splits > 1) {
+    int64_t total = M * N;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * ctx->num_sms);
+    splitk_reduce<<<blocks, 256, 0, ctx->stream>>>(M, N, (int)splits, partial, C, ldc, alpha,
+                                                   beta, sym ? 1 : 0);
+    TK_LAUNCH_CHECK(ctx);
+  }
+  return TK_OK;
+}

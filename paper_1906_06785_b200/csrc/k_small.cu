@@ -1,0 +1,295 @@
+// Small fp64 helper kernels of the rounding / dot / axpby path (sm_100a).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "ttk_internal.h"
+
+namespace {
+
+inline int grid_for(tk_ctx* ctx, int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 16LL * ctx->num_sms));
+}
+
+// mode 0: dst = src * f[col]; 1: dst = src / f[col] (0 where f == 0)
+__global__ void col_scale_k(int64_t rows, int64_t cols, const double* __restrict__ src,
+                            int64_t lds, double* __restrict__ dst, int64_t ldd,
+                            const double* __restrict__ f, int mode) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    double s = src[r * lds + c], g = f[c];
+    dst[r * ldd + c] = mode == 0 ? s * g : (g != 0.0 ? s / g : 0.0);
+  }
+}
+
+__global__ void row_scale_k(int64_t rows, int64_t cols, const double* __restrict__ src,
+                            int64_t lds, double* __restrict__ dst, int64_t ldd,
+                            const double* __restrict__ f, int mode) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    double s = src[r * lds + c], g = f[r];
+    dst[r * ldd + c] = mode == 0 ? s * g : (g != 0.0 ? s / g : 0.0);
+  }
+}
+
+__global__ void copy2d_k(int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
+                         double* __restrict__ dst, int64_t ldd) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+__global__ void fill_k(double* dst, int64_t n, double v) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = v;
+}
+
+__global__ void eye_k(double* dst, int64_t n) {
+  int64_t nn = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+// Rank rule of PAPER.md:247-249 / SPEC.md:105,109 on sigma = sqrt(max(lam,0)), lam descending.
+// One warp: tail sums accumulated from the smallest value upward, sequentially (n <= a few
+// thousand), so the result does not depend on the launch shape.
+__global__ void rank_select_k(int n, const double* __restrict__ lam, double* __restrict__ sig,
+                              double tol, const double* __restrict__ delta_in, int64_t rmax,
+                              double kthr, int* __restrict__ info, double* __restrict__ dinfo) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = sqrt(fmax(lam[i], 0.0));
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  double nrm2 = 0.0;
+  for (int i = n - 1; i >= 0; i--) nrm2 += sig[i] * sig[i];
+  double nrm = sqrt(nrm2);
+  double delta = delta_in ? delta_in[0] : tol * nrm / sqrt(2.0);
+  // smallest r >= 1 with ||sig[r:]|| <= delta
+  double tail2 = 0.0;
+  int r = n;
+  // walk from the end: tail2 after adding sig[j] is ||sig[j:]||^2
+  // r = smallest cand with ||sig[cand:]|| <= delta; iterate cand from n down to 1
+  for (int cand = n; cand >= 1; cand--) {
+    double t = (cand < n) ? sqrt(tail2) : 0.0;
+    if (t <= delta)
+      r = cand;
+    else
+      break;
+    if (cand - 1 >= 0) tail2 += sig[cand - 1] * sig[cand - 1];
+  }
+  while (r < n && sig[r] == sig[r - 1]) r++;
+  if (rmax > 0 && r > rmax) r = (int)rmax;
+  if (r < 1) r = 1;
+  int k = 0;
+  for (int i = 0; i < n; i++)
+    if (sig[i] > kthr * sig[0]) k = i + 1;
+  if (k < 1) k = 1;
+  double disc2 = 0.0;
+  for (int i = n - 1; i >= r; i--) disc2 += sig[i] * sig[i];
+  info[0] = r;
+  info[1] = k;
+  dinfo[0] = nrm;
+  dinfo[1] = delta;
+  dinfo[2] = sqrt(disc2);
+}
+
+// z = a x + b y cores (concatenation)
+__global__ void axpby_u1_k(int64_t n_x, int64_t rx, int64_t ry, const double* __restrict__ x1,
+                           const double* __restrict__ y1, double* __restrict__ z1) {
+  int64_t R = rx + ry, n = n_x * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / R, c = e % R;
+    z1[e] = c < rx ? x1[i * rx + c] : y1[i * ry + (c - rx)];
+  }
+}
+__global__ void axpby_u2_k(int64_t rx1, int64_t ry1, int64_t n_xi, int64_t rx2, int64_t ry2,
+                           const double* __restrict__ x2, const double* __restrict__ y2,
+                           double* __restrict__ z2) {
+  int64_t R1 = rx1 + ry1, R2 = rx2 + ry2, n = R1 * n_xi * R2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = e % R2, t = e / R2, i = t % n_xi, a = t / n_xi;
+    double v = 0.0;
+    if (a < rx1 && b < rx2)
+      v = x2[(a * n_xi + i) * rx2 + b];
+    else if (a >= rx1 && b >= rx2)
+      v = y2[((a - rx1) * n_xi + i) * ry2 + (b - rx2)];
+    z2[e] = v;
+  }
+}
+__global__ void axpby_u3_k(int64_t rx2, int64_t ry2, int64_t n_t, const double* __restrict__ a,
+                           const double* __restrict__ x3, const double* __restrict__ b,
+                           const double* __restrict__ y3, double* __restrict__ z3) {
+  int64_t n = (rx2 + ry2) * n_t;
+  double av = a[0], bv = b[0];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / n_t;
+    z3[e] = r < rx2 ? av * x3[e] : bv * y3[e - rx2 * n_t];
+  }
+}
+
+__global__ void scale_k(double* U, int64_t n, const double* s, int invert) {
+  double f = invert ? 1.0 / s[0] : s[0];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    U[e] *= f;
+}
+
+// out = sum(a .* b) (single block, deterministic order); optional sqrt
+__global__ void dot_final_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                            double* out, int take_sqrt) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) s += a[e] * b[e];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = take_sqrt ? sqrt(fmax(red[0], 0.0)) : red[0];
+}
+
+__global__ void set_scalar_k(double* dst, double v) { dst[0] = v; }
+__global__ void neg_scalar_k(const double* src, double* dst) { dst[0] = -src[0]; }
+
+__global__ void transpose_k(int64_t rows, int64_t cols, const double* __restrict__ src,
+                            int64_t lds, double* __restrict__ dst, int64_t ldd) {
+  __shared__ double tile[32][33];
+  for (int64_t r0 = (int64_t)blockIdx.y * 32; r0 < rows; r0 += (int64_t)gridDim.y * 32)
+    for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < cols; c0 += (int64_t)gridDim.x * 32) {
+      for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        int64_t r = r0 + dy, c = c0 + threadIdx.x;
+        tile[dy][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.0;
+      }
+      __syncthreads();
+      for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        int64_t c = c0 + dy, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][dy];
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void symmetrize_k(int64_t n, double* A) {
+  int64_t nn = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / n, j = e % n;
+    if (j > i) {
+      double v = 0.5 * (A[i * n + j] + A[j * n + i]);
+      A[i * n + j] = v;
+      A[j * n + i] = v;
+    }
+  }
+}
+
+}  // namespace
+
+int tk_neg_scalar(tk_ctx* ctx, const double* src, double* dst) {
+  neg_scalar_k<<<1, 1, 0, ctx->stream>>>(src, dst);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_transpose(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return TK_OK;
+  dim3 grid((unsigned)std::min<int64_t>((cols + 31) / 32, 1024),
+            (unsigned)std::min<int64_t>((rows + 31) / 32, 1024));
+  transpose_k<<<grid, dim3(32, 8), 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_symmetrize(tk_ctx* ctx, int64_t n, double* A) {
+  if (n <= 1) return TK_OK;
+  symmetrize_k<<<grid_for(ctx, n * n), 256, 0, ctx->stream>>>(n, A);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+int tk_col_scale(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd, const double* f, int mode) {
+  if (rows <= 0 || cols <= 0) return TK_OK;
+  col_scale_k<<<grid_for(ctx, rows * cols), 256, 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd,
+                                                                   f, mode);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_row_scale(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd, const double* f, int mode) {
+  if (rows <= 0 || cols <= 0) return TK_OK;
+  row_scale_k<<<grid_for(ctx, rows * cols), 256, 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd,
+                                                                   f, mode);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_copy2d(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+              double* dst, int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return TK_OK;
+  copy2d_k<<<grid_for(ctx, rows * cols), 256, 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_fill(tk_ctx* ctx, double* dst, int64_t n, double v) {
+  if (n <= 0) return TK_OK;
+  fill_k<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(dst, n, v);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_eye(tk_ctx* ctx, double* dst, int64_t n) {
+  if (n <= 0) return TK_OK;
+  eye_k<<<grid_for(ctx, n * n), 256, 0, ctx->stream>>>(dst, n);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
+                   const double* delta_dev_in, int64_t rmax, double kthr, int* info,
+                   double* dinfo) {
+  rank_select_k<<<1, 32, 0, ctx->stream>>>(n, lam, sig, tol, delta_dev_in, rmax, kthr, info,
+                                           dinfo);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_axpby_cores(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
+                   const tk_tt* y, tk_tt* z) {
+  int64_t R1 = x->r1 + y->r1, R2 = x->r2 + y->r2;
+  axpby_u1_k<<<grid_for(ctx, x->n_x * R1), 256, 0, ctx->stream>>>(x->n_x, x->r1, y->r1, x->U1,
+                                                                  y->U1, z->U1);
+  TK_LAUNCH_CHECK(ctx);
+  axpby_u2_k<<<grid_for(ctx, R1 * x->n_xi * R2), 256, 0, ctx->stream>>>(
+      x->r1, y->r1, x->n_xi, x->r2, y->r2, x->U2, y->U2, z->U2);
+  TK_LAUNCH_CHECK(ctx);
+  axpby_u3_k<<<grid_for(ctx, R2 * x->n_t), 256, 0, ctx->stream>>>(x->r2, y->r2, x->n_t, a_dev,
+                                                                  x->U3, b_dev, y->U3, z->U3);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_scale_rows(tk_ctx* ctx, double* U3, int64_t n, const double* s_dev, int invert) {
+  scale_k<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(U3, n, s_dev, invert);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_dot_final(tk_ctx* ctx, int64_t n, const double* a, const double* b, double* out,
+                 int take_sqrt) {
+  dot_final_k<<<1, 256, 0, ctx->stream>>>(n, a, b, out, take_sqrt);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+int tk_set_scalar(tk_ctx* ctx, double* dst, double v) {
+  set_scalar_k<<<1, 1, 0, ctx->stream>>>(dst, v);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

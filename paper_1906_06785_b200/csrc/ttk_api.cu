@@ -1,0 +1,707 @@
+// libttk C ABI: context, operator descriptor, apply, round, dot, axpby, GMRES cycle.
+// See include/ttk.h for the contract of every entry point and DESIGN.md for the algorithms.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "ttk_internal.h"
+
+static const double kEps = 2.220446049250313e-16;
+
+// ============================================================================ memory
+int tk_alloc(tk_ctx* ctx, void** p, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(p, bytes, ctx->stream);
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaMallocAsync(") + std::to_string(bytes) + "): " +
+               cudaGetErrorString(e);
+    *p = nullptr;
+    return TK_ECUDA;
+  }
+  return TK_OK;
+}
+void tk_free(tk_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+// ============================================================================ context
+extern "C" const char* tk_version(void) { return "ttk 0.1 (sm_100a, fp64 DMMA)"; }
+
+extern "C" int tk_ctx_create(tk_ctx** out, void* stream) {
+  if (!out) return TK_EARG;
+  auto* ctx = new tk_ctx();
+  ctx->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (e == cudaSuccess) {
+    // keep freed pool memory cached: stream-ordered allocations stay cheap in steady state
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    ctx->pinned_bytes = 1 << 16;
+    e = cudaMallocHost(&ctx->pinned, ctx->pinned_bytes);
+  }
+  if (e != cudaSuccess) {
+    delete ctx;
+    return TK_ECUDA;
+  }
+  *out = ctx;
+  return TK_OK;
+}
+
+extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
+  if (!ctx) return TK_OK;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  return TK_OK;
+}
+
+extern "C" const char* tk_last_error(const tk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+extern "C" int64_t tk_ctx_launch_count(const tk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (bytes > ctx->pinned_bytes) {
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TK_OK;
+  }
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(host, ctx->pinned, bytes);
+  return TK_OK;
+}
+
+// ============================================================================ operator
+extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_t n_xi,
+                            int64_t n_t, const int32_t* const* K_rowptr,
+                            const int32_t* const* K_col, const double* const* K_val,
+                            const double* const* G, const int* T_kl, const int* T_ku,
+                            const double* const* T_band) {
+  if (!ctx || !out) return TK_EARG;
+  if (T < 1 || n_x < 1 || n_xi < 1 || n_t < 1) {
+    ctx->err = "tk_op_create: T, n_x, n_xi, n_t must be >= 1";
+    return TK_EARG;
+  }
+  if (n_x >= INT32_MAX) {
+    ctx->err = "tk_op_create: n_x must fit int32 CSR indices";
+    return TK_EARG;
+  }
+  auto op = std::make_unique<tk_op>();
+  op->ctx = ctx;
+  op->T = T;
+  op->n_x = n_x;
+  op->n_xi = n_xi;
+  op->n_t = n_t;
+  std::vector<int64_t> nnz_off(T + 1, 0), band_off(T + 1, 0);
+  for (int k = 0; k < T; k++) {
+    if (!K_rowptr[k] || !G[k] || !T_band[k] || T_kl[k] < 0 || T_ku[k] < 0) {
+      ctx->err = "tk_op_create: null descriptor array or negative band width";
+      return TK_EARG;
+    }
+    int64_t nnz = K_rowptr[k][n_x] - K_rowptr[k][0];
+    if (K_rowptr[k][0] != 0 || nnz < 0) {
+      ctx->err = "tk_op_create: rowptr must start at 0 and be non-decreasing";
+      return TK_EARG;
+    }
+    if (nnz > 0 && (!K_col[k] || !K_val[k])) {
+      ctx->err = "tk_op_create: null CSR arrays";
+      return TK_EARG;
+    }
+    for (int64_t c = 0; c < nnz; c++)
+      if (K_col[k][c] < 0 || K_col[k][c] >= n_x) {
+        ctx->err = "tk_op_create: CSR column index out of range";
+        return TK_EARG;
+      }
+    nnz_off[k + 1] = nnz_off[k] + nnz;
+    band_off[k + 1] = band_off[k] + (int64_t)(T_kl[k] + T_ku[k] + 1) * n_t;
+    op->max_kl = std::max(op->max_kl, T_kl[k]);
+    op->max_ku = std::max(op->max_ku, T_ku[k]);
+    op->h_nnz.push_back(nnz);
+  }
+  const int64_t tot = nnz_off[T];
+  auto dmal = [&](void** p, size_t b) -> int {
+    TK_CUDA_TRY(ctx, cudaMalloc(p, b ? b : 8));
+    return TK_OK;
+  };
+  TK_TRY(dmal((void**)&op->rowptr, sizeof(int32_t) * T * (n_x + 1)));
+  TK_TRY(dmal((void**)&op->col, sizeof(int32_t) * tot));
+  TK_TRY(dmal((void**)&op->val, sizeof(double) * tot));
+  TK_TRY(dmal((void**)&op->nnz_off, sizeof(int64_t) * (T + 1)));
+  TK_TRY(dmal((void**)&op->G, sizeof(double) * T * n_xi * n_xi));
+  TK_TRY(dmal((void**)&op->band_kl, sizeof(int) * T));
+  TK_TRY(dmal((void**)&op->band_ku, sizeof(int) * T));
+  TK_TRY(dmal((void**)&op->band_off, sizeof(int64_t) * (T + 1)));
+  TK_TRY(dmal((void**)&op->band, sizeof(double) * band_off[T]));
+  for (int k = 0; k < T; k++) {
+    TK_CUDA_TRY(ctx, cudaMemcpy(op->rowptr + (int64_t)k * (n_x + 1), K_rowptr[k],
+                                sizeof(int32_t) * (n_x + 1), cudaMemcpyHostToDevice));
+    int64_t nnz = nnz_off[k + 1] - nnz_off[k];
+    if (nnz) {
+      TK_CUDA_TRY(ctx, cudaMemcpy(op->col + nnz_off[k], K_col[k], sizeof(int32_t) * nnz,
+                                  cudaMemcpyHostToDevice));
+      TK_CUDA_TRY(ctx, cudaMemcpy(op->val + nnz_off[k], K_val[k], sizeof(double) * nnz,
+                                  cudaMemcpyHostToDevice));
+    }
+    TK_CUDA_TRY(ctx, cudaMemcpy(op->G + (int64_t)k * n_xi * n_xi, G[k],
+                                sizeof(double) * n_xi * n_xi, cudaMemcpyHostToDevice));
+    TK_CUDA_TRY(ctx, cudaMemcpy(op->band + band_off[k], T_band[k],
+                                sizeof(double) * (band_off[k + 1] - band_off[k]),
+                                cudaMemcpyHostToDevice));
+  }
+  TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
+                              cudaMemcpyHostToDevice));
+  TK_CUDA_TRY(ctx, cudaMemcpy(op->band_kl, T_kl, sizeof(int) * T, cudaMemcpyHostToDevice));
+  TK_CUDA_TRY(ctx, cudaMemcpy(op->band_ku, T_ku, sizeof(int) * T, cudaMemcpyHostToDevice));
+  TK_CUDA_TRY(ctx, cudaMemcpy(op->band_off, band_off.data(), sizeof(int64_t) * (T + 1),
+                              cudaMemcpyHostToDevice));
+  *out = op.release();
+  return TK_OK;
+}
+
+extern "C" int tk_op_destroy(tk_op* op) {
+  if (!op) return TK_OK;
+  cudaFree(op->rowptr);
+  cudaFree(op->col);
+  cudaFree(op->val);
+  cudaFree(op->nnz_off);
+  cudaFree(op->G);
+  cudaFree(op->band_kl);
+  cudaFree(op->band_ku);
+  cudaFree(op->band_off);
+  cudaFree(op->band);
+  delete op;
+  return TK_OK;
+}
+extern "C" int tk_op_terms(const tk_op* op) { return op ? op->T : 0; }
+
+// ============================================================================ validation
+static int check_tt(tk_ctx* ctx, const tk_tt* x, const char* who) {
+  if (!x || !x->U1 || !x->U2 || !x->U3) {
+    ctx->err = std::string(who) + ": null TT or core pointer";
+    return TK_EARG;
+  }
+  if (x->n_x < 1 || x->n_xi < 1 || x->n_t < 1 || x->r1 < 1 || x->r2 < 1) {
+    ctx->err = std::string(who) + ": mode sizes and ranks must be >= 1";
+    return TK_EARG;
+  }
+  if (x->r1 > x->cap1 || x->r2 > x->cap2) {
+    ctx->err = std::string(who) + ": rank exceeds capacity";
+    return TK_ECAP;
+  }
+  return TK_OK;
+}
+
+// ============================================================================ apply
+extern "C" int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y) {
+  if (!ctx || !op) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_apply_op(x)"));
+  if (!y || !y->U1 || !y->U2 || !y->U3) {
+    ctx->err = "tk_apply_op: null output TT";
+    return TK_EARG;
+  }
+  if (x->n_x != op->n_x || x->n_xi != op->n_xi || x->n_t != op->n_t || y->n_x != op->n_x ||
+      y->n_xi != op->n_xi || y->n_t != op->n_t) {
+    ctx->err = "tk_apply_op: mode sizes differ from the operator's";
+    return TK_ESHAPE;
+  }
+  const int64_t R1 = op->T * x->r1, R2 = op->T * x->r2;
+  if (R1 > y->cap1 || R2 > y->cap2) {
+    ctx->err = "tk_apply_op: output capacity < (T r1, T r2)";
+    return TK_ECAP;
+  }
+  TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
+  TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, y->U2));
+  TK_TRY(tk_launch_time_apply(ctx, op, (int)x->r2, x->U3, y->U3));
+  y->r1 = R1;
+  y->r2 = R2;
+  return TK_OK;
+}
+
+// ============================================================================ rounding
+namespace {
+
+struct EigOpts {
+  double abs_scale, rel;
+};
+const EigOpts kPass1{kEps, kEps};            // orthogonal basis, absolute accuracy
+const EigOpts kPass2{kEps * kEps, kEps};     // relative accuracy (graded Gram)
+const int kMaxSweeps = 40;
+const double kDropThr = 64.0 * kEps;         // numerical-dimension threshold of orth_rows
+
+// A (R x N, row-major, ld N) = L (R x k) * Q (k x N, orthonormal rows) with Q stored
+// transposed as Qc (N x k).  Two-pass Gram-Jacobi on B = A^T.
+// Outputs are allocated here.  Returns k via *k_out (host; blocks).
+int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, DevBuf& Qc,
+              int64_t* k_out) {
+  DevBuf G, V, W, GW, lam, V2, sig, scr, tmp;
+  TK_TRY(G.get(ctx, R * R));
+  TK_TRY(V.get(ctx, R * R));
+  TK_TRY(lam.get(ctx, R));
+  // pass 1: G = A A^T, orthogonal eigenbasis V
+  TK_TRY(tk_dgemm(ctx, false, true, R, R, N, 1.0, A, N, A, N, 0.0, G.p, R, true));
+  TK_TRY(tk_jacobi_eig(ctx, (int)R, G.p, lam.p, V.p, kPass1.abs_scale, kPass1.rel, kMaxSweeps,
+                       nullptr));
+  // W = A^T V  (N x R)
+  TK_TRY(W.get(ctx, N * R));
+  TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
+  // pass 2: GW = W^T W, relative eigen-decomposition
+  TK_TRY(GW.get(ctx, R * R));
+  TK_TRY(tk_dgemm(ctx, true, false, R, R, N, 1.0, W.p, R, W.p, R, 0.0, GW.p, R, true));
+  TK_TRY(V2.get(ctx, R * R));
+  TK_TRY(tk_jacobi_eig(ctx, (int)R, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel,
+                       kMaxSweeps, nullptr));
+  TK_TRY(sig.get(ctx, R));
+  TK_TRY(scr.get(ctx, 8));
+  int* info = (int*)scr.p;
+  double* dinfo = scr.p + 2;
+  TK_TRY(tk_rank_select(ctx, (int)R, lam.p, sig.p, 0.0, nullptr, 0, kDropThr, info, dinfo));
+  int hinfo[2];
+  TK_TRY(sync_read(ctx, hinfo, info, sizeof(hinfo)));
+  const int64_t k = hinfo[1];
+  // Qc = W V2[:, :k] diag(1/sig)   (N x k)
+  TK_TRY(tmp.get(ctx, R * k));
+  TK_TRY(tk_col_scale(ctx, R, k, V2.p, R, tmp.p, k, sig.p, 1));
+  TK_TRY(Qc.get(ctx, N * k));
+  TK_TRY(tk_dgemm(ctx, false, false, N, k, R, 1.0, W.p, R, tmp.p, k, 0.0, Qc.p, k));
+  // L = (V V2)[:, :k] diag(sig)   (R x k)
+  DevBuf VV;
+  TK_TRY(VV.get(ctx, R * k));
+  TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, V.p, R, V2.p, R, 0.0, VV.p, k));
+  TK_TRY(L.get(ctx, R * k));
+  TK_TRY(tk_col_scale(ctx, R, k, VV.p, k, L.p, k, sig.p, 0));
+  *k_out = k;
+  return TK_OK;
+}
+
+// SVD of Z = Y L (Y: M x R explicit, ld R; L: R x k, ld k; L == nullptr means identity with
+// k = R) by two-pass Gram-Jacobi.  Returns W (M x k), V2 (k x k), Vt = V V2 (k x k), lam
+// (k, descending eigenvalues of W^T W = squared singular values of Z).
+int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const double* Lm,
+                 int64_t k, DevBuf& W, DevBuf& V2, DevBuf& Vt, DevBuf& lam) {
+  DevBuf GY, GZ, T1, V, P;
+  TK_TRY(GZ.get(ctx, k * k));
+  if (Lm) {
+    TK_TRY(GY.get(ctx, R * R));
+    TK_TRY(tk_dgemm(ctx, true, false, R, R, M, 1.0, Y, R, Y, R, 0.0, GY.p, R, true));
+    TK_TRY(T1.get(ctx, R * k));
+    TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, GY.p, R, Lm, k, 0.0, T1.p, k));
+    TK_TRY(tk_dgemm(ctx, true, false, k, k, R, 1.0, Lm, k, T1.p, k, 0.0, GZ.p, k));
+    TK_TRY(tk_symmetrize(ctx, k, GZ.p));
+  } else {
+    TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, Y, R, Y, R, 0.0, GZ.p, k, true));
+  }
+  TK_TRY(V.get(ctx, k * k));
+  TK_TRY(lam.get(ctx, k));
+  TK_TRY(tk_jacobi_eig(ctx, (int)k, GZ.p, lam.p, V.p, kPass1.abs_scale, kPass1.rel, kMaxSweeps,
+                       nullptr));
+  // W = Y (L V)
+  const double* PV = V.p;
+  if (Lm) {
+    TK_TRY(P.get(ctx, R * k));
+    TK_TRY(tk_dgemm(ctx, false, false, R, k, k, 1.0, Lm, k, V.p, k, 0.0, P.p, k));
+    PV = P.p;
+  }
+  TK_TRY(W.get(ctx, M * k));
+  TK_TRY(tk_dgemm(ctx, false, false, M, k, R, 1.0, Y, R, PV, k, 0.0, W.p, k));
+  DevBuf GW;
+  TK_TRY(GW.get(ctx, k * k));
+  TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, W.p, k, W.p, k, 0.0, GW.p, k, true));
+  TK_TRY(V2.get(ctx, k * k));
+  TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
+                       nullptr));
+  TK_TRY(Vt.get(ctx, k * k));
+  TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
+  return TK_OK;
+}
+
+int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
+  x->r1 = 1;
+  x->r2 = 1;
+  TK_TRY(tk_fill(ctx, x->U1, x->n_x, 0.0));
+  TK_TRY(tk_fill(ctx, x->U2, x->n_xi, 0.0));
+  TK_TRY(tk_fill(ctx, x->U3, x->n_t, 0.0));
+  return TK_OK;
+}
+
+}  // namespace
+
+extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                        double* sigma2_out, double* discarded_out, double* norm_out) {
+  if (!ctx) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_round"));
+  if (!(tol >= 0.0) || !std::isfinite(tol)) {
+    ctx->err = "tk_round: tol must be finite and >= 0";
+    return TK_EARG;
+  }
+  const int64_t n_x = x->n_x, n_xi = x->n_xi, n_t = x->n_t, R1 = x->r1, R2 = x->r2;
+  // ---- step A: time core  U3 = L3 Q3  (Q3 = identity when n_t <= R2)
+  DevBuf L3b, Q3c;
+  const double* L3 = x->U3;
+  int64_t k3 = n_t;
+  bool q3_id = true;
+  if (n_t > R2) {
+    TK_TRY(orth_rows(ctx, R2, n_t, x->U3, L3b, Q3c, &k3));
+    L3 = L3b.p;
+    q3_id = false;
+  }
+  // ---- step B: Y2p = U2 x_3 L3   ((R1 n_xi) x R2) (R2 x k3)
+  DevBuf Y2p;
+  TK_TRY(Y2p.get(ctx, R1 * n_xi * k3));
+  TK_TRY(tk_dgemm(ctx, false, false, R1 * n_xi, k3, R2, 1.0, x->U2, R2, L3, k3, 0.0, Y2p.p, k3));
+  // ---- step C: Y2p as R1 x (n_xi k3) = L2 Q2
+  const int64_t N2 = n_xi * k3;
+  DevBuf L2b, Q2c;
+  const double* L2 = Y2p.p;
+  int64_t k2 = N2;
+  bool q2_id = true;
+  if (N2 > R1) {
+    TK_TRY(orth_rows(ctx, R1, N2, Y2p.p, L2b, Q2c, &k2));
+    L2 = L2b.p;
+    q2_id = false;
+  }
+  // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
+  DevBuf W, V2, Vt, lam;
+  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, V2, Vt, lam));
+  DevBuf sig1, scr;
+  TK_TRY(sig1.get(ctx, k2));
+  TK_TRY(scr.get(ctx, 16));
+  int* info1 = (int*)scr.p;
+  double* dinfo1 = scr.p + 2;  // [norm, delta, discarded]
+  int* info2 = (int*)(scr.p + 6);
+  double* dinfo2 = scr.p + 8;
+  TK_TRY(tk_rank_select(ctx, (int)k2, lam.p, sig1.p, tol, nullptr, rmax, kDropThr, info1, dinfo1));
+  int hi1[2];
+  double hd1[3];
+  TK_TRY(sync_read(ctx, hi1, info1, sizeof(hi1)));
+  TK_TRY(sync_read(ctx, hd1, dinfo1, sizeof(hd1)));
+  if (!std::isfinite(hd1[0])) {
+    ctx->err = "tk_round: non-finite norm";
+    return TK_ENUMERIC;
+  }
+  if (norm_out) *norm_out = hd1[0];
+  if (hd1[0] == 0.0) {
+    if (sigma1_out) memset(sigma1_out, 0, sizeof(double) * R1);
+    if (sigma2_out) memset(sigma2_out, 0, sizeof(double) * R2);
+    if (discarded_out) discarded_out[0] = discarded_out[1] = 0.0;
+    return set_zero_tt(ctx, x);
+  }
+  const int64_t r1 = hi1[0];
+  if (sigma1_out) {
+    std::vector<double> s(k2);
+    TK_TRY(sync_read(ctx, s.data(), sig1.p, sizeof(double) * k2));
+    for (int64_t i = 0; i < R1; i++) sigma1_out[i] = i < k2 ? s[i] : 0.0;
+  }
+  // U1_new = W V2[:, :r1] diag(1/sig)  -> x->U1 (n_x x r1)
+  {
+    DevBuf F1;
+    TK_TRY(F1.get(ctx, k2 * r1));
+    TK_TRY(tk_col_scale(ctx, k2, r1, V2.p, k2, F1.p, r1, sig1.p, 1));
+    TK_TRY(tk_dgemm(ctx, false, false, n_x, r1, k2, 1.0, W.p, k2, F1.p, r1, 0.0, x->U1, r1));
+  }
+  W.release();
+  // C = (Vt[:, :r1] diag(sig))^T Q2   (r1 x N2)
+  DevBuf S1, C;
+  TK_TRY(S1.get(ctx, k2 * r1));
+  TK_TRY(tk_col_scale(ctx, k2, r1, Vt.p, k2, S1.p, r1, sig1.p, 0));
+  TK_TRY(C.get(ctx, r1 * N2));
+  if (q2_id) {
+    TK_TRY(tk_transpose(ctx, k2, r1, S1.p, r1, C.p, N2));  // k2 == N2
+  } else {
+    TK_TRY(tk_dgemm(ctx, true, true, r1, N2, k2, 1.0, S1.p, r1, Q2c.p, k2, 0.0, C.p, N2));
+  }
+  // ---- step E: SVD of C as (r1 n_xi) x k3, time bond truncation
+  DevBuf W2, V22, Vt2, lam2;
+  const int64_t M2 = r1 * n_xi;
+  TK_TRY(svd_two_pass(ctx, M2, k3, C.p, nullptr, k3, W2, V22, Vt2, lam2));
+  DevBuf sig2;
+  TK_TRY(sig2.get(ctx, k3));
+  TK_TRY(tk_rank_select(ctx, (int)k3, lam2.p, sig2.p, tol, dinfo1 + 1, rmax, kDropThr, info2,
+                        dinfo2));
+  int hi2[2];
+  double hd2[3];
+  TK_TRY(sync_read(ctx, hi2, info2, sizeof(hi2)));
+  TK_TRY(sync_read(ctx, hd2, dinfo2, sizeof(hd2)));
+  const int64_t r2 = hi2[0];
+  if (sigma2_out) {
+    std::vector<double> s(k3);
+    TK_TRY(sync_read(ctx, s.data(), sig2.p, sizeof(double) * k3));
+    for (int64_t i = 0; i < R2; i++) sigma2_out[i] = i < k3 ? s[i] : 0.0;
+  }
+  if (discarded_out) {
+    discarded_out[0] = hd1[2];
+    discarded_out[1] = hd2[2];
+  }
+  // U2_new = W2 V22[:, :r2] diag(1/sig2) -> x->U2 ((r1 n_xi) x r2)
+  {
+    DevBuf F2;
+    TK_TRY(F2.get(ctx, k3 * r2));
+    TK_TRY(tk_col_scale(ctx, k3, r2, V22.p, k3, F2.p, r2, sig2.p, 1));
+    TK_TRY(tk_dgemm(ctx, false, false, M2, r2, k3, 1.0, W2.p, k3, F2.p, r2, 0.0, x->U2, r2));
+  }
+  // U3_new = (Vt2[:, :r2] diag(sig2))^T Q3   (r2 x n_t)
+  {
+    DevBuf S2;
+    TK_TRY(S2.get(ctx, k3 * r2));
+    TK_TRY(tk_col_scale(ctx, k3, r2, Vt2.p, k3, S2.p, r2, sig2.p, 0));
+    if (q3_id) {
+      TK_TRY(tk_transpose(ctx, k3, r2, S2.p, r2, x->U3, n_t));  // k3 == n_t
+    } else {
+      TK_TRY(tk_dgemm(ctx, true, true, r2, n_t, k3, 1.0, S2.p, r2, Q3c.p, k3, 0.0, x->U3, n_t));
+    }
+  }
+  x->r1 = r1;
+  x->r2 = r2;
+  TK_CUDA_TRY(ctx, cudaGetLastError());
+  return TK_OK;
+}
+
+// ============================================================================ dot / norm
+static int same_modes(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, const char* who) {
+  if (x->n_x != y->n_x || x->n_xi != y->n_xi || x->n_t != y->n_t) {
+    ctx->err = std::string(who) + ": mode sizes differ";
+    return TK_ESHAPE;
+  }
+  return TK_OK;
+}
+
+static int dot_impl(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out, int take_sqrt) {
+  const int64_t n_x = x->n_x, n_xi = x->n_xi, n_t = x->n_t;
+  const int64_t a1 = x->r1, a2 = x->r2, b1 = y->r1, b2 = y->r2;
+  DevBuf W1, Tm, W2, W3;
+  TK_TRY(W1.get(ctx, a1 * b1));
+  TK_TRY(tk_dgemm(ctx, true, false, a1, b1, n_x, 1.0, x->U1, a1, y->U1, b1, 0.0, W1.p, b1));
+  TK_TRY(Tm.get(ctx, a1 * n_xi * b2));
+  TK_TRY(tk_dgemm(ctx, false, false, a1, n_xi * b2, b1, 1.0, W1.p, b1, y->U2, n_xi * b2, 0.0,
+                  Tm.p, n_xi * b2));
+  TK_TRY(W2.get(ctx, a2 * b2));
+  TK_TRY(tk_dgemm(ctx, true, false, a2, b2, a1 * n_xi, 1.0, x->U2, a2, Tm.p, b2, 0.0, W2.p, b2));
+  TK_TRY(W3.get(ctx, a2 * b2));
+  TK_TRY(tk_dgemm(ctx, false, true, a2, b2, n_t, 1.0, x->U3, n_t, y->U3, n_t, 0.0, W3.p, b2));
+  TK_TRY(tk_dot_final(ctx, a2 * b2, W2.p, W3.p, out, take_sqrt));
+  return TK_OK;
+}
+
+extern "C" int tk_dot(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out_dev) {
+  if (!ctx || !out_dev) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_dot(x)"));
+  TK_TRY(check_tt(ctx, y, "tk_dot(y)"));
+  TK_TRY(same_modes(ctx, x, y, "tk_dot"));
+  return dot_impl(ctx, x, y, out_dev, 0);
+}
+
+extern "C" int tk_norm(tk_ctx* ctx, const tk_tt* x, double* out_dev) {
+  if (!ctx || !out_dev) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_norm"));
+  return dot_impl(ctx, x, x, out_dev, 1);
+}
+
+// ============================================================================ axpby / scale
+extern "C" int tk_axpby(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
+                        const tk_tt* y, tk_tt* z) {
+  if (!ctx || !a_dev || !b_dev) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_axpby(x)"));
+  TK_TRY(check_tt(ctx, y, "tk_axpby(y)"));
+  TK_TRY(same_modes(ctx, x, y, "tk_axpby"));
+  if (!z || !z->U1 || !z->U2 || !z->U3) {
+    ctx->err = "tk_axpby: null output";
+    return TK_EARG;
+  }
+  TK_TRY(same_modes(ctx, x, z, "tk_axpby(z)"));
+  if (x->r1 + y->r1 > z->cap1 || x->r2 + y->r2 > z->cap2) {
+    ctx->err = "tk_axpby: output capacity < rank sums";
+    return TK_ECAP;
+  }
+  TK_TRY(tk_axpby_cores(ctx, a_dev, x, b_dev, y, z));
+  z->r1 = x->r1 + y->r1;
+  z->r2 = x->r2 + y->r2;
+  return TK_OK;
+}
+
+extern "C" int tk_axpby_host(tk_ctx* ctx, double a, const tk_tt* x, double b, const tk_tt* y,
+                             tk_tt* z) {
+  if (!ctx) return TK_EARG;
+  DevBuf s;
+  TK_TRY(s.get(ctx, 2));
+  TK_TRY(tk_set_scalar(ctx, s.p, a));
+  TK_TRY(tk_set_scalar(ctx, s.p + 1, b));
+  return tk_axpby(ctx, s.p, x, s.p + 1, y, z);
+}
+
+extern "C" int tk_scale(tk_ctx* ctx, tk_tt* x, const double* s_dev, int invert) {
+  if (!ctx || !s_dev) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_scale"));
+  return tk_scale_rows(ctx, x->U3, x->r2 * x->n_t, s_dev, invert);
+}
+
+// ============================================================================ GMRES cycle
+namespace {
+
+// A TT whose buffers are owned by the library (stream-ordered pool).
+struct OwnedTT {
+  tk_tt t{};
+  DevBuf b1, b2, b3;
+  int make(tk_ctx* ctx, int64_t n_x, int64_t n_xi, int64_t n_t, int64_t c1, int64_t c2) {
+    t.n_x = n_x;
+    t.n_xi = n_xi;
+    t.n_t = n_t;
+    t.cap1 = c1;
+    t.cap2 = c2;
+    t.r1 = c1;
+    t.r2 = c2;
+    TK_TRY(b1.get(ctx, n_x * c1));
+    TK_TRY(b2.get(ctx, c1 * n_xi * c2));
+    TK_TRY(b3.get(ctx, c2 * n_t));
+    t.U1 = b1.p;
+    t.U2 = b2.p;
+    t.U3 = b3.p;
+    return TK_OK;
+  }
+};
+
+int clone_tt(tk_ctx* ctx, const tk_tt* src, OwnedTT& dst) {
+  TK_TRY(dst.make(ctx, src->n_x, src->n_xi, src->n_t, src->r1, src->r2));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U1, src->U1, sizeof(double) * src->n_x * src->r1,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U2, src->U2,
+                                   sizeof(double) * src->r1 * src->n_xi * src->r2,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U3, src->U3, sizeof(double) * src->r2 * src->n_t,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  return TK_OK;
+}
+
+}  // namespace
+
+extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps,
+                              double tol, double* history_out, int* steps_done,
+                              double* explicit_out, double* step_ms_out) {
+  if (!ctx || !op || !history_out || !steps_done || steps < 1) return TK_EARG;
+  TK_TRY(check_tt(ctx, b, "tk_gmres_cycle(b)"));
+  if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t) {
+    ctx->err = "tk_gmres_cycle: b mode sizes differ from the operator's";
+    return TK_ESHAPE;
+  }
+  const int64_t n_x = b->n_x, n_xi = b->n_xi, n_t = b->n_t;
+  const int T = op->T;
+  DevBuf sc;  // device scalars: [beta, hn, nav, h(0..steps), negh(0..steps), one]
+  TK_TRY(sc.get(ctx, 4 + 2 * (steps + 1)));
+  double* d_beta = sc.p;
+  double* d_hn = sc.p + 1;
+  double* d_nav = sc.p + 2;
+  double* d_h = sc.p + 3;
+  double* d_negh = d_h + (steps + 1);
+  double* d_one = d_negh + (steps + 1);
+  TK_TRY(tk_set_scalar(ctx, d_one, 1.0));
+
+  std::vector<std::unique_ptr<OwnedTT>> V;
+  V.emplace_back(new OwnedTT());
+  TK_TRY(clone_tt(ctx, b, *V[0]));
+  TK_TRY(tk_round(ctx, &V[0]->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_norm(ctx, &V[0]->t, d_beta));
+  double beta;
+  TK_TRY(sync_read(ctx, &beta, d_beta, sizeof(double)));
+  TK_TRY(tk_scale(ctx, &V[0]->t, d_beta, 1));
+  std::vector<double> H((size_t)(steps + 1) * steps, 0.0), cs, sn, g(steps + 1, 0.0);
+  g[0] = beta;
+  history_out[0] = beta;
+  int k_done = 0;
+  for (int k = 0; k < steps; k++) {
+    auto t0 = std::chrono::high_resolution_clock::now();
+    const tk_tt& vk = V[k]->t;
+    auto x = std::make_unique<OwnedTT>();
+    TK_TRY(x->make(ctx, n_x, n_xi, n_t, T * vk.r1, T * vk.r2));
+    TK_TRY(tk_apply_op(ctx, op, &vk, &x->t));
+    TK_TRY(tk_round(ctx, &x->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_norm(ctx, &x->t, d_nav));
+    for (int i = 0; i <= k; i++) {
+      TK_TRY(tk_dot(ctx, &x->t, &V[i]->t, d_h + i));
+      TK_TRY(tk_neg_scalar(ctx, d_h + i, d_negh + i));
+      auto z = std::make_unique<OwnedTT>();
+      TK_TRY(z->make(ctx, n_x, n_xi, n_t, x->t.r1 + V[i]->t.r1, x->t.r2 + V[i]->t.r2));
+      TK_TRY(tk_axpby(ctx, d_one, &x->t, d_negh + i, &V[i]->t,
+                      &z->t));
+      TK_TRY(tk_round(ctx, &z->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+      x = std::move(z);
+    }
+    TK_TRY(tk_norm(ctx, &x->t, d_hn));
+    std::vector<double> hcol(k + 1);
+    double hn, nav;
+    TK_TRY(sync_read(ctx, hcol.data(), d_h, sizeof(double) * (k + 1)));
+    TK_TRY(sync_read(ctx, &hn, d_hn, sizeof(double)));
+    TK_TRY(sync_read(ctx, &nav, d_nav, sizeof(double)));
+    // Givens update of column k of H-bar
+    std::vector<double> col(k + 2);
+    for (int i = 0; i <= k; i++) col[i] = hcol[i];
+    col[k + 1] = hn;
+    for (int i = 0; i < k; i++) {
+      double t0v = cs[i] * col[i] + sn[i] * col[i + 1];
+      col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+      col[i] = t0v;
+    }
+    double c = 1.0, s = 0.0;
+    if (col[k + 1] != 0.0) {
+      double r = std::hypot(col[k], col[k + 1]);
+      c = col[k] / r;
+      s = col[k + 1] / r;
+    }
+    cs.push_back(c);
+    sn.push_back(s);
+    col[k] = c * col[k] + s * col[k + 1];
+    col[k + 1] = 0.0;
+    for (int i = 0; i <= k + 1; i++) H[(size_t)i * steps + k] = col[i];
+    g[k + 1] = -s * g[k];
+    g[k] = c * g[k];
+    history_out[k + 1] = std::fabs(g[k + 1]);
+    k_done = k + 1;
+    bool breakdown = hn <= 1e-14 * nav;
+    if (!breakdown) {
+      TK_TRY(tk_scale(ctx, &x->t, d_hn, 1));
+      V.push_back(std::move(x));
+    }
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    auto t1 = std::chrono::high_resolution_clock::now();
+    if (step_ms_out) step_ms_out[k] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (breakdown) break;
+  }
+  *steps_done = k_done;
+  if (explicit_out) {
+    // y = R^{-1} g  (back substitution on the rotated H-bar)
+    std::vector<double> y(k_done, 0.0);
+    for (int i = k_done - 1; i >= 0; i--) {
+      double s = g[i];
+      for (int j = i + 1; j < k_done; j++) s -= H[(size_t)i * steps + j] * y[j];
+      y[i] = s / H[(size_t)i * steps + i];
+    }
+    auto z = std::make_unique<OwnedTT>();
+    TK_TRY(clone_tt(ctx, &V[0]->t, *z));
+    TK_TRY(tk_set_scalar(ctx, d_h, y[0]));
+    TK_TRY(tk_scale(ctx, &z->t, d_h, 0));
+    for (int i = 1; i < k_done; i++) {
+      auto z2 = std::make_unique<OwnedTT>();
+      TK_TRY(z2->make(ctx, n_x, n_xi, n_t, z->t.r1 + V[i]->t.r1, z->t.r2 + V[i]->t.r2));
+      TK_TRY(tk_axpby_host(ctx, 1.0, &z->t, y[i], &V[i]->t, &z2->t));
+      TK_TRY(tk_round(ctx, &z2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+      z = std::move(z2);
+    }
+    auto az = std::make_unique<OwnedTT>();
+    TK_TRY(az->make(ctx, n_x, n_xi, n_t, T * z->t.r1, T * z->t.r2));
+    TK_TRY(tk_apply_op(ctx, op, &z->t, &az->t));
+    auto r = std::make_unique<OwnedTT>();
+    TK_TRY(r->make(ctx, n_x, n_xi, n_t, b->r1 + az->t.r1, b->r2 + az->t.r2));
+    TK_TRY(tk_axpby_host(ctx, 1.0, b, -1.0, &az->t, &r->t));
+    TK_TRY(tk_round(ctx, &r->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_norm(ctx, &r->t, d_hn));
+    TK_TRY(sync_read(ctx, explicit_out, d_hn, sizeof(double)));
+  }
+  return TK_OK;
+}

@@ -1,0 +1,138 @@
+// Internal declarations of libttk (B200 / sm_100a, fp64).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ttk.h"
+
+struct tk_ctx {
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+  int device = 0;
+  // pinned host scratch for the few device->host reads (ranks, scalars)
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct tk_op {
+  tk_ctx* ctx = nullptr;
+  int T = 0;
+  int64_t n_x = 0, n_xi = 0, n_t = 0;
+  // device copies
+  int32_t* rowptr = nullptr;   // T * (n_x + 1), each term's rowptr offset into the global col/val
+  int32_t* col = nullptr;      // sum nnz
+  double* val = nullptr;       // sum nnz
+  int64_t* nnz_off = nullptr;  // T+1 (device), prefix offsets of each term's nnz
+  double* G = nullptr;         // T * n_xi * n_xi
+  int* band_kl = nullptr;      // T
+  int* band_ku = nullptr;      // T
+  int64_t* band_off = nullptr; // T+1 prefix offsets into band
+  double* band = nullptr;      // concatenated LAPACK band arrays
+  std::vector<int64_t> h_nnz;  // host copy of per-term nnz
+  int max_kl = 0, max_ku = 0;
+};
+
+// ----------------------------------------------------------------------------- errors
+#define TK_CUDA_TRY(ctx, call)                                                      \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(_e);              \
+      return TK_ECUDA;                                                              \
+    }                                                                               \
+  } while (0)
+
+#define TK_LAUNCH_CHECK(ctx)                                                        \
+  do {                                                                              \
+    (ctx)->launches++;                                                              \
+    cudaError_t _e = cudaGetLastError();                                            \
+    if (_e != cudaSuccess) {                                                        \
+      (ctx)->err = std::string("kernel launch: ") + cudaGetErrorString(_e);         \
+      return TK_ECUDA;                                                              \
+    }                                                                               \
+  } while (0)
+
+#define TK_TRY(expr)              \
+  do {                            \
+    int _s = (expr);              \
+    if (_s != TK_OK) return _s;   \
+  } while (0)
+
+// ----------------------------------------------------------------------------- memory
+int tk_alloc(tk_ctx* ctx, void** p, size_t bytes);  // stream-ordered (cudaMallocAsync)
+void tk_free(tk_ctx* ctx, void* p);                 // stream-ordered (cudaFreeAsync)
+
+// RAII scratch buffer on the context stream.
+struct DevBuf {
+  tk_ctx* ctx = nullptr;
+  double* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  int get(tk_ctx* c, size_t n_doubles) {
+    release();
+    ctx = c;
+    return tk_alloc(c, (void**)&p, (n_doubles ? n_doubles : 1) * sizeof(double));
+  }
+  void release() {
+    if (p) tk_free(ctx, p);
+    p = nullptr;
+  }
+};
+
+// ----------------------------------------------------------------------------- kernels (host wrappers)
+// Row-major fp64 GEMM on DMMA (mma.sync m8n8k4 f64):
+//   C[M x N] (ldc) = alpha * op(A) * op(B) + beta * C
+//   transA: A is stored K x M (lda) and op(A) = A^T; else A is M x K.
+//   transB: B is stored N x K (ldb) and op(B) = B^T; else B is K x N.
+//   sym: M == N and the product is symmetric (a Gram); only the upper triangle of tiles is
+//        computed and mirrored.  Split-K with a deterministic reduction is chosen internally.
+int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+             double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+             double beta, double* C, int64_t ldc, bool sym = false);
+
+// Symmetric eigen-decomposition by parallel cyclic two-sided Jacobi.
+//   A: n x n symmetric (device, row-major, ld = n), destroyed.
+//   lam: n eigenvalues sorted DESCENDING; V: n x n eigenvectors (columns), row-major.
+//   A rotation on (p,q) is skipped when |a_pq| <= max(abs_tol, rel_tol*sqrt(|a_pp a_qq|)).
+int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
+                  double rel_tol, int max_sweeps, int* sweeps_out);
+
+// Apply kernels
+int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1);
+int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
+                          double* Y2);
+int tk_launch_time_apply(tk_ctx* ctx, const tk_op* op, int r2, const double* U3, double* Y3);
+
+// small helpers (k_small.cu)
+int tk_col_scale(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd, const double* f, int mode);  // mode 0: *f, 1: /f
+int tk_row_scale(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd, const double* f, int mode);
+int tk_copy2d(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+              double* dst, int64_t ldd);
+int tk_fill(tk_ctx* ctx, double* dst, int64_t n, double v);
+int tk_eye(tk_ctx* ctx, double* dst, int64_t n);
+// Rank decision on device from eigenvalues lam (descending, n of them):
+//   sigma = sqrt(max(lam,0)) written to sig; info[0] = r (rule), info[1] = k (numerical dim
+//   sigma > kthr*sigma_0), dinfo[0] = ||sigma||, dinfo[1] = delta used, dinfo[2] = discarded.
+//   If delta_in < 0, delta = tol * ||sigma|| / sqrt(2) else delta = delta_in (device).
+int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
+                   const double* delta_dev_in, int64_t rmax, double kthr, int* info,
+                   double* dinfo);
+int tk_axpby_cores(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
+                   const tk_tt* y, tk_tt* z);
+int tk_scale_rows(tk_ctx* ctx, double* U3, int64_t n, const double* s_dev, int invert);
+int tk_dot_final(tk_ctx* ctx, int64_t n, const double* a, const double* b, double* out,
+                 int take_sqrt);
+int tk_set_scalar(tk_ctx* ctx, double* dst, double v);
+int tk_neg_scalar(tk_ctx* ctx, const double* src, double* dst);
+int tk_transpose(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 double* dst, int64_t ldd);
+int tk_symmetrize(tk_ctx* ctx, int64_t n, double* A);

@@ -1,0 +1,307 @@
+"""Thin ctypes binding of libttk (include/ttk.h).  Argument marshalling only: every step of
+the path runs in the library's CUDA kernels; there is no CPU fallback.  PyTorch provides
+device memory (the caller-owned TT core buffers) and the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libttk.so")
+
+TK_OK, TK_ESHAPE, TK_ECAP, TK_EARG, TK_ENUMERIC, TK_ECUDA = 0, -1, -2, -3, -4, -5
+_CODES = {TK_ESHAPE: "TK_ESHAPE", TK_ECAP: "TK_ECAP", TK_EARG: "TK_EARG",
+          TK_ENUMERIC: "TK_ENUMERIC", TK_ECUDA: "TK_ECUDA"}
+
+EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "tk_ctx_launch_count",
+            "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round", "tk_dot",
+            "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle"]
+
+
+class TkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class tk_tt(ctypes.Structure):
+    _fields_ = [("n_x", ctypes.c_int64), ("n_xi", ctypes.c_int64), ("n_t", ctypes.c_int64),
+                ("r1", ctypes.c_int64), ("r2", ctypes.c_int64),
+                ("cap1", ctypes.c_int64), ("cap2", ctypes.c_int64),
+                ("U1", ctypes.c_void_p), ("U2", ctypes.c_void_p), ("U3", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libttk.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"libttk.so not built at {_LIB_PATH}; run __graft_entry__.build()")
+    L = ctypes.CDLL(_LIB_PATH)
+    P, I64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    L.tk_version.restype = ctypes.c_char_p
+    L.tk_ctx_create.argtypes = [ctypes.POINTER(P), P]
+    L.tk_ctx_destroy.argtypes = [P]
+    L.tk_last_error.argtypes = [P]
+    L.tk_last_error.restype = ctypes.c_char_p
+    L.tk_ctx_launch_count.argtypes = [P]
+    L.tk_ctx_launch_count.restype = I64
+    L.tk_op_create.argtypes = [P, ctypes.POINTER(P), I, I64, I64, I64, PP, PP, PP, PP,
+                               ctypes.POINTER(I), ctypes.POINTER(I), PP]
+    L.tk_op_destroy.argtypes = [P]
+    L.tk_op_terms.argtypes = [P]
+    TTP = ctypes.POINTER(tk_tt)
+    DP = ctypes.POINTER(D)
+    L.tk_apply_op.argtypes = [P, P, TTP, TTP]
+    L.tk_round.argtypes = [P, TTP, D, I64, DP, DP, DP, DP]
+    L.tk_dot.argtypes = [P, TTP, TTP, P]
+    L.tk_norm.argtypes = [P, TTP, P]
+    L.tk_axpby.argtypes = [P, P, TTP, P, TTP, TTP]
+    L.tk_axpby_host.argtypes = [P, D, TTP, D, TTP, TTP]
+    L.tk_scale.argtypes = [P, TTP, P, I]
+    L.tk_gmres_cycle.argtypes = [P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
+    for name in EXPORTED:
+        if name not in ("tk_version", "tk_last_error", "tk_ctx_launch_count"):
+            getattr(L, name).restype = I
+    _lib = L
+    return L
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1906_06785_b200 needs a CUDA device (B200); no CPU fallback")
+
+
+class Context:
+    """A libttk context bound to the current torch CUDA stream."""
+
+    def __init__(self, stream: torch.cuda.Stream | None = None):
+        _require_cuda()
+        self.stream = stream or torch.cuda.current_stream()
+        self._h = ctypes.c_void_p()
+        rc = lib().tk_ctx_create(ctypes.byref(self._h), ctypes.c_void_p(self.stream.cuda_stream))
+        if rc != TK_OK:
+            raise TkError(rc, "tk_ctx_create failed")
+
+    def check(self, rc: int):
+        if rc != TK_OK:
+            raise TkError(rc, lib().tk_last_error(self._h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(lib().tk_ctx_launch_count(self._h))
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().tk_ctx_destroy(self._h)
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+class TT:
+    """A 3-core tensor train in caller-owned device buffers (layouts of include/ttk.h)."""
+
+    def __init__(self, n_x, n_xi, n_t, r1, r2, cap1=None, cap2=None, device="cuda"):
+        self.n_x, self.n_xi, self.n_t = int(n_x), int(n_xi), int(n_t)
+        self.r1, self.r2 = int(r1), int(r2)
+        self.cap1 = int(cap1 if cap1 is not None else r1)
+        self.cap2 = int(cap2 if cap2 is not None else r2)
+        dt = torch.float64
+        self.b1 = torch.empty(self.n_x * self.cap1, dtype=dt, device=device)
+        self.b2 = torch.empty(self.cap1 * self.n_xi * self.cap2, dtype=dt, device=device)
+        self.b3 = torch.empty(self.cap2 * self.n_t, dtype=dt, device=device)
+
+    @classmethod
+    def from_cores(cls, u1, u2, u3, cap1=None, cap2=None, non_blocking=False):
+        n_x, r1 = u1.shape
+        _, n_xi, r2 = u2.shape
+        n_t = u3.shape[1]
+        t = cls(n_x, n_xi, n_t, r1, r2, cap1, cap2)
+        for buf, src in ((t.b1, u1), (t.b2, u2), (t.b3, u3)):
+            src_t = torch.as_tensor(np.ascontiguousarray(src) if isinstance(src, np.ndarray) else src,
+                                    dtype=torch.float64)
+            buf[: src_t.numel()].copy_(src_t.reshape(-1), non_blocking=non_blocking)
+        return t
+
+    @property
+    def U1(self):
+        return self.b1[: self.n_x * self.r1].view(self.n_x, self.r1)
+
+    @property
+    def U2(self):
+        return self.b2[: self.r1 * self.n_xi * self.r2].view(self.r1, self.n_xi, self.r2)
+
+    @property
+    def U3(self):
+        return self.b3[: self.r2 * self.n_t].view(self.r2, self.n_t)
+
+    @property
+    def ranks(self):
+        return self.r1, self.r2
+
+    def cores_numpy(self):
+        return (self.U1.cpu().numpy().copy(), self.U2.cpu().numpy().copy(),
+                self.U3.cpu().numpy().copy())
+
+    def struct(self) -> tk_tt:
+        return tk_tt(self.n_x, self.n_xi, self.n_t, self.r1, self.r2, self.cap1, self.cap2,
+                     self.b1.data_ptr(), self.b2.data_ptr(), self.b3.data_ptr())
+
+    def _update(self, s: tk_tt):
+        self.r1, self.r2 = int(s.r1), int(s.r2)
+
+
+class Operator:
+    """Device copy of A = sum_k T_k (x) G_k (x) K_k (tk_op_create).
+
+    `terms` is any sequence of objects with attributes K (CSR with indptr/indices/data),
+    G (n_xi x n_xi array), kl, ku, band ((kl+ku+1) x n_t LAPACK band array)."""
+
+    def __init__(self, n_x, n_xi, n_t, terms, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.n_x, self.n_xi, self.n_t = int(n_x), int(n_xi), int(n_t)
+        T = len(terms)
+        self.T = T
+        keep = []
+        rp, cl, vl, gg, bd = [(ctypes.c_void_p * T)() for _ in range(5)]
+        kl = (ctypes.c_int * T)()
+        ku = (ctypes.c_int * T)()
+        for k, t in enumerate(terms):
+            a_rp = np.ascontiguousarray(t.K.indptr, dtype=np.int32)
+            a_cl = np.ascontiguousarray(t.K.indices, dtype=np.int32)
+            a_vl = np.ascontiguousarray(t.K.data, dtype=np.float64)
+            a_g = np.ascontiguousarray(t.G, dtype=np.float64)
+            # LAPACK band storage is column-major: element (row, col) at col*ldab + row
+            a_b = np.asfortranarray(np.asarray(t.band, dtype=np.float64)).ravel(order="F")
+            keep += [a_rp, a_cl, a_vl, a_g, a_b]
+            rp[k], cl[k], vl[k] = a_rp.ctypes.data, a_cl.ctypes.data, a_vl.ctypes.data
+            gg[k], bd[k] = a_g.ctypes.data, a_b.ctypes.data
+            kl[k], ku[k] = int(t.kl), int(t.ku)
+        self._h = ctypes.c_void_p()
+        self.ctx.check(lib().tk_op_create(self.ctx._h, ctypes.byref(self._h), T, self.n_x,
+                                          self.n_xi, self.n_t, rp, cl, vl, gg, kl, ku, bd))
+
+    @classmethod
+    def from_kronsum(cls, op, ctx=None):
+        return cls(op.n_x, op.n_xi, op.n_t, op.terms, ctx)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().tk_op_destroy(self._h)
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------------------- the path
+def tt_apply_op(op: Operator, x: TT, out: TT | None = None) -> TT:
+    """y = A x (tk_apply_op); y ranks (T r1, T r2)."""
+    ctx = op.ctx
+    y = out or TT(x.n_x, x.n_xi, x.n_t, op.T * x.r1, op.T * x.r2)
+    xs, ys = x.struct(), y.struct()
+    ctx.check(lib().tk_apply_op(ctx._h, op._h, ctypes.byref(xs), ctypes.byref(ys)))
+    y._update(ys)
+    return y
+
+
+@dataclass
+class RoundInfo:
+    ranks: tuple
+    sigma1: np.ndarray
+    sigma2: np.ndarray
+    discarded: tuple
+    norm: float
+
+
+def tt_round(x: TT, tol: float, rmax: int = 0, ctx: Context | None = None,
+             want_info: bool = False):
+    """In-place TT rounding T_tol (tk_round).  Returns x (and a RoundInfo)."""
+    ctx = ctx or default_context()
+    s = x.struct()
+    D = ctypes.c_double
+    if want_info:
+        s1 = (D * max(x.r1, 1))()
+        s2 = (D * max(x.r2, 1))()
+        disc = (D * 2)()
+        nrm = D()
+        ctx.check(lib().tk_round(ctx._h, ctypes.byref(s), float(tol), int(rmax), s1, s2, disc,
+                                 ctypes.byref(nrm)))
+    else:
+        ctx.check(lib().tk_round(ctx._h, ctypes.byref(s), float(tol), int(rmax), None, None, None,
+                                 None))
+    x._update(s)
+    if want_info:
+        return x, RoundInfo((x.r1, x.r2), np.array(s1[:]), np.array(s2[:]), (disc[0], disc[1]),
+                            nrm.value)
+    return x
+
+
+def tt_dot(x: TT, y: TT, ctx: Context | None = None, out: torch.Tensor | None = None):
+    """<x, y>_F into a 1-element device tensor (tk_dot); .item() syncs."""
+    ctx = ctx or default_context()
+    out = out if out is not None else torch.empty(1, dtype=torch.float64, device="cuda")
+    xs, ys = x.struct(), y.struct()
+    ctx.check(lib().tk_dot(ctx._h, ctypes.byref(xs), ctypes.byref(ys), ctypes.c_void_p(out.data_ptr())))
+    return out
+
+
+def tt_norm(x: TT, ctx: Context | None = None, out: torch.Tensor | None = None):
+    ctx = ctx or default_context()
+    out = out if out is not None else torch.empty(1, dtype=torch.float64, device="cuda")
+    xs = x.struct()
+    ctx.check(lib().tk_norm(ctx._h, ctypes.byref(xs), ctypes.c_void_p(out.data_ptr())))
+    return out
+
+
+def tt_axpby(a, x: TT, b, y: TT, ctx: Context | None = None, out: TT | None = None) -> TT:
+    """z = a x + b y (tk_axpby / tk_axpby_host); a, b floats or 1-element device tensors."""
+    ctx = ctx or default_context()
+    z = out or TT(x.n_x, x.n_xi, x.n_t, x.r1 + y.r1, x.r2 + y.r2)
+    xs, ys, zs = x.struct(), y.struct(), z.struct()
+    if isinstance(a, torch.Tensor) or isinstance(b, torch.Tensor):
+        at = a if isinstance(a, torch.Tensor) else torch.tensor([float(a)], dtype=torch.float64, device="cuda")
+        bt = b if isinstance(b, torch.Tensor) else torch.tensor([float(b)], dtype=torch.float64, device="cuda")
+        ctx.check(lib().tk_axpby(ctx._h, ctypes.c_void_p(at.data_ptr()), ctypes.byref(xs),
+                                 ctypes.c_void_p(bt.data_ptr()), ctypes.byref(ys), ctypes.byref(zs)))
+    else:
+        ctx.check(lib().tk_axpby_host(ctx._h, float(a), ctypes.byref(xs), float(b), ctypes.byref(ys),
+                                      ctypes.byref(zs)))
+    z._update(zs)
+    return z
+
+
+def gmres_cycle(op: Operator, b: TT, steps: int = 20, tol: float = 1e-6):
+    """One low-rank GMRES cycle (tk_gmres_cycle).  Returns dict(history, steps, explicit, step_ms)."""
+    ctx = op.ctx
+    D = ctypes.c_double
+    hist = (D * (steps + 1))()
+    ms = (D * steps)()
+    done = ctypes.c_int()
+    expl = D()
+    bs = b.struct()
+    ctx.check(lib().tk_gmres_cycle(ctx._h, op._h, ctypes.byref(bs), int(steps), float(tol), hist,
+                                   ctypes.byref(done), ctypes.byref(expl), ms))
+    k = done.value
+    return dict(history=np.array(hist[: k + 1]), steps=k, explicit=expl.value,
+                step_ms=np.array(ms[:k]))

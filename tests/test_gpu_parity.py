@@ -1,0 +1,220 @@
+"""GPU-vs-oracle parity through the C ABI (libttk.so) — the parity tests proper.
+
+Bars (BASELINE.json north_star):
+  apply      : exact arithmetic path, rel. error <= 1e-13 per core
+  round      : relative Frobenius error of the reconstructed tensor <= 1e-10, singular values
+               |s_gpu - s_orc| <= 1e-10 s_1, identical ranks away from ties (R5)
+  dot / norm : <= 1e-12 relative;  axpby exact
+  GMRES (c5) : residual history within 1e-8 relative (to beta)
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1906_06785_b200 as ttk  # noqa: E402
+from oracle import tt as otT  # noqa: E402
+from oracle.gmres import gmres_cycle as o_gmres  # noqa: E402
+from synth.configs import CONFIGS  # noqa: E402
+from synth.operator import build_operator, random_operator  # noqa: E402
+from synth.tt import make_input_tt, make_rhs_tt, random_tt  # noqa: E402
+
+TOL_TENSOR = 1e-10
+TOL_SIGMA = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def tt_diff_rel(a, b):
+    """||a - b||_F / ||b||_F for TTs too large to densify: orthogonalise the TT a + (-b)
+    with the oracle at tol 0 and read the norm off the last core (hard part 4)."""
+    d = otT.round_tt(otT.axpby(1.0, a, -1.0, b), 0.0)
+    nb = otT.round_tt(b, 0.0)
+    return float(np.linalg.norm(d[2]) / max(np.linalg.norm(nb[2]), 1e-300))
+
+
+def ranks_excused(sig, delta, r_gpu, r_orc, rmax):
+    """DESIGN.md R5: a rank mismatch is a tie if the tail at the boundary is within 1e-10 ||x||
+    of delta, or if rmax binds and the singular values straddling it are within 1e-10 s_1."""
+    if r_gpu == r_orc:
+        return True
+    nrm = np.linalg.norm(sig)
+    lo = min(r_gpu, r_orc)
+    tail = np.linalg.norm(sig[lo:])
+    if abs(tail - delta) <= 1e-10 * nrm:
+        return True
+    if rmax and max(r_gpu, r_orc) == rmax and abs(sig[rmax - 1] - sig[min(rmax, len(sig) - 1)]) <= 1e-10 * sig[0]:
+        return True
+    return False
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return ttk.default_context()
+
+
+def gpu_op(op, ctx):
+    return ttk.Operator.from_kronsum(op, ctx)
+
+
+# ----------------------------------------------------------------------------- apply
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_apply_parity_configs(name, ctx):
+    cfg = CONFIGS[name]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    y_o = otT.apply_op(op, x)
+    y_g = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x)).cores_numpy()
+    for a, b in zip(y_g, y_o):
+        assert a.shape == b.shape
+        assert rel(a, b) <= 1e-13
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_apply_parity_random_ragged(seed, ctx):
+    rng = np.random.default_rng(seed)
+    n_x = int(rng.integers(1, 300))
+    n_xi, n_t = int(rng.integers(1, 12)), int(rng.integers(1, 40))
+    T = int(rng.integers(1, 5))
+    r1 = [1, 3, 17, 33, 65, 97][seed]
+    r2 = int(rng.integers(1, 9))
+    op = random_operator(rng, n_x, n_xi, n_t, T, density=0.05, max_band=3)
+    x = random_tt(rng, n_x, n_xi, n_t, r1, r2)
+    y_o = otT.apply_op(op, x)
+    y_g = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x)).cores_numpy()
+    for a, b in zip(y_g, y_o):
+        assert rel(a, b) <= 1e-13
+
+
+def test_apply_capacity_and_shape_errors(ctx):
+    rng = np.random.default_rng(3)
+    op = random_operator(rng, 10, 3, 4, 2)
+    g = gpu_op(op, ctx)
+    x = ttk.TT.from_cores(*random_tt(rng, 10, 3, 4, 2, 2))
+    small = ttk.TT(10, 3, 4, 2, 2)
+    with pytest.raises(ttk.TkError) as e:
+        ttk.tt_apply_op(g, x, out=small)
+    assert e.value.code == -2
+    bad = ttk.TT.from_cores(*random_tt(rng, 11, 3, 4, 2, 2))
+    with pytest.raises(ttk.TkError) as e:
+        ttk.tt_apply_op(g, bad)
+    assert e.value.code == -1
+
+
+# ----------------------------------------------------------------------------- round
+def check_round(y_cores, tol, rmax, ctx, dense=True):
+    o, info = otT.round_tt(y_cores, tol, rmax, return_info=True)
+    g = ttk.TT.from_cores(*y_cores)
+    g, ginfo = ttk.tt_round(g, tol, rmax, ctx, want_info=True)
+    gc = g.cores_numpy()
+    assert ranks_excused(info["sigma1"], info["delta"], ginfo.ranks[0], info["ranks"][0], rmax)
+    k = min(len(info["sigma1"]), len(ginfo.sigma1))
+    assert np.max(np.abs(ginfo.sigma1[:k] - info["sigma1"][:k])) <= TOL_SIGMA * info["sigma1"][0]
+    if ginfo.ranks == info["ranks"]:
+        k2 = min(len(info["sigma2"]), len(ginfo.sigma2))
+        assert np.max(np.abs(ginfo.sigma2[:k2] - info["sigma2"][:k2])) <= TOL_SIGMA * max(info["sigma2"][0], 1e-300)
+        err = rel(otT.full(gc), otT.full(o)) if dense else tt_diff_rel(gc, o)
+        assert err <= TOL_TENSOR, err
+    assert ginfo.norm == pytest.approx(info["norm"], rel=1e-12)
+    # invariants of the GPU output
+    u1, u2, u3 = gc
+    assert np.max(np.abs(u1.T @ u1 - np.eye(u1.shape[1]))) <= 1e-10
+    m2 = u2.reshape(-1, u2.shape[2])
+    assert np.max(np.abs(m2.T @ m2 - np.eye(m2.shape[1]))) <= 1e-10
+    return ginfo, info
+
+
+@pytest.mark.parametrize("tol", [1e-10, 1e-6, 1e-3, 0.1])
+def test_round_parity_c1(tol, ctx):
+    cfg = CONFIGS["c1"]
+    op = build_operator(cfg)
+    y = otT.apply_op(op, make_input_tt(cfg, op.n_xi))
+    check_round(y, tol, 0, ctx)
+
+
+def test_round_parity_c2(ctx):
+    cfg = CONFIGS["c2"]
+    op = build_operator(cfg)
+    y = otT.apply_op(op, make_input_tt(cfg, op.n_xi))
+    check_round(y, cfg.tol, cfg.rmax, ctx, dense=False)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_round_parity_random(seed, ctx):
+    rng = np.random.default_rng(500 + seed)
+    n = [int(v) for v in rng.integers(1, 30, size=3)]
+    r1, r2 = [int(v) for v in rng.integers(1, 24, size=2)]
+    x = random_tt(rng, *n, r1, r2)
+    tol = [1e-12, 1e-8, 1e-4, 0.2][seed % 4]
+    check_round(x, tol, 0, ctx)
+
+
+def test_round_rank_one_and_zero(ctx):
+    rng = np.random.default_rng(9)
+    x = random_tt(rng, 5, 4, 3, 1, 1)
+    check_round(x, 1e-8, 0, ctx)
+    z = (np.zeros((6, 2)), np.zeros((2, 3, 2)), np.zeros((2, 5)))
+    g, info = ttk.tt_round(ttk.TT.from_cores(*z), 1e-3, 0, ctx, want_info=True)
+    assert g.ranks == (1, 1) and info.norm == 0.0
+    assert not np.any(np.concatenate([c.ravel() for c in g.cores_numpy()]))
+
+
+def test_round_bad_tol(ctx):
+    rng = np.random.default_rng(1)
+    g = ttk.TT.from_cores(*random_tt(rng, 4, 3, 3, 2, 2))
+    with pytest.raises(ttk.TkError) as e:
+        ttk.tt_round(g, -1.0, 0, ctx)
+    assert e.value.code == -3
+
+
+# ----------------------------------------------------------------------------- dot / axpby
+@pytest.mark.parametrize("seed", range(5))
+def test_dot_norm_axpby_parity(seed, ctx):
+    rng = np.random.default_rng(70 + seed)
+    n = [int(v) for v in rng.integers(1, 200, size=3)]
+    x = random_tt(rng, *n, int(rng.integers(1, 20)), int(rng.integers(1, 20)))
+    y = random_tt(rng, *n, int(rng.integers(1, 20)), int(rng.integers(1, 20)))
+    gx, gy = ttk.TT.from_cores(*x), ttk.TT.from_cores(*y)
+    assert ttk.tt_dot(gx, gy, ctx).item() == pytest.approx(otT.dot(x, y), rel=1e-12, abs=1e-12)
+    assert ttk.tt_norm(gx, ctx).item() == pytest.approx(otT.norm(x), rel=1e-12)
+    z = ttk.tt_axpby(1.5, gx, -0.25, gy, ctx)
+    zo = otT.axpby(1.5, x, -0.25, y)
+    for a, b in zip(z.cores_numpy(), zo):
+        assert np.array_equal(a, b)
+    a_dev = torch.tensor([2.0], dtype=torch.float64, device="cuda")
+    z2 = ttk.tt_axpby(a_dev, gx, 1.0, gy, ctx)
+    assert np.array_equal(z2.cores_numpy()[2], otT.axpby(2.0, x, 1.0, y)[2])
+
+
+# ----------------------------------------------------------------------------- c3 (large)
+@pytest.mark.slow
+def test_round_parity_c3(ctx):
+    cfg = CONFIGS["c3"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    y = otT.apply_op(op, x)
+    yg = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x))
+    for a, b in zip(yg.cores_numpy(), y):
+        assert rel(a, b) <= 1e-13
+    check_round(y, cfg.tol, cfg.rmax, ctx, dense=False)
+
+
+# ----------------------------------------------------------------------------- GMRES c5
+def test_gmres_cycle_parity_c5(ctx):
+    cfg = CONFIGS["c5"]
+    op = build_operator(cfg)
+    b = make_rhs_tt(cfg, op.n_xi)
+    ref = o_gmres(op, b, steps=cfg.gmres_steps, tol=cfg.tol)
+    res = ttk.gmres_cycle(gpu_op(op, ctx), ttk.TT.from_cores(*b), steps=cfg.gmres_steps, tol=cfg.tol)
+    assert res["steps"] == ref["steps"]
+    h, hr = res["history"], ref["history"]
+    assert np.max(np.abs(h - hr)) <= 1e-8 * hr[0], (h, hr)
+    assert res["explicit"] == pytest.approx(ref["explicit"], rel=1e-6, abs=1e-8 * hr[0])
