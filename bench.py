@@ -1,0 +1,353 @@
+"""Benchmark: TT apply + round (one "op") on one B200 per rank, fp64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Metric (BASELINE.json "metric"): TT apply+round ops/s, with
+the dominant kernel's roofline (FP64 tensor pipe or HBM) and the CPU oracle beside it.
+
+* a step = tk_apply_op + tk_round on the config's seeded input TT (inputs resident in HBM);
+* timed with CUDA events on the library's stream, barrier + synchronize on both sides,
+  max over ranks; multi-GPU = independent replicas (the path does not shard: DESIGN.md);
+* L2: c3/c4 inputs and intermediates are far larger than the 126 MB L2; for c1/c2 a 256 MB
+  buffer is written between timed steps (outside the per-step event brackets);
+* e2e: the same op through the public binding with HOST inputs: pinned H2D copy of the
+  input cores, apply + round, D2H of the rounded cores, all inside the timed region;
+* --impl reference: the CPU oracle (oracle/) timed on this host's cores on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "TT apply+round ops/s"
+UNIT = "ops/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default=os.environ.get("TTK_BENCH_CONFIG", "c3"))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--breakdown", action="store_true", help="per-phase times to stderr")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- dist helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def cpu_cores_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_oracle_op(op, x, cfg):
+    from oracle import tt as otT
+    t0 = time.perf_counter()
+    y = otT.apply_op(op, x)
+    t1 = time.perf_counter()
+    otT.round_tt(y, cfg.tol, cfg.rmax)
+    t2 = time.perf_counter()
+    return t2 - t0, t1 - t0, t2 - t1
+
+
+def run_reference(args, cfg, op, x):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    budget = 150.0
+    for _ in range(max(args.warmup, 0) if args.warmup <= 1 else 1):
+        time_oracle_op(op, x, cfg)  # warm-up (page-in, BLAS threads)
+    times = []
+    t_start = time.perf_counter()
+    for k in range(args.steps):
+        dt, _, _ = time_oracle_op(op, x, cfg)
+        times.append(dt)
+        if time.perf_counter() - t_start > budget:
+            break
+    total = sum(times)
+    v = len(times) / total
+    cores = cpu_cores_used()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg, op),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{len(times)} full {cfg.name} ops (apply+round), NumPy/SciPy "
+                                   f"OpenBLAS, {cores} threads; capped at ~{budget:.0f}s"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def workload_config(cfg, op):
+    return {"workload": f"{cfg.name}: apply+round", "n_x": op.n_x, "n_xi": op.n_xi, "n_t": op.n_t,
+            "terms": op.T, "ranks_in": list(cfg.ranks),
+            "ranks_grown": [op.T * cfg.ranks[0], op.T * cfg.ranks[1]], "tol": cfg.tol,
+            "rmax": cfg.rmax, "parallelism": "replicas",
+            "l2": "inputs+intermediates > L2" if cfg.name in ("c3", "c4") else "256MB flush between steps"}
+
+
+def run_ours(args, cfg, op, x):
+    import torch
+    import torch.distributed as tdist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        tdist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    import paper_1906_06785_b200 as ttk
+    from paper_1906_06785_b200 import ttk as ttkmod
+
+    stream = torch.cuda.current_stream()
+    ctx = ttk.default_context()
+    gop = ttk.Operator.from_kronsum(op, ctx)
+    xg = ttk.TT.from_cores(*x)
+    T = op.T
+    ycap = ttk.TT(op.n_x, op.n_xi, op.n_t, T * xg.r1, T * xg.r2)
+    flush = None
+    if cfg.name not in ("c3", "c4"):
+        flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    def step():
+        y = ttk.tt_apply_op(gop, xg, out=ycap)
+        ttk.tt_round(y, cfg.tol, cfg.rmax, ctx)
+        return y
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    L = ttkmod.lib()
+    L.tk_ctx_profile(ctx._h, 1)
+    launches0 = ctx.launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(float(i))
+            evs[i][0].record(stream)
+            y = step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    buf = __import__("ctypes").create_string_buffer(1 << 22)
+    nrec = L.tk_ctx_profile_dump(ctx._h, buf, len(buf))
+    L.tk_ctx_profile(ctx._h, 0)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        tdist.barrier()
+    ranks_out = y.ranks
+
+    # per-phase breakdown and the dominant kernel
+    phases = {}
+    for ln in buf.value.decode().splitlines():
+        cat, ms, fl, by = ln.split()
+        d = phases.setdefault(cat, [0, 0.0, 0.0, 0.0])
+        d[0] += 1
+        d[1] += float(ms)
+        d[2] += float(fl)
+        d[3] += float(by)
+    peaks, peak_kind = load_peaks()
+    fp64_peak = peaks["bf16_tflops"] * (45.0 / 2250.0)  # bf16 measured x nominal fp64/bf16 ratio
+    dom = max(phases.items(), key=lambda kv: kv[1][1]) if phases else None
+    roofline = None
+    if dom:
+        cat, (cnt, ms, fl, by) = dom
+        avg_ms = ms / cnt
+        if fl > 0 and (fl / by) > 6.0:
+            ach = fl / cnt / (avg_ms * 1e-3) / 1e12
+            roofline = {"kernel": cat, "bound": "tensor", "achieved": ach, "peak": fp64_peak,
+                        "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                        "peak_source": f"bf16 {peak_kind} {peaks['bf16_tflops']} x 45/2250 (fp64 DMMA nominal ratio)",
+                        "launches": cnt, "avg_ms": avg_ms, "share_of_step": ms / total_ms}
+        elif by > 0:
+            ach = by / cnt / (avg_ms * 1e-3) / 1e9
+            roofline = {"kernel": cat, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+                        "peak_source": peak_kind, "launches": cnt, "avg_ms": avg_ms,
+                        "share_of_step": ms / total_ms}
+        else:
+            roofline = {"kernel": cat, "bound": "latency", "achieved": None, "peak": None,
+                        "unit": None, "frac": None, "traffic": None, "launches": cnt,
+                        "avg_ms": avg_ms, "share_of_step": ms / total_ms}
+    spmm = phases.get("spmm_multi")
+    spmm_gbs = spmm[3] / (spmm[1] * 1e-3) / 1e9 if spmm else None
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if rank == 0 or world > 1:
+        pinned = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in x]
+        h2d = sum(p.numel() * 8 for p in pinned)
+        xe = ttk.TT(op.n_x, op.n_xi, op.n_t, cfg.ranks[0], cfg.ranks[1])
+        outs = [torch.empty(n, dtype=torch.float64).pin_memory()
+                for n in (op.n_x * T * cfg.ranks[0], T * cfg.ranks[0] * op.n_xi * T * cfg.ranks[1],
+                          T * cfg.ranks[1] * op.n_t)]
+        ee = []
+        d2h = 0
+        for i in range(max(1, min(args.steps, 5))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for buf_, src in zip((xe.b1, xe.b2, xe.b3), pinned):
+                buf_[: src.numel()].copy_(src.reshape(-1), non_blocking=True)
+            ye = ttk.tt_apply_op(gop, xe, out=ycap)
+            ttk.tt_round(ye, cfg.tol, cfg.rmax, ctx)
+            d2h = 0
+            for o, c in zip(outs, (ye.U1, ye.U2, ye.U3)):
+                o[: c.numel()].copy_(c.reshape(-1), non_blocking=True)
+                d2h += c.numel() * 8
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ee.append(e0.elapsed_time(e1))
+        e2e = {"value": world * 1000.0 / statistics.mean(ee), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": len(ee)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = cpu_cores_used()
+        times = []
+        t0 = time.perf_counter()
+        while True:
+            dt, ta, tr = time_oracle_op(op, x, cfg)
+            times.append(dt)
+            if time.perf_counter() - t0 > 10.0 or len(times) >= 5:
+                break
+        cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{len(times)} full {cfg.name} apply+round op(s) on the host (NumPy/SciPy "
+                         f"OpenBLAS {cores} threads), median {1000 * statistics.median(times):.0f} ms/op"}
+
+    if args.breakdown and rank == 0:
+        for cat, (cnt, ms, fl, by) in sorted(phases.items(), key=lambda kv: -kv[1][1]):
+            tf = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0
+            gb = by / (ms * 1e-3) / 1e9 if ms > 0 else 0
+            print(f"  {cat:18s} n={cnt:4d} {ms / args.steps:9.3f} ms/step  {tf:7.2f} TF/s  {gb:8.1f} GB/s",
+                  file=sys.stderr)
+        print(f"  step times ms: {[round(s, 3) for s in step_ms]}", file=sys.stderr)
+
+    if rank == 0:
+        ms_per_step = total_ms / args.steps
+        line = {
+            "metric": METRIC, "value": world * 1000.0 * args.steps / total_ms, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(cfg, op), "ranks_out": list(ranks_out),
+            "roofline": roofline, "spmm_gbs": spmm_gbs,
+            "phases_ms_per_step": {k: round(v[1] / args.steps, 4) for k, v in phases.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from synth.configs import CONFIGS
+    from synth.operator import build_operator
+    from synth.tt import make_input_tt
+    cfg = CONFIGS[args.config]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    if args.impl == "reference":
+        run_reference(args, cfg, op, x)
+    else:
+        run_ours(args, cfg, op, x)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,6 +68,13 @@ const char* tk_last_error(const tk_ctx* ctx);
 /* Number of kernels this context has launched since creation (for the bench's
  * "gpu_launches"). */
 int64_t tk_ctx_launch_count(const tk_ctx* ctx);
+/* Profiling: enable != 0 clears the record list and starts recording CUDA events around
+ * every kernel (tagged with its phase and its algorithmic flop and byte counts); 0 stops.
+ * tk_ctx_profile_dump synchronises the stream and writes one line per record,
+ * "<phase> <ms> <flops> <bytes>\n", into buf (truncated to len); returns the number of
+ * records. */
+int tk_ctx_profile(tk_ctx* ctx, int enable);
+int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len);
 
 /* Operator descriptor  A = sum_{k<T} T_k (x) G_k (x) K_k.
  *   K_k : n_x x n_x CSR, HOST arrays: rowptr[n_x+1] (int32), col[nnz_k] (int32, 0-based),

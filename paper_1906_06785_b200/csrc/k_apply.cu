@@ -29,38 +29,41 @@ __global__ void __launch_bounds__(256) spmm_multi_k(int64_t n_x, int T, int r,
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t R = (int64_t)T * r;
+  constexpr int CW = 32 * RPL;  // columns per chunk
   for (int64_t i = warp; i < n_x; i += nwarps) {
     double* yrow = Y1 + i * R;
     for (int k = 0; k < T; k++) {
       const int32_t* rp = rowptr + (int64_t)k * (n_x + 1);
       const int64_t base = nnz_off[k];
       const int beg = rp[i], end = rp[i + 1];
-      double acc[RPL];
+      for (int c0 = 0; c0 < r; c0 += CW) {
+        double acc[RPL];
 #pragma unroll
-      for (int u = 0; u < RPL; u++) acc[u] = 0.0;
-      for (int e0 = beg; e0 < end; e0 += 32) {
-        int myc = 0;
-        double myv = 0.0;
-        if (e0 + lane < end) {
-          myc = __ldg(col + base + e0 + lane);
-          myv = __ldg(val + base + e0 + lane);
-        }
-        const int cnt = min(32, end - e0);
-        for (int q = 0; q < cnt; q++) {
-          const int c = __shfl_sync(0xffffffffu, myc, q);
-          const double v = __shfl_sync(0xffffffffu, myv, q);
-          const double* urow = U1 + (int64_t)c * r;
+        for (int u = 0; u < RPL; u++) acc[u] = 0.0;
+        for (int e0 = beg; e0 < end; e0 += 32) {
+          int myc = 0;
+          double myv = 0.0;
+          if (e0 + lane < end) {
+            myc = __ldg(col + base + e0 + lane);
+            myv = __ldg(val + base + e0 + lane);
+          }
+          const int cnt = min(32, end - e0);
+          for (int q = 0; q < cnt; q++) {
+            const int c = __shfl_sync(0xffffffffu, myc, q);
+            const double v = __shfl_sync(0xffffffffu, myv, q);
+            const double* urow = U1 + (int64_t)c * r + c0;
 #pragma unroll
-          for (int u = 0; u < RPL; u++) {
-            const int cc = lane + 32 * u;
-            if (cc < r) acc[u] = fma(v, __ldg(urow + cc), acc[u]);
+            for (int u = 0; u < RPL; u++) {
+              const int cc = lane + 32 * u;
+              if (c0 + cc < r) acc[u] = fma(v, __ldg(urow + cc), acc[u]);
+            }
           }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < RPL; u++) {
-        const int cc = lane + 32 * u;
-        if (cc < r) yrow[(int64_t)k * r + cc] = acc[u];
+        for (int u = 0; u < RPL; u++) {
+          const int cc = lane + 32 * u;
+          if (c0 + cc < r) yrow[(int64_t)k * r + c0 + cc] = acc[u];
+        }
       }
     }
   }
@@ -127,12 +130,8 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
     TK_SPMM(3);
   else if (rpl == 4)
     TK_SPMM(4);
-  else if (rpl <= 8)
+  else
     TK_SPMM(8);
-  else {
-    ctx->err = "tk_apply_op: r1 > 256 not supported by spmm_multi";
-    return TK_EARG;
-  }
 #undef TK_SPMM
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;

@@ -290,6 +290,9 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
     partial = pbuf.p;
   }
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
+  const double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
+  const double bytes = 8.0 * ((double)M * K + (sym ? 0.0 : (double)K * N) + (double)M * N);
+  const int prof_id = tk_prof_begin(ctx, ctx->tag, flops, bytes);
   const bool AK = transA, BKm = !transB;
   // 16-byte vector path: contiguous dims even and 16-byte aligned bases
   bool v2 = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
@@ -316,5 +319,6 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
                                                    beta, sym ? 1 : 0);
     TK_LAUNCH_CHECK(ctx);
   }
+  tk_prof_end(ctx, prof_id);
   return TK_OK;
 }

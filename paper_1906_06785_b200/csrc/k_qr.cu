@@ -1,0 +1,190 @@
+// Blocked Householder QR of a square fp64 matrix, returning the explicit orthogonal Q.
+//
+// Used as PASS 1 of the two-pass Gram-Jacobi rounding: for the Gram
+// G = Z^T Z, Q from G = Q R is one step of orthogonal iteration, i.e. an exactly orthogonal
+// basis whose leading columns already follow the dominant eigenvectors; W = Z Q is then
+// graded enough that pass 2 (relative Jacobi on W^T W) converges in a few sweeps.  Only the
+// orthogonality of Q matters for accuracy (Householder: ||Q^T Q - I|| = O(eps)).
+//
+// Panel (width QB = 16) factorised by one CTA (LAPACK dgeqr2 + dlarft: reflectors v_c, tau_c
+// and the compact-WY factor T with H_1..H_QB = I - V T V^T); trailing update and the
+// backward accumulation of Q use the DMMA GEMM (tk_dgemm):
+//   A[j0:, j1:] -= V (T^T (V^T A[j0:, j1:]))        Q[j0:, j0:] -= V (T (V^T Q[j0:, j0:]))
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ttk_internal.h"
+
+namespace {
+
+constexpr int QB = 16;     // panel width
+constexpr int QT = 512;    // threads of the panel kernel
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Factor the m x jb panel P (row-major, leading dimension ld, in global memory) in place.
+// Outputs: Vout (m x QB row-major, unit lower trapezoidal, zero padded), Tout (QB x QB).
+__global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restrict__ P,
+                                                 int64_t ld, double* __restrict__ Vout,
+                                                 double* __restrict__ Tout) {
+  __shared__ double red[QT / 32][QB + 1];
+  __shared__ double s_tau[QB], s_w[QB], s_beta, s_scale;
+  __shared__ double Ts[QB][QB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
+  for (int c = 0; c < jb; c++) {
+    // ---- norm of x = P[c:, c]
+    double s = 0.0;
+    for (int i = c + 1 + tid; i < m; i += blockDim.x) {
+      double v = P[(int64_t)i * ld + c];
+      s += v * v;
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[warp][0] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double sig = 0.0;
+      for (int w = 0; w < nw; w++) sig += red[w][0];
+      double alpha = P[(int64_t)c * ld + c];
+      double tau = 0.0, scale = 0.0, beta = alpha;
+      if (sig > 0.0 || alpha < 0.0) {
+        double nrm = sqrt(alpha * alpha + sig);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      if (c < m && sig == 0.0 && alpha >= 0.0) {
+        tau = 0.0;
+        scale = 0.0;
+        beta = alpha;
+      }
+      s_tau[c] = tau;
+      s_beta = beta;
+      s_scale = scale;
+    }
+    __syncthreads();
+    const double tau = s_tau[c], scale = s_scale;
+    // ---- v = [1; x[1:] * scale] into P[c:, c] (below diagonal) and R diag
+    for (int i = c + 1 + tid; i < m; i += blockDim.x) P[(int64_t)i * ld + c] *= scale;
+    if (tid == 0) P[(int64_t)c * ld + c] = s_beta;
+    __syncthreads();
+    // ---- w_j = v^T P[c:, j] for j > c  and  z_l = V[:, l]^T v for l < c (T column)
+    // warp-parallel partial sums over rows, reduced through shared memory
+    {
+      double accw[QB], accz[QB];
+#pragma unroll
+      for (int j = 0; j < QB; j++) accw[j] = accz[j] = 0.0;
+      for (int i = c + tid; i < m; i += blockDim.x) {
+        const double vi = (i == c) ? 1.0 : P[(int64_t)i * ld + c];
+        const double* row = P + (int64_t)i * ld;
+#pragma unroll
+        for (int j = 0; j < QB; j++) {
+          if (j > c && j < jb) accw[j] += vi * row[j];
+          if (j < c) {
+            const double vl = (i == j) ? 1.0 : (i > j ? row[j] : 0.0);
+            accz[j] += vl * vi;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < QB; j++) {
+        double a = warp_sum(accw[j]);
+        double b = warp_sum(accz[j]);
+        if (lane == 0) {
+          red[warp][j] = (j > c) ? a : b;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < QB) {
+      double t = 0.0;
+      for (int w = 0; w < nw; w++) t += red[w][tid];
+      s_w[tid] = t;  // j > c: w_j ; j < c: z_j
+    }
+    __syncthreads();
+    // ---- apply H_c to the remaining panel columns: P[c:, j] -= tau v w_j
+    for (int e = tid; e < (m - c) * QB; e += blockDim.x) {
+      const int i = c + e / QB, j = e % QB;
+      if (j <= c || j >= jb) continue;
+      const double vi = (i == c) ? 1.0 : P[(int64_t)i * ld + c];
+      P[(int64_t)i * ld + j] -= tau * vi * s_w[j];
+    }
+    // ---- T column c (dlarft, forward, columnwise): T[0:c, c] = -tau T[0:c, 0:c] z
+    if (tid == 0) {
+      for (int l = 0; l < c; l++) {
+        double t = 0.0;
+        for (int q = l; q < c; q++) t += Ts[l][q] * s_w[q];
+        Ts[l][c] = -tau * t;
+      }
+      Ts[c][c] = tau;
+    }
+    __syncthreads();
+  }
+  // ---- export V (unit lower trapezoidal) and T
+  for (int e = tid; e < m * QB; e += blockDim.x) {
+    const int i = e / QB, j = e % QB;
+    double v = 0.0;
+    if (j < jb) {
+      if (i == j)
+        v = 1.0;
+      else if (i > j)
+        v = P[(int64_t)i * ld + j];
+    }
+    Vout[e] = v;
+  }
+  for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
+}
+
+}  // namespace
+
+// Q (n x n, row-major) from the Householder QR of A (n x n, row-major; A is not modified).
+int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
+  if (n <= 0) return TK_OK;
+  TagScope tag(ctx, "qr_pass1");
+  const int prof_id = tk_prof_begin(ctx, "qr_pass1", 4.0 / 3.0 * n * (double)n * n, 0.0);
+  DevBuf Aw, Vb, Tb, W1, W2;
+  TK_TRY(Aw.get(ctx, (size_t)n * n));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(Aw.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+  const int np = (n + QB - 1) / QB;
+  TK_TRY(Vb.get(ctx, (size_t)np * n * QB));  // panel p: (n - j0) x QB at offset p*n*QB
+  TK_TRY(Tb.get(ctx, (size_t)np * QB * QB));
+  TK_TRY(W1.get(ctx, (size_t)QB * n));
+  TK_TRY(W2.get(ctx, (size_t)QB * n));
+  for (int p = 0; p < np; p++) {
+    const int j0 = p * QB, jb = std::min(QB, n - j0), m = n - j0;
+    double* Vp = Vb.p + (size_t)p * n * QB;
+    double* Tp = Tb.p + (size_t)p * QB * QB;
+    qr_panel_k<<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+    TK_LAUNCH_CHECK(ctx);
+    const int nt = n - (j0 + jb);
+    if (nt > 0) {
+      double* At = Aw.p + (int64_t)j0 * n + j0 + jb;
+      // W1 = V^T A_t (QB x nt);  W2 = T^T W1;  A_t -= V W2
+      TK_TRY(tk_dgemm(ctx, true, false, QB, nt, m, 1.0, Vp, QB, At, n, 0.0, W1.p, nt));
+      TK_TRY(tk_dgemm(ctx, true, false, QB, nt, QB, 1.0, Tp, QB, W1.p, nt, 0.0, W2.p, nt));
+      TK_TRY(tk_dgemm(ctx, false, false, m, nt, QB, -1.0, Vp, QB, W2.p, nt, 1.0, At, n));
+    }
+  }
+  // Q = H_1 ... H_np : backward accumulation from the identity
+  TK_TRY(tk_eye(ctx, Q, n));
+  for (int p = np - 1; p >= 0; p--) {
+    const int j0 = p * QB, m = n - j0;
+    double* Vp = Vb.p + (size_t)p * n * QB;
+    double* Tp = Tb.p + (size_t)p * QB * QB;
+    double* Qs = Q + (int64_t)j0 * n + j0;
+    // W1 = V^T Qs (QB x m);  W2 = T W1;  Qs -= V W2
+    TK_TRY(tk_dgemm(ctx, true, false, QB, m, m, 1.0, Vp, QB, Qs, n, 0.0, W1.p, m));
+    TK_TRY(tk_dgemm(ctx, false, false, QB, m, QB, 1.0, Tp, QB, W1.p, m, 0.0, W2.p, m));
+    TK_TRY(tk_dgemm(ctx, false, false, m, m, QB, -1.0, Vp, QB, W2.p, m, 1.0, Qs, n));
+  }
+  tk_prof_end(ctx, prof_id);
+  return TK_OK;
+}

@@ -66,6 +66,54 @@ extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
   return TK_OK;
 }
 
+// ============================================================================ profiling
+int tk_prof_begin(tk_ctx* ctx, const char* cat, double flops, double bytes) {
+  if (!ctx->prof) return -1;
+  while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    ctx->ev_pool.push_back(e);
+  }
+  ProfRec r{cat, flops, bytes, ctx->ev_pool[ctx->ev_used], ctx->ev_pool[ctx->ev_used + 1]};
+  ctx->ev_used += 2;
+  cudaEventRecord(r.a, ctx->stream);
+  ctx->recs.push_back(r);
+  return (int)ctx->recs.size() - 1;
+}
+void tk_prof_end(tk_ctx* ctx, int id) {
+  if (id < 0 || !ctx->prof) return;
+  cudaEventRecord(ctx->recs[id].b, ctx->stream);
+}
+
+extern "C" int tk_ctx_profile(tk_ctx* ctx, int enable) {
+  if (!ctx) return TK_EARG;
+  ctx->prof = enable != 0;
+  if (enable) {
+    ctx->recs.clear();
+    ctx->ev_used = 0;
+  }
+  return TK_OK;
+}
+
+extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
+  if (!ctx) return TK_EARG;
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  std::string out;
+  for (auto& r : ctx->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    char line[256];
+    snprintf(line, sizeof(line), "%s %.6f %.6e %.6e\n", r.cat, ms, r.flops, r.bytes);
+    out += line;
+  }
+  if (buf && len) {
+    size_t n = std::min(len - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int)ctx->recs.size();
+}
+
 extern "C" const char* tk_last_error(const tk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 extern "C" int64_t tk_ctx_launch_count(const tk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -219,9 +267,28 @@ extern "C" int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* 
     ctx->err = "tk_apply_op: output capacity < (T r1, T r2)";
     return TK_ECAP;
   }
-  TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
-  TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, y->U2));
-  TK_TRY(tk_launch_time_apply(ctx, op, (int)x->r2, x->U3, y->U3));
+  {
+    // algorithmic bytes: read U1 once, write Y1 once, read the CSR (12 B/nnz + rowptr)
+    double nnz = 0;
+    for (auto v : op->h_nnz) nnz += (double)v;
+    double bytes = 8.0 * x->n_x * x->r1 + 8.0 * x->n_x * R1 + 12.0 * nnz +
+                   4.0 * op->T * (x->n_x + 1);
+    int id = tk_prof_begin(ctx, "spmm_multi", 2.0 * nnz * x->r1, bytes);
+    TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
+    tk_prof_end(ctx, id);
+  }
+  {
+    double bytes = 8.0 * (R1 * x->n_xi * R2 + x->r1 * x->n_xi * x->r2);
+    int id = tk_prof_begin(ctx, "stoch_apply", 2.0 * op->T * x->r1 * x->n_xi * x->n_xi * x->r2,
+                           bytes);
+    TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, y->U2));
+    tk_prof_end(ctx, id);
+  }
+  {
+    int id = tk_prof_begin(ctx, "time_apply", 0.0, 8.0 * (R2 + x->r2) * x->n_t);
+    TK_TRY(tk_launch_time_apply(ctx, op, (int)x->r2, x->U3, y->U3));
+    tk_prof_end(ctx, id);
+  }
   y->r1 = R1;
   y->r2 = R2;
   return TK_OK;
@@ -233,8 +300,28 @@ namespace {
 struct EigOpts {
   double abs_scale, rel;
 };
-const EigOpts kPass1{kEps, kEps};            // orthogonal basis, absolute accuracy
-const EigOpts kPass2{kEps * kEps, kEps};     // relative accuracy (graded Gram)
+// Pass 1 only needs an orthogonal V that diagonalises G to absolute accuracy: its skip
+// threshold sits above the rounding noise the block updates re-inject (~sqrt(64) eps ||G||),
+// otherwise rotations never stop.  Pass 2 needs relative accuracy: skip when
+// |g_pq| <= 32 eps sqrt(g_pp g_qq) (second-order effect on the eigenvalues: ~1e-29).
+const EigOpts kPass1{512 * kEps, 0.0};
+
+// Pass 1: an exactly orthogonal basis V of R^n whose leading columns follow the dominant
+// eigenvectors of the Gram G.  Default: Q of the Householder QR of G (one orthogonal-
+// iteration step; direct, O(n^3) on DMMA).  TTK_PASS1=jacobi uses a full Jacobi
+// eigen-decomposition instead (slower; kept for comparison).
+int pass1_basis(tk_ctx* ctx, int n, const double* G, double* lam, double* V) {
+  static const bool use_jacobi = getenv("TTK_PASS1") && !strcmp(getenv("TTK_PASS1"), "jacobi");
+  if (use_jacobi) {
+    DevBuf Gc;
+    TK_TRY(Gc.get(ctx, (size_t)n * n));
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(Gc.p, G, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+    return tk_jacobi_eig(ctx, n, Gc.p, lam, V, kPass1.abs_scale, kPass1.rel, 40, nullptr);
+  }
+  return tk_householder_q(ctx, n, G, V);
+}
+const EigOpts kPass2{kEps * kEps, 32 * kEps};
 const int kMaxSweeps = 40;
 const double kDropThr = 64.0 * kEps;         // numerical-dimension threshold of orth_rows
 
@@ -243,14 +330,14 @@ const double kDropThr = 64.0 * kEps;         // numerical-dimension threshold of
 // Outputs are allocated here.  Returns k via *k_out (host; blocks).
 int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, DevBuf& Qc,
               int64_t* k_out) {
+  TagScope tag(ctx, "orth_rows");
   DevBuf G, V, W, GW, lam, V2, sig, scr, tmp;
   TK_TRY(G.get(ctx, R * R));
   TK_TRY(V.get(ctx, R * R));
   TK_TRY(lam.get(ctx, R));
   // pass 1: G = A A^T, orthogonal eigenbasis V
   TK_TRY(tk_dgemm(ctx, false, true, R, R, N, 1.0, A, N, A, N, 0.0, G.p, R, true));
-  TK_TRY(tk_jacobi_eig(ctx, (int)R, G.p, lam.p, V.p, kPass1.abs_scale, kPass1.rel, kMaxSweeps,
-                       nullptr));
+  TK_TRY(pass1_basis(ctx, (int)R, G.p, lam.p, V.p));
   // W = A^T V  (N x R)
   TK_TRY(W.get(ctx, N * R));
   TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
@@ -290,20 +377,24 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
                  int64_t k, DevBuf& W, DevBuf& V2, DevBuf& Vt, DevBuf& lam) {
   DevBuf GY, GZ, T1, V, P;
   TK_TRY(GZ.get(ctx, k * k));
+  TagScope tag0(ctx, Lm ? "bond1.small" : "bond2.small");
   if (Lm) {
     TK_TRY(GY.get(ctx, R * R));
-    TK_TRY(tk_dgemm(ctx, true, false, R, R, M, 1.0, Y, R, Y, R, 0.0, GY.p, R, true));
+    {
+      TagScope t(ctx, "bond1.gram_Y");
+      TK_TRY(tk_dgemm(ctx, true, false, R, R, M, 1.0, Y, R, Y, R, 0.0, GY.p, R, true));
+    }
     TK_TRY(T1.get(ctx, R * k));
     TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, GY.p, R, Lm, k, 0.0, T1.p, k));
     TK_TRY(tk_dgemm(ctx, true, false, k, k, R, 1.0, Lm, k, T1.p, k, 0.0, GZ.p, k));
     TK_TRY(tk_symmetrize(ctx, k, GZ.p));
   } else {
+    TagScope t(ctx, "bond2.gram_C");
     TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, Y, R, Y, R, 0.0, GZ.p, k, true));
   }
   TK_TRY(V.get(ctx, k * k));
   TK_TRY(lam.get(ctx, k));
-  TK_TRY(tk_jacobi_eig(ctx, (int)k, GZ.p, lam.p, V.p, kPass1.abs_scale, kPass1.rel, kMaxSweeps,
-                       nullptr));
+  TK_TRY(pass1_basis(ctx, (int)k, GZ.p, lam.p, V.p));
   // W = Y (L V)
   const double* PV = V.p;
   if (Lm) {
@@ -312,10 +403,16 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
     PV = P.p;
   }
   TK_TRY(W.get(ctx, M * k));
-  TK_TRY(tk_dgemm(ctx, false, false, M, k, R, 1.0, Y, R, PV, k, 0.0, W.p, k));
+  {
+    TagScope t(ctx, Lm ? "bond1.form_W" : "bond2.form_W");
+    TK_TRY(tk_dgemm(ctx, false, false, M, k, R, 1.0, Y, R, PV, k, 0.0, W.p, k));
+  }
   DevBuf GW;
   TK_TRY(GW.get(ctx, k * k));
-  TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, W.p, k, W.p, k, 0.0, GW.p, k, true));
+  {
+    TagScope t(ctx, Lm ? "bond1.gram_W" : "bond2.gram_W");
+    TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, W.p, k, W.p, k, 0.0, GW.p, k, true));
+  }
   TK_TRY(V2.get(ctx, k * k));
   TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
                        nullptr));
@@ -356,6 +453,7 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
   }
   // ---- step B: Y2p = U2 x_3 L3   ((R1 n_xi) x R2) (R2 x k3)
   DevBuf Y2p;
+  TagScope tagr(ctx, "round.small");
   TK_TRY(Y2p.get(ctx, R1 * n_xi * k3));
   TK_TRY(tk_dgemm(ctx, false, false, R1 * n_xi, k3, R2, 1.0, x->U2, R2, L3, k3, 0.0, Y2p.p, k3));
   // ---- step C: Y2p as R1 x (n_xi k3) = L2 Q2
@@ -406,6 +504,7 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
     DevBuf F1;
     TK_TRY(F1.get(ctx, k2 * r1));
     TK_TRY(tk_col_scale(ctx, k2, r1, V2.p, k2, F1.p, r1, sig1.p, 1));
+    TagScope t(ctx, "bond1.form_U1");
     TK_TRY(tk_dgemm(ctx, false, false, n_x, r1, k2, 1.0, W.p, k2, F1.p, r1, 0.0, x->U1, r1));
   }
   W.release();

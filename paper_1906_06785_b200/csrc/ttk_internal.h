@@ -8,6 +8,14 @@
 
 #include "../../include/ttk.h"
 
+// One profiled kernel (or kernel group): CUDA events on the context stream around it, with
+// the algorithmic flop / byte counts of that launch.
+struct ProfRec {
+  const char* cat;
+  double flops, bytes;
+  cudaEvent_t a, b;
+};
+
 struct tk_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
@@ -17,7 +25,25 @@ struct tk_ctx {
   // pinned host scratch for the few device->host reads (ranks, scalars)
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // profiling (tk_ctx_profile): per-launch event pairs, tagged by the current phase
+  bool prof = false;
+  const char* tag = "misc";
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
+
+// Scoped phase tag for profiling records.
+struct TagScope {
+  tk_ctx* c;
+  const char* old;
+  TagScope(tk_ctx* ctx, const char* t) : c(ctx), old(ctx->tag) { ctx->tag = t; }
+  ~TagScope() { c->tag = old; }
+};
+
+// Open / close a profiling record on the context stream (no-ops unless ctx->prof).
+int tk_prof_begin(tk_ctx* ctx, const char* cat, double flops, double bytes);
+void tk_prof_end(tk_ctx* ctx, int id);
 
 struct tk_op {
   tk_ctx* ctx = nullptr;
@@ -103,6 +129,9 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   A rotation on (p,q) is skipped when |a_pq| <= max(abs_tol, rel_tol*sqrt(|a_pp a_qq|)).
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out);
+
+// Q (n x n, row-major, exactly orthogonal) of the blocked Householder QR of A (n x n).
+int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
 
 // Apply kernels
 int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1);

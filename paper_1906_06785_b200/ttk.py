@@ -19,6 +19,7 @@ _CODES = {TK_ESHAPE: "TK_ESHAPE", TK_ECAP: "TK_ECAP", TK_EARG: "TK_EARG",
           TK_ENUMERIC: "TK_ENUMERIC", TK_ECUDA: "TK_ECUDA"}
 
 EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "tk_ctx_launch_count",
+            "tk_ctx_profile", "tk_ctx_profile_dump",
             "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle"]
 
@@ -70,6 +71,8 @@ def lib():
     L.tk_axpby_host.argtypes = [P, D, TTP, D, TTP, TTP]
     L.tk_scale.argtypes = [P, TTP, P, I]
     L.tk_gmres_cycle.argtypes = [P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
+    L.tk_ctx_profile.argtypes = [P, I]
+    L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
         if name not in ("tk_version", "tk_last_error", "tk_ctx_launch_count"):
             getattr(L, name).restype = I
