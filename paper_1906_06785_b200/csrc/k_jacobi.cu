@@ -1,41 +1,68 @@
-// Symmetric eigen-decomposition by two-sided BLOCK Jacobi (fp64, on device).
+// Symmetric eigen-decomposition by two-sided BLOCK Jacobi (fp64, on device), as ONE
+// persistent cooperative kernel.
 //
-// Used for the small R x R Gram matrices of the rounding: pass 1
-// needs an ORTHOGONAL eigenbasis to absolute accuracy, pass 2 needs eigenvalues with
-// RELATIVE accuracy on a graded matrix — Jacobi with the relative skip test
-// |a_pq| <= rel * sqrt(|a_pp a_qq|) provides that (Demmel-Veselic), tridiagonal QR does not.
+// Used for PASS 2 of the two-pass Gram-Jacobi rounding: eigenvalues
+// of the graded Gram W^T W with RELATIVE accuracy — Jacobi with the relative skip test
+// |a_pq| <= rel * sqrt(|a_pp a_qq|) provides that (Demmel-Veselic); tridiagonal QR does not.
 //
 // Layout: the matrix is embedded in an n_pad x n_pad buffer (n_pad = 64 * ceil(n/64), zero
 // padding — padded indices never rotate since their couplings are 0), split into
 // nb = n_pad/32 blocks of 32 rows/cols.  One sweep = nb-1 rounds of a round-robin
-// tournament over blocks; a round handles nb/2 disjoint block pairs (I, J):
-//   inner_k      one CTA per pair: load S = G[I u J, I u J] (64 x 64) into shared memory,
-//                run scalar cyclic Jacobi on it (parallel ordering, Rutishauser updates of
-//                each 2x2 pivot block) accumulating Q (64 x 64); write Q and the rotated S.
-//   col_update_k G[:, I u J] <- G[:, I u J] Q  and  V[:, I u J] <- V[:, I u J] Q
-//   row_update_k G[I u J, :] <- Q^T G[I u J, :]  (the pair's own 64 x 64 block takes the
-//                inner solver's S, so its annihilated entries stay exactly 0)
-// Three launches per round; a per-sweep rotation counter (read by the host) ends the loop.
+// tournament over blocks; a round handles nb/2 disjoint block pairs (I, J) in three phases
+// separated by grid-wide barriers:
+//   inner  one CTA per pair: S = G[I u J, I u J] (64 x 64) in shared memory, one scalar
+//          cyclic Jacobi sweep (parallel ordering, Rutishauser updates of each 2x2 pivot)
+//          accumulating Q (64 x 64); Q and the rotated S go to global memory.
+//   cols   G[:, I u J] <- G[:, I u J] Q  and  V[:, I u J] <- V[:, I u J] Q   (64 x 64 tiles)
+//   rows   G[I u J, :] <- Q^T G[I u J, :]  (the pair's own block takes the inner S, so its
+//          annihilated entries stay exactly 0)
+// Rotation counts per sweep end the loop (all CTAs read the counter after the barrier).
+//
+// Cluster skip (bond SVDs only): when lskip >= 0, rotations between two indices whose
+// diagonal entries are both <= lskip are skipped.  lskip is chosen (cluster_skip_k) so the
+// skipped cluster's total mass is <= delta^2/4: its internal structure cannot move the rank
+// decision (only its trace enters the discarded tail, and the trace is invariant); couplings
+// between the cluster and the rest are still annihilated.  tk_round verifies afterwards that
+// the chosen rank lies above the cluster and otherwise re-runs without the skip.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
-#include <vector>
 
 #include "ttk_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
 constexpr int JB = 32;        // block size
 constexpr int JS = 2 * JB;    // pair size (64)
 constexpr int JLD = JS + 1;   // shared-memory leading dimension
-constexpr int JT = 256;       // threads per CTA (update kernels)
-constexpr int JTI = 512;      // threads per CTA (inner solver)
+constexpr int JT = 512;       // threads per CTA
+
+struct JacArgs {
+  int n_pad, nb, npairs;
+  double* G;
+  double* V;
+  double* Qb;
+  double* Sb;
+  const double* d_maxdiag;
+  double abs_scale, rel_tol;
+  const double* lskip;  // nullable
+  int max_inner, max_sweeps;
+  int* stats;           // rotation count per sweep
+  unsigned long long* offmax;  // per sweep: max |a_pq|/sqrt(a_pp a_qq) over applied rotations
+  double stop_rel;      // stop after a sweep whose offmax <= stop_rel (0: only when no rotation)
+  unsigned long long* tstamp;  // nullable: per-phase time sums of CTA 0 (TTK_DEBUG)
+  int* sweeps_out;
+};
 
 __host__ __device__ __forceinline__ int rr_player(int pos, int r, int ne) {
   return pos == 0 ? 0 : 1 + (pos - 1 + r) % (ne - 1);
 }
-
 __device__ __forceinline__ void pair_blocks(int t, int r, int nb, int& I, int& J) {
   int a = rr_player(t, r, nb), b = rr_player(nb - 1 - t, r, nb);
   I = min(a, b);
@@ -46,200 +73,343 @@ __device__ __forceinline__ int gidx(int l, int I, int J) {
   return l < JB ? I * JB + l : J * JB + (l - JB);
 }
 
-__global__ void __launch_bounds__(JTI) inner_k(int n_pad, const double* __restrict__ G,
-                                               double* __restrict__ Qout, double* __restrict__ Sout,
-                                               int* __restrict__ skip, int r, int nb,
-                                               const double* __restrict__ d_maxdiag,
-                                               double abs_scale, double rel_tol, int max_inner,
-                                               int* __restrict__ counter) {
-  extern __shared__ double sm[];
-  double* S = sm;                 // [64][65]
-  double* Q = sm + JS * JLD;      // [64][65]
-  __shared__ double rc[JB], rs[JB], rt[JB], rapp[JB], raqq[JB], rapq[JB];
-  __shared__ int rp_[JB], rq_[JB], ract[JB];
-  __shared__ int nrot;
-  const int t = blockIdx.x;
+struct InnerShared {
+  double rc[JB], rs[JB], rt[JB], rapp[JB], raqq[JB], rapq[JB];
+  int rp[JB], rq[JB], ract[JB];
+  int nrot;
+  double offmax;
+};
+
+// skip test without a square root: rotate iff |a_pq| > thr, thr = max(abs, rel sqrt(a_pp a_qq)),
+// i.e. a_pq^2 > max(abs^2, rel^2 |a_pp a_qq|); cluster pairs never rotate.
+__device__ __forceinline__ bool needs_rot(double app, double aqq, double apq, double abs_tol,
+                                          double rel, double lsk) {
+  if (app <= lsk && aqq <= lsk) return false;
+  const double a2 = apq * apq;
+  return a2 > abs_tol * abs_tol && a2 > rel * rel * fabs(app * aqq);
+}
+
+// One pair's inner problem, by one CTA (JT = 512 threads).  Per inner round: (a) warp 0
+// computes the 32 disjoint rotations; (b) every thread applies J^T S J to two 2x2 blocks
+// (rows of one pair x columns of another: each element belongs to exactly one block, so the
+// update is in place) and Q <- Q J to four (row, pair) items.  Two barriers per round.
+__device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerShared& sh,
+                            double abs_tol, double lsk) {
+  double* S = sm;
+  double* Q = sm + JS * JLD;
   int I, J;
-  pair_blocks(t, r, nb, I, J);
-  const double abs_tol = fmax(abs_scale * d_maxdiag[0], 1e-300);
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+  pair_blocks(t, r, a.nb, I, J);
+  const double* G = a.G;
+  const int n_pad = a.n_pad;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < JS * JS; e += blockDim.x) {
     int i = e / JS, j = e % JS;
     int gi = gidx(i, I, J), gj = gidx(j, I, J);
-    double v = 0.5 * (G[(int64_t)gi * n_pad + gj] + G[(int64_t)gj * n_pad + gi]);
-    S[i * JLD + j] = v;
+    S[i * JLD + j] = 0.5 * (G[(int64_t)gi * n_pad + gj] + G[(int64_t)gj * n_pad + gi]);
     Q[i * JLD + j] = (i == j) ? 1.0 : 0.0;
   }
-  if (threadIdx.x == 0) nrot = 0;
   __syncthreads();
-  // already converged block pair (every |s_ij| below its skip threshold): no rotation
   {
     int any = 0;
-    for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    for (int e = tid; e < JS * JS; e += blockDim.x) {
       int i = e / JS, j = e % JS;
       if (j <= i) continue;
-      double thr = fmax(abs_tol, rel_tol * sqrt(fabs(S[i * JLD + i] * S[j * JLD + j])));
-      any |= fabs(S[i * JLD + j]) > thr;
+      any |= needs_rot(S[i * JLD + i], S[j * JLD + j], S[i * JLD + j], abs_tol, a.rel_tol, lsk);
     }
-    if (!__syncthreads_or(any)) {
-      if (threadIdx.x == 0) skip[t] = 1;
+    any = __syncthreads_or(any);
+    if (!any) {
+      double* Qo = a.Qb + (int64_t)t * JS * JS;
+      double* So = a.Sb + (int64_t)t * JS * JS;
+      for (int e = tid; e < JS * JS; e += blockDim.x) {
+        Qo[e] = Q[(e / JS) * JLD + e % JS];
+        So[e] = S[(e / JS) * JLD + e % JS];
+      }
+      __syncthreads();
       return;
     }
-    if (threadIdx.x == 0) skip[t] = 0;
   }
-  for (int sweep = 0; sweep < max_inner; sweep++) {
-    const int before = nrot;
-    __syncthreads();
+  long long pa_sum = 0, pb_sum = 0, t_a = 0;
+  int my_rot = 0;          // warp 0 lanes: rotations applied (this call)
+  double my_off = 0.0;     // warp 0 lanes: largest relative coupling rotated away
+  for (int sweep = 0; sweep < a.max_inner; sweep++) {
+    int sweep_rot = 0;
     for (int ir = 0; ir < JS - 1; ir++) {
-      // (a) rotation parameters of the 32 disjoint pairs of this inner round
-      if (threadIdx.x < JB) {
-        const int k = threadIdx.x;
-        int a = rr_player(k, ir, JS), b = rr_player(JS - 1 - k, ir, JS);
-        int p = min(a, b), q = max(a, b);
-        double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
-        double c = 1.0, s = 0.0, tt = 0.0;
+      if (tid == 0) t_a = clock64();
+      if (tid < JB) {
+        const int k = tid;
+        const int pa = rr_player(k, ir, JS), pb = rr_player(JS - 1 - k, ir, JS);
+        const int p = min(pa, pb), q = max(pa, pb);
+        const double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
+        double c = 1.0, sn = 0.0, tt = 0.0;
         int act = 0;
-        double thr = fmax(abs_tol, rel_tol * sqrt(fabs(app * aqq)));
-        if (fabs(apq) > thr) {
-          double theta = (aqq - app) / (2.0 * apq);
-          double at = fabs(theta);
-          if (at > 1e150) {
-            tt = 0.5 / theta;
-          } else {
-            tt = 1.0 / (at + sqrt(1.0 + at * at));
-            if (theta < 0) tt = -tt;
-          }
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          s = tt * c;
+        if (needs_rot(app, aqq, apq, abs_tol, a.rel_tol, lsk)) {
+          // t = sgn(d) e / (|d| + sqrt(d^2 + e^2)),  d = a_qq - a_pp, e = 2 a_pq
+          const double d = aqq - app, e2 = 2.0 * apq;
+          const double rr = sqrt(fma(d, d, e2 * e2));
+          tt = (d >= 0.0 ? e2 : -e2) / (fabs(d) + rr);
+          c = rsqrt(fma(tt, tt, 1.0));
+          sn = tt * c;
           act = 1;
+          my_off = fmax(my_off, fabs(apq) * rsqrt(fmax(fabs(app * aqq), 1e-300)));
         }
-        rc[k] = c;
-        rs[k] = s;
-        rt[k] = tt;
-        rapp[k] = app;
-        raqq[k] = aqq;
-        rapq[k] = apq;
-        rp_[k] = p;
-        rq_[k] = q;
-        ract[k] = act;
-        const unsigned bal = __ballot_sync(0xffffffffu, act);
-        if (k == 0) nrot += __popc(bal);
+        sh.rc[k] = c;
+        sh.rs[k] = sn;
+        sh.rt[k] = tt;
+        sh.rapp[k] = app;
+        sh.raqq[k] = aqq;
+        sh.rapq[k] = apq;
+        sh.rp[k] = p;
+        sh.rq[k] = q;
+        sh.ract[k] = act;
+        sweep_rot += act;
       }
       __syncthreads();
-      // (b) column update of S and Q:  (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q)
-      for (int e = threadIdx.x; e < JB * JS; e += blockDim.x) {
-        const int pr = e / JS, i = e % JS;
-        if (!ract[pr]) continue;
-        const int p = rp_[pr], q = rq_[pr];
-        const double c = rc[pr], s = rs[pr];
-        double sp = S[i * JLD + p], sq = S[i * JLD + q];
-        S[i * JLD + p] = c * sp - s * sq;
-        S[i * JLD + q] = s * sp + c * sq;
-        double qp = Q[i * JLD + p], qq = Q[i * JLD + q];
-        Q[i * JLD + p] = c * qp - s * qq;
-        Q[i * JLD + q] = s * qp + c * qq;
+      if (tid == 0) {
+        long long now = clock64();
+        pa_sum += now - t_a;
+        t_a = now;
       }
-      __syncthreads();
-      // (c) row update of S; the 2x2 pivot block takes Rutishauser's values
-      for (int e = threadIdx.x; e < JB * JS; e += blockDim.x) {
-        const int pr = e / JS, j = e % JS;
-        if (!ract[pr]) continue;
-        const int p = rp_[pr], q = rq_[pr];
-        if (j == p) {
-          S[p * JLD + p] = rapp[pr] - rt[pr] * rapq[pr];
-          S[q * JLD + p] = 0.0;
-        } else if (j == q) {
-          S[q * JLD + q] = raqq[pr] + rt[pr] * rapq[pr];
-          S[p * JLD + q] = 0.0;
-        } else {
-          const double c = rc[pr], s = rs[pr];
-          double sp = S[p * JLD + j], sq = S[q * JLD + j];
-          S[p * JLD + j] = c * sp - s * sq;
-          S[q * JLD + j] = s * sp + c * sq;
+      // S <- J^T S J on 2x2 blocks (pair P1 rows, pair P2 cols) and Q <- Q J.
+      // Thread map: P2 = lane (parameters loaded once), P1 = warp and warp + 16; Q rows
+      // warp + 16 m (m < 4) of pair lane.
+      {
+        const int lane = tid & 31, wq = tid >> 5;
+        const double c2 = sh.rc[lane], s2 = sh.rs[lane];
+        const int p2 = sh.rp[lane], q2 = sh.rq[lane], act2 = sh.ract[lane];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int P1 = wq + 16 * h;
+          const int act1 = sh.ract[P1];
+          if (!act1 && !act2) continue;
+          const int p1 = sh.rp[P1], q1 = sh.rq[P1];
+          if (P1 == lane) {
+            const double t1 = sh.rt[P1], a1 = sh.rapq[P1];
+            S[p1 * JLD + p1] = sh.rapp[P1] - t1 * a1;
+            S[q1 * JLD + q1] = sh.raqq[P1] + t1 * a1;
+            S[p1 * JLD + q1] = 0.0;
+            S[q1 * JLD + p1] = 0.0;
+            continue;
+          }
+          const double c1 = sh.rc[P1], s1 = sh.rs[P1];
+          const double x00 = S[p1 * JLD + p2], x01 = S[p1 * JLD + q2];
+          const double x10 = S[q1 * JLD + p2], x11 = S[q1 * JLD + q2];
+          const double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
+          const double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
+          S[p1 * JLD + p2] = c1 * y00 - s1 * y10;
+          S[q1 * JLD + p2] = s1 * y00 + c1 * y10;
+          S[p1 * JLD + q2] = c1 * y01 - s1 * y11;
+          S[q1 * JLD + q2] = s1 * y01 + c1 * y11;
+        }
+        if (act2) {
+#pragma unroll
+          for (int m = 0; m < 4; m++) {
+            const int i = wq + 16 * m;
+            const double qp = Q[i * JLD + p2], qq = Q[i * JLD + q2];
+            Q[i * JLD + p2] = c2 * qp - s2 * qq;
+            Q[i * JLD + q2] = s2 * qp + c2 * qq;
+          }
         }
       }
       __syncthreads();
+      if (tid == 0) pb_sum += clock64() - t_a;
     }
-    const bool done = (nrot == before);
+    // inner convergence (only matters when max_inner > 1)
+    if (tid < JB) {
+      int v = sweep_rot;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) sh.nrot = v;
+      my_rot += sweep_rot;
+    }
+    __syncthreads();
+    const bool done = (sh.nrot == 0);
     __syncthreads();
     if (done) break;
   }
-  // write Q and S (rotated pair block)
-  double* Qo = Qout + (int64_t)t * JS * JS;
-  double* So = Sout + (int64_t)t * JS * JS;
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    Qo[e] = Q[i * JLD + j];
-    So[e] = S[i * JLD + j];
+  double* Qo = a.Qb + (int64_t)t * JS * JS;
+  double* So = a.Sb + (int64_t)t * JS * JS;
+  for (int e = tid; e < JS * JS; e += blockDim.x) {
+    Qo[e] = Q[(e / JS) * JLD + e % JS];
+    So[e] = S[(e / JS) * JLD + e % JS];
   }
-  if (threadIdx.x == 0 && nrot) atomicAdd(counter, nrot);
-}
-
-// G[:, I u J] <- G[:, I u J] Q (z = 0),  V[:, I u J] <- V[:, I u J] Q (z = 1)
-__global__ void __launch_bounds__(JT) col_update_k(int n_pad, double* __restrict__ G,
-                                                   double* __restrict__ V,
-                                                   const double* __restrict__ Qall,
-                                                   const int* __restrict__ skip, int r, int nb) {
-  extern __shared__ double dsm[];
-  double(*Qs)[JS + 1] = reinterpret_cast<double(*)[JS + 1]>(dsm);
-  double(*Ts)[JS + 1] = reinterpret_cast<double(*)[JS + 1]>(dsm + JS * (JS + 1));
-  const int t = blockIdx.y;
-  if (skip[t]) return;
-  int I, J;
-  pair_blocks(t, r, nb, I, J);
-  double* M = blockIdx.z == 0 ? G : V;
-  const int row0 = blockIdx.x * JS;
-  const double* Q = Qall + (int64_t)t * JS * JS;
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    Qs[i][j] = Q[e];
-    Ts[i][j] = M[(int64_t)(row0 + i) * n_pad + gidx(j, I, J)];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < JS; k++) acc = fma(Ts[i][k], Qs[k][j], acc);
-    M[(int64_t)(row0 + i) * n_pad + gidx(j, I, J)] = acc;
-  }
-}
-
-// G[I u J, :] <- Q^T G[I u J, :]; the pair's own columns take the inner solver's S
-__global__ void __launch_bounds__(JT) row_update_k(int n_pad, double* __restrict__ G,
-                                                   const double* __restrict__ Qall,
-                                                   const double* __restrict__ Sall,
-                                                   const int* __restrict__ skip, int r, int nb) {
-  extern __shared__ double dsm[];
-  double(*Qs)[JS + 1] = reinterpret_cast<double(*)[JS + 1]>(dsm);
-  double(*Ts)[JS + 1] = reinterpret_cast<double(*)[JS + 1]>(dsm + JS * (JS + 1));
-  const int t = blockIdx.y;
-  if (skip[t]) return;
-  int I, J;
-  pair_blocks(t, r, nb, I, J);
-  const int col0 = blockIdx.x * JS;
-  const double* Q = Qall + (int64_t)t * JS * JS;
-  const double* S = Sall + (int64_t)t * JS * JS;
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    Qs[i][j] = Q[e];
-    Ts[i][j] = G[(int64_t)gidx(i, I, J) * n_pad + col0 + j];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    int gc = col0 + j;
-    int bc = gc / JB;
-    double v;
-    if (bc == I || bc == J) {
-      int lj = (bc == I) ? gc - I * JB : JB + gc - J * JB;
-      v = S[i * JS + lj];
-    } else {
-      v = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < JS; k++) v = fma(Qs[k][i], Ts[k][j], v);
+  if (tid < JB) {
+    int v = my_rot;
+    double o = my_off;
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, w);
+      o = fmax(o, __shfl_xor_sync(0xffffffffu, o, w));
     }
-    G[(int64_t)gidx(i, I, J) * n_pad + gc] = v;
+    if (tid == 0 && a.tstamp && t == 0) {
+      a.tstamp[6] += pa_sum;
+      a.tstamp[7] += pb_sum;
+    }
+    if (tid == 0 && v) {
+      atomicAdd(a.stats, v);
+      atomicMax(a.offmax, (unsigned long long)__double_as_longlong(o));
+    }
   }
+  __syncthreads();
+}
+
+constexpr int TLD = JS + 4;  // tile leading dimension (68): conflict-free DMMA fragments
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// acc (this warp's 16 x 16 block of C = op(A) B, 64 x 64 x 64, A/B in shared memory with
+// leading dimension TLD; transA: op(A)[m][k] = A[k][m]).  16 warps cover the 64 x 64 C.
+__device__ __forceinline__ void tile_mma(const double* As, bool transA, const double* Bs,
+                                         double acc[2][2][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < JS; k += 4) {
+    double av[2], bv[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const int m = wm + 8 * i + lr, kk = k + lc;
+      av[i] = transA ? As[kk * TLD + m] : As[m * TLD + kk];
+    }
+#pragma unroll
+    for (int j = 0; j < 2; j++) bv[j] = Bs[(k + lc) * TLD + wn + 8 * j + lr];
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+      for (int j = 0; j < 2; j++) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+  }
+}
+
+// 64-row tile of M[:, I u J] <- M[:, I u J] Q   (DMMA)
+__device__ void col_tile(const JacArgs& a, double* M, int row0, int t, int r, double* sm) {
+  double* Qs = sm;
+  double* Ts = sm + JS * TLD;
+  int I, J;
+  pair_blocks(t, r, a.nb, I, J);
+  const double* Q = a.Qb + (int64_t)t * JS * JS;
+  const int n_pad = a.n_pad;
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = Q[e];
+    Ts[i * TLD + j] = M[(int64_t)(row0 + i) * n_pad + gidx(j, I, J)];
+  }
+  __syncthreads();
+  double acc[2][2][2];
+  tile_mma(Ts, false, Qs, acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
+        M[(int64_t)(row0 + m) * n_pad + gidx(n, I, J)] = acc[i][j][h];
+      }
+  __syncthreads();
+}
+
+// 64-column tile of G[I u J, :] <- Q^T G[I u J, :]; the pair's own columns take S  (DMMA)
+__device__ void row_tile(const JacArgs& a, int col0, int t, int r, double* sm) {
+  double* Qs = sm;
+  double* Ts = sm + JS * TLD;
+  int I, J;
+  pair_blocks(t, r, a.nb, I, J);
+  const double* Q = a.Qb + (int64_t)t * JS * JS;
+  const double* S = a.Sb + (int64_t)t * JS * JS;
+  double* G = a.G;
+  const int n_pad = a.n_pad;
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = Q[e];
+    Ts[i * TLD + j] = G[(int64_t)gidx(i, I, J) * n_pad + col0 + j];
+  }
+  __syncthreads();
+  double acc[2][2][2];
+  tile_mma(Qs, true, Ts, acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
+        const int gc = col0 + n, bc = gc / JB;
+        double v = acc[i][j][h];
+        if (bc == I || bc == J) v = S[m * JS + ((bc == I) ? gc - I * JB : JB + gc - J * JB)];
+        G[(int64_t)gidx(m, I, J) * n_pad + gc] = v;
+      }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
+  extern __shared__ double sm[];
+  __shared__ InnerShared sh;
+  const double abs_tol = fmax(a.abs_scale * a.d_maxdiag[0], 1e-300);
+  const double lsk = a.lskip ? a.lskip[0] : -1.0;
+  const int rtiles = a.n_pad / JS;
+  unsigned long long tsum[6] = {0, 0, 0, 0, 0, 0}, tprev = 0;
+  const bool rec = a.tstamp && blockIdx.x == 0 && threadIdx.x == 0;
+  auto mark = [&](int k) {
+    if (rec) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (k >= 0) tsum[k] += now - tprev;
+      tprev = now;
+    }
+  };
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; sweep++) {
+    JacArgs as = a;
+    as.stats = a.stats + sweep;
+    as.offmax = a.offmax + sweep;
+    for (int r = 0; r < a.nb - 1; r++) {
+      mark(-1);
+      for (int t = blockIdx.x; t < a.npairs; t += gridDim.x) inner_solve(as, t, r, sm, sh, abs_tol, lsk);
+      mark(0);
+      if (coop) cg::this_grid().sync(); else __syncthreads();
+      mark(1);
+      const int nct = rtiles * a.npairs * 2;
+      for (int w = blockIdx.x; w < nct; w += gridDim.x) {
+        const int which = w / (rtiles * a.npairs), rem = w % (rtiles * a.npairs);
+        const int t = rem / rtiles, rt = rem % rtiles;
+        col_tile(as, which ? a.V : a.G, rt * JS, t, r, sm);
+      }
+      mark(2);
+      if (coop) cg::this_grid().sync(); else __syncthreads();
+      mark(3);
+      const int nrt = rtiles * a.npairs;
+      for (int w = blockIdx.x; w < nrt; w += gridDim.x) {
+        const int t = w / rtiles, ct = w % rtiles;
+        row_tile(as, ct * JS, t, r, sm);
+      }
+      mark(4);
+      if (coop) cg::this_grid().sync(); else __syncthreads();
+      mark(5);
+    }
+    const int rot = *((volatile int*)(a.stats + sweep));
+    const double om = __longlong_as_double(
+        (long long)*((volatile unsigned long long*)(a.offmax + sweep)));
+    if (rot == 0 || a.npairs == 1 || om <= a.stop_rel) {
+      sweep++;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.sweeps_out[0] = sweep;
+  if (rec)
+    for (int k = 0; k < 6; k++) a.tstamp[k] = tsum[k];  // [6], [7]: inner phase cycles
 }
 
 __global__ void embed_k(int n, int n_pad, const double* __restrict__ A, double* __restrict__ G,
@@ -282,10 +452,56 @@ __global__ void max_abs_diag_k(int n, const double* A, double* out) {
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
+// lskip = largest diagonal value of the set of smallest diagonal entries whose total is
+// <= frac * delta^2, delta^2 = tol^2 * trace / 2  (-1 if that set is empty).
+__global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, double frac,
+                               double* out) {
+  extern __shared__ double d[];
+  __shared__ double tr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = fmax(A[(int64_t)i * n + i], 0.0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; i++) s += d[i];
+    tr = s;
+  }
+  __syncthreads();
+  // rank-sort ascending into d[n .. 2n)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rk = 0;
+    for (int j = 0; j < n; j++) rk += (d[j] < d[i]) || (d[j] == d[i] && j < i);
+    d[n + rk] = d[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double lim = frac * tol * tol * tr * 0.5;
+    double cum = 0.0, l = -1.0;
+    for (int i = 0; i < n; i++) {
+      cum += d[n + i];
+      if (cum > lim) break;
+      l = d[n + i];
+    }
+    out[0] = l;
+  }
+}
+
 }  // namespace
 
+int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev) {
+  size_t smem = 2 * (size_t)n * sizeof(double);
+  if (smem > 200 * 1024) {
+    // too large for the shared-memory sort: no skipping (always safe)
+    return tk_set_scalar(ctx, lskip_dev, -1.0);
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(cluster_skip_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cluster_skip_k<<<1, 512, smem, ctx->stream>>>(n, A, tol, 0.25, lskip_dev);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
-                  double rel_tol, int max_sweeps, int* sweeps_out) {
+                  double rel_tol, int max_sweeps, int* sweeps_out, const double* lskip_dev) {
   if (n <= 0) return TK_OK;
   const int n_pad = ((n + JS - 1) / JS) * JS;
   const int nb = n_pad / JB;
@@ -295,10 +511,13 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   TK_TRY(Vp.get(ctx, (size_t)n_pad * n_pad));
   TK_TRY(Qb.get(ctx, (size_t)npairs * JS * JS));
   TK_TRY(Sb.get(ctx, (size_t)npairs * JS * JS));
-  TK_TRY(scr.get(ctx, 2 + (size_t)max_sweeps));
+  TK_TRY(scr.get(ctx, 2 + 2 * (size_t)max_sweeps));
   double* d_maxdiag = scr.p;
-  int* counters = (int*)(scr.p + 1);
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(counters, 0, sizeof(int) * (max_sweeps + 1), ctx->stream));
+  unsigned long long* offmax = (unsigned long long*)(scr.p + 1);
+  int* stats = (int*)(scr.p + 1 + max_sweeps);
+  int* d_sweeps = stats + max_sweeps;
+  TK_CUDA_TRY(ctx, cudaMemsetAsync(scr.p + 1, 0, sizeof(double) * (1 + 2 * (size_t)max_sweeps),
+                                   ctx->stream));
   const int prof_id = tk_prof_begin(ctx, "jacobi", 0.0, 0.0);
   max_abs_diag_k<<<1, 256, 0, ctx->stream>>>(n, A, d_maxdiag);
   TK_LAUNCH_CHECK(ctx);
@@ -308,48 +527,80 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
     embed_k<<<g, 256, 0, ctx->stream>>>(n, n_pad, A, Gp.p, Vp.p);
     TK_LAUNCH_CHECK(ctx);
   }
-  static bool attr = false;
-  const size_t ismem = 2 * (size_t)JS * JLD * sizeof(double);
-  if (!attr) {
-    cudaFuncSetAttribute(inner_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem);
-    cudaFuncSetAttribute(col_update_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem);
-    cudaFuncSetAttribute(row_update_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ismem);
-    attr = true;
+  const size_t smem = 2 * (size_t)JS * TLD * sizeof(double);
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    cudaFuncSetAttribute(jacobi_persistent_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_persistent_k, JT, smem);
+    max_grid = std::max(1, per_sm) * ctx->num_sms;
   }
-  DevBuf skipb;
-  TK_TRY(skipb.get(ctx, (size_t)npairs));
-  int* skip = (int*)skipb.p;
-  // a single pair (n <= 64) is solved completely by the inner solver; otherwise one inner
-  // sweep per block pair and round (classical block Jacobi)
-  const int max_inner = (npairs == 1) ? 60 : 1;
-  int sweep = 0;
-  for (; sweep < max_sweeps; sweep++) {
-    for (int r = 0; r < nb - 1; r++) {
-      inner_k<<<npairs, JTI, ismem, ctx->stream>>>(n_pad, Gp.p, Qb.p, Sb.p, skip, r, nb,
-                                                  d_maxdiag, abs_tol_scale, rel_tol, max_inner,
-                                                  counters + sweep);
-      TK_LAUNCH_CHECK(ctx);
-      col_update_k<<<dim3(n_pad / JS, npairs, 2), JT, ismem, ctx->stream>>>(n_pad, Gp.p, Vp.p,
-                                                                           Qb.p, skip, r, nb);
-      TK_LAUNCH_CHECK(ctx);
-      row_update_k<<<dim3(n_pad / JS, npairs), JT, ismem, ctx->stream>>>(n_pad, Gp.p, Qb.p, Sb.p,
-                                                                        skip, r, nb);
-      TK_LAUNCH_CHECK(ctx);
-    }
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, counters + sweep, sizeof(int),
-                                     cudaMemcpyDeviceToHost, ctx->stream));
-    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    const int rot = *(int*)ctx->pinned;
-    if (rot == 0 || (npairs == 1 && sweep == 0)) {
-      sweep++;
-      break;
-    }
+  JacArgs a;
+  a.n_pad = n_pad;
+  a.nb = nb;
+  a.npairs = npairs;
+  a.G = Gp.p;
+  a.V = Vp.p;
+  a.Qb = Qb.p;
+  a.Sb = Sb.p;
+  a.d_maxdiag = d_maxdiag;
+  a.abs_scale = abs_tol_scale;
+  a.rel_tol = rel_tol;
+  a.lskip = lskip_dev;
+  a.offmax = offmax;
+  // relative mode: a sweep whose largest applied relative coupling is <= 1e-10 leaves
+  // couplings of O(1e-20) behind (quadratic convergence): stop after it
+  a.stop_rel = rel_tol > 0.0 ? 1e-10 : 0.0;
+  static const bool dbg = getenv("TTK_DEBUG") != nullptr;
+  DevBuf tsb;
+  a.tstamp = nullptr;
+  if (dbg) {
+    TK_TRY(tsb.get(ctx, 8));
+    TK_CUDA_TRY(ctx, cudaMemsetAsync(tsb.p, 0, 8 * sizeof(double), ctx->stream));
+    a.tstamp = (unsigned long long*)tsb.p;
+  }
+  a.max_inner = (npairs == 1) ? 60 : 1;
+  a.max_sweeps = max_sweeps;
+  a.stats = stats;
+  a.sweeps_out = d_sweeps;
+  const int rtiles = n_pad / JS;
+  int grid = std::min(max_grid, std::max(npairs, rtiles * npairs * 2));
+  grid = std::min(grid, ctx->num_sms);
+  int coop = grid > 1 ? 1 : 0;
+  if (coop) {
+    void* args[] = {&a, &coop};
+    TK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)jacobi_persistent_k, dim3(grid),
+                                                 dim3(JT), args, smem, ctx->stream));
+    ctx->launches++;
+  } else {
+    jacobi_persistent_k<<<1, JT, smem, ctx->stream>>>(a, 0);
+    TK_LAUNCH_CHECK(ctx);
   }
   int sg = (int)std::min<int64_t>((n + 127) / 128, 4LL * ctx->num_sms);
   eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, Gp.p, Vp.p, lam, V);
   TK_LAUNCH_CHECK(ctx);
   tk_prof_end(ctx, prof_id);
-  if (sweeps_out) *sweeps_out = sweep;
-  if (getenv("TTK_DEBUG")) fprintf(stderr, "[ttk] jacobi n=%d sweeps=%d rel=%g\n", n, sweep, rel_tol);
+  if (sweeps_out || getenv("TTK_DEBUG")) {
+    int sw = 0;
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_sweeps, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    sw = *(int*)ctx->pinned;
+    if (sweeps_out) *sweeps_out = sw;
+    if (getenv("TTK_DEBUG")) {
+      unsigned long long ts[8];
+      TK_CUDA_TRY(ctx, cudaMemcpy(ts, tsb.p, sizeof(ts), cudaMemcpyDeviceToHost));
+      const double rounds = (double)sw * (nb - 1);
+      fprintf(stderr,
+              "[ttk] jacobi n=%d sweeps=%d rel=%g skip=%d grid=%d | per round us: inner %.1f "
+              "sync %.1f cols %.1f sync %.1f rows %.1f sync %.1f\n",
+              n, sw, rel_tol, lskip_dev ? 1 : 0, grid, ts[0] / rounds / 1e3, ts[1] / rounds / 1e3,
+              ts[2] / rounds / 1e3, ts[3] / rounds / 1e3, ts[4] / rounds / 1e3,
+              ts[5] / rounds / 1e3);
+      fprintf(stderr, "[ttk]    inner round cycles: params %.0f  update %.0f\n",
+              ts[6] / rounds / 63.0, ts[7] / rounds / 63.0);
+    }
+  }
   return TK_OK;
 }

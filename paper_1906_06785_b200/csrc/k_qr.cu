@@ -147,8 +147,7 @@ __global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restri
 // Q (n x n, row-major) from the Householder QR of A (n x n, row-major; A is not modified).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   if (n <= 0) return TK_OK;
-  TagScope tag(ctx, "qr_pass1");
-  const int prof_id = tk_prof_begin(ctx, "qr_pass1", 4.0 / 3.0 * n * (double)n * n, 0.0);
+  TagScope tag(ctx, "qr_pass1.gemm");
   DevBuf Aw, Vb, Tb, W1, W2;
   TK_TRY(Aw.get(ctx, (size_t)n * n));
   TK_CUDA_TRY(ctx, cudaMemcpyAsync(Aw.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
@@ -162,8 +161,10 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     const int j0 = p * QB, jb = std::min(QB, n - j0), m = n - j0;
     double* Vp = Vb.p + (size_t)p * n * QB;
     double* Tp = Tb.p + (size_t)p * QB * QB;
+    const int pid = tk_prof_begin(ctx, "qr_panel", 2.0 * m * (double)jb * jb, 0.0);
     qr_panel_k<<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
     TK_LAUNCH_CHECK(ctx);
+    tk_prof_end(ctx, pid);
     const int nt = n - (j0 + jb);
     if (nt > 0) {
       double* At = Aw.p + (int64_t)j0 * n + j0 + jb;
@@ -185,6 +186,5 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     TK_TRY(tk_dgemm(ctx, false, false, QB, m, QB, 1.0, Tp, QB, W1.p, m, 0.0, W2.p, m));
     TK_TRY(tk_dgemm(ctx, false, false, m, m, QB, -1.0, Vp, QB, W2.p, m, 1.0, Qs, n));
   }
-  tk_prof_end(ctx, prof_id);
   return TK_OK;
 }

@@ -67,10 +67,18 @@ __global__ void eye_k(double* dst, int64_t n) {
 // thousand), so the result does not depend on the launch shape.
 __global__ void rank_select_k(int n, const double* __restrict__ lam, double* __restrict__ sig,
                               double tol, const double* __restrict__ delta_in, int64_t rmax,
-                              double kthr, int* __restrict__ info, double* __restrict__ dinfo) {
+                              double kthr, int* __restrict__ info, double* __restrict__ dinfo,
+                              const double* __restrict__ lskip) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = sqrt(fmax(lam[i], 0.0));
   __syncwarp();
   if (threadIdx.x != 0) return;
+  int nres = n;
+  if (lskip) {
+    const double l = lskip[0];
+    nres = 0;
+    for (int i = 0; i < n; i++) nres += lam[i] > l;
+  }
+  info[2] = nres;
   double nrm2 = 0.0;
   for (int i = n - 1; i >= 0; i--) nrm2 += sig[i] * sig[i];
   double nrm = sqrt(nrm2);
@@ -257,9 +265,9 @@ int tk_eye(tk_ctx* ctx, double* dst, int64_t n) {
 }
 int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
                    const double* delta_dev_in, int64_t rmax, double kthr, int* info,
-                   double* dinfo) {
+                   double* dinfo, const double* lskip_dev) {
   rank_select_k<<<1, 32, 0, ctx->stream>>>(n, lam, sig, tol, delta_dev_in, rmax, kthr, info,
-                                           dinfo);
+                                           dinfo, lskip_dev);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }

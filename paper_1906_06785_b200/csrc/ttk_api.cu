@@ -371,11 +371,12 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
 }
 
 // SVD of Z = Y L (Y: M x R explicit, ld R; L: R x k, ld k; L == nullptr means identity with
-// k = R) by two-pass Gram-Jacobi.  Returns W (M x k), V2 (k x k), Vt = V V2 (k x k), lam
-// (k, descending eigenvalues of W^T W = squared singular values of Z).
+// k = R) by two-pass Gram-Jacobi, first part: pass 1 basis V (k x k, orthogonal),
+// W = Z V (M x k) and its Gram GW = W^T W.  pass2() finishes: lam (k, descending
+// eigenvalues of GW = squared singular values of Z), V2 (k x k), Vt = V V2.
 int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const double* Lm,
-                 int64_t k, DevBuf& W, DevBuf& V2, DevBuf& Vt, DevBuf& lam) {
-  DevBuf GY, GZ, T1, V, P;
+                 int64_t k, DevBuf& W, DevBuf& GW, DevBuf& V) {
+  DevBuf GY, GZ, T1, P, lam;
   TK_TRY(GZ.get(ctx, k * k));
   TagScope tag0(ctx, Lm ? "bond1.small" : "bond2.small");
   if (Lm) {
@@ -395,6 +396,7 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
   TK_TRY(V.get(ctx, k * k));
   TK_TRY(lam.get(ctx, k));
   TK_TRY(pass1_basis(ctx, (int)k, GZ.p, lam.p, V.p));
+  GZ.release();
   // W = Y (L V)
   const double* PV = V.p;
   if (Lm) {
@@ -407,17 +409,48 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
     TagScope t(ctx, Lm ? "bond1.form_W" : "bond2.form_W");
     TK_TRY(tk_dgemm(ctx, false, false, M, k, R, 1.0, Y, R, PV, k, 0.0, W.p, k));
   }
-  DevBuf GW;
   TK_TRY(GW.get(ctx, k * k));
   {
     TagScope t(ctx, Lm ? "bond1.gram_W" : "bond2.gram_W");
     TK_TRY(tk_dgemm(ctx, true, false, k, k, M, 1.0, W.p, k, W.p, k, 0.0, GW.p, k, true));
   }
+  return TK_OK;
+}
+
+int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, const double* lskip,
+          DevBuf& lam, DevBuf& V2, DevBuf& Vt) {
+  TK_TRY(lam.get(ctx, k));
   TK_TRY(V2.get(ctx, k * k));
   TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
-                       nullptr));
+                       nullptr, lskip));
   TK_TRY(Vt.get(ctx, k * k));
   TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
+  return TK_OK;
+}
+
+// pass 2 with the cluster skip, then the rank rule; if the chosen rank falls inside the
+// skipped cluster, pass 2 is redone without the skip (cluster skip).
+int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double tol,
+                   const double* delta_dev, int64_t rmax, DevBuf& lam, DevBuf& V2, DevBuf& Vt,
+                   DevBuf& sig, int* info, double* dinfo, int hinfo[3], double hd[3]) {
+  static const bool no_skip = getenv("TTK_NO_CLUSTER_SKIP") != nullptr;
+  DevBuf lsk;
+  const double* lskip = nullptr;
+  if (tol > 0.0 && !no_skip) {
+    TK_TRY(lsk.get(ctx, 1));
+    TK_TRY(tk_cluster_skip(ctx, (int)k, GW.p, tol, lsk.p));
+    lskip = lsk.p;
+  }
+  TK_TRY(sig.get(ctx, k));
+  for (int attempt = 0; attempt < 2; attempt++) {
+    TK_TRY(pass2(ctx, k, GW, V, lskip, lam, V2, Vt));
+    TK_TRY(tk_rank_select(ctx, (int)k, lam.p, sig.p, tol, delta_dev, rmax, kDropThr, info, dinfo,
+                          lskip));
+    TK_TRY(sync_read(ctx, hinfo, info, 3 * sizeof(int)));
+    TK_TRY(sync_read(ctx, hd, dinfo, 3 * sizeof(double)));
+    if (!lskip || hinfo[0] <= hinfo[2]) break;
+    lskip = nullptr;  // the cut fell inside the skipped cluster: resolve it fully
+  }
   return TK_OK;
 }
 
@@ -468,20 +501,20 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
     q2_id = false;
   }
   // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
-  DevBuf W, V2, Vt, lam;
-  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, V2, Vt, lam));
+  DevBuf W, GW1, V1, V2, Vt, lam;
+  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1));
   DevBuf sig1, scr;
-  TK_TRY(sig1.get(ctx, k2));
   TK_TRY(scr.get(ctx, 16));
   int* info1 = (int*)scr.p;
   double* dinfo1 = scr.p + 2;  // [norm, delta, discarded]
   int* info2 = (int*)(scr.p + 6);
   double* dinfo2 = scr.p + 8;
-  TK_TRY(tk_rank_select(ctx, (int)k2, lam.p, sig1.p, tol, nullptr, rmax, kDropThr, info1, dinfo1));
-  int hi1[2];
+  int hi1[3];
   double hd1[3];
-  TK_TRY(sync_read(ctx, hi1, info1, sizeof(hi1)));
-  TK_TRY(sync_read(ctx, hd1, dinfo1, sizeof(hd1)));
+  TK_TRY(pass2_and_rank(ctx, k2, GW1, V1, tol, nullptr, rmax, lam, V2, Vt, sig1, info1, dinfo1,
+                        hi1, hd1));
+  GW1.release();
+  V1.release();
   if (!std::isfinite(hd1[0])) {
     ctx->err = "tk_round: non-finite norm";
     return TK_ENUMERIC;
@@ -519,17 +552,14 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
     TK_TRY(tk_dgemm(ctx, true, true, r1, N2, k2, 1.0, S1.p, r1, Q2c.p, k2, 0.0, C.p, N2));
   }
   // ---- step E: SVD of C as (r1 n_xi) x k3, time bond truncation
-  DevBuf W2, V22, Vt2, lam2;
+  DevBuf W2, GW2, V21, V22, Vt2, lam2;
   const int64_t M2 = r1 * n_xi;
-  TK_TRY(svd_two_pass(ctx, M2, k3, C.p, nullptr, k3, W2, V22, Vt2, lam2));
+  TK_TRY(svd_two_pass(ctx, M2, k3, C.p, nullptr, k3, W2, GW2, V21));
   DevBuf sig2;
-  TK_TRY(sig2.get(ctx, k3));
-  TK_TRY(tk_rank_select(ctx, (int)k3, lam2.p, sig2.p, tol, dinfo1 + 1, rmax, kDropThr, info2,
-                        dinfo2));
-  int hi2[2];
+  int hi2[3];
   double hd2[3];
-  TK_TRY(sync_read(ctx, hi2, info2, sizeof(hi2)));
-  TK_TRY(sync_read(ctx, hd2, dinfo2, sizeof(hd2)));
+  TK_TRY(pass2_and_rank(ctx, k3, GW2, V21, tol, dinfo1 + 1, rmax, lam2, V22, Vt2, sig2, info2,
+                        dinfo2, hi2, hd2));
   const int64_t r2 = hi2[0];
   if (sigma2_out) {
     std::vector<double> s(k3);

@@ -127,8 +127,14 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   A: n x n symmetric (device, row-major, ld = n), destroyed.
 //   lam: n eigenvalues sorted DESCENDING; V: n x n eigenvectors (columns), row-major.
 //   A rotation on (p,q) is skipped when |a_pq| <= max(abs_tol, rel_tol*sqrt(|a_pp a_qq|)).
+//   lskip_dev (nullable device double): rotations between two indices whose diagonal entries
+//   are both <= *lskip_dev are skipped (cluster skip of the bond SVDs, see k_jacobi.cu).
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
-                  double rel_tol, int max_sweeps, int* sweeps_out);
+                  double rel_tol, int max_sweeps, int* sweeps_out,
+                  const double* lskip_dev = nullptr);
+// lskip for the cluster skip: the diagonal mass of A below it is <= delta^2/4,
+// delta^2 = tol^2 trace(A)/2.
+int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev);
 
 // Q (n x n, row-major, exactly orthogonal) of the blocked Householder QR of A (n x n).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
@@ -152,9 +158,10 @@ int tk_eye(tk_ctx* ctx, double* dst, int64_t n);
 //   sigma = sqrt(max(lam,0)) written to sig; info[0] = r (rule), info[1] = k (numerical dim
 //   sigma > kthr*sigma_0), dinfo[0] = ||sigma||, dinfo[1] = delta used, dinfo[2] = discarded.
 //   If delta_in < 0, delta = tol * ||sigma|| / sqrt(2) else delta = delta_in (device).
+//   info[2] = number of lam > *lskip_dev (n if lskip_dev is null).
 int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
                    const double* delta_dev_in, int64_t rmax, double kthr, int* info,
-                   double* dinfo);
+                   double* dinfo, const double* lskip_dev = nullptr);
 int tk_axpby_cores(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
                    const tk_tt* y, tk_tt* z);
 int tk_scale_rows(tk_ctx* ctx, double* U3, int64_t n, const double* s_dev, int invert);
