@@ -143,12 +143,16 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
         double c = 1.0, sn = 0.0, tt = 0.0;
         int act = 0;
         if (needs_rot(app, aqq, apq, abs_tol, a.rel_tol, lsk)) {
-          // t = sgn(d) e / (|d| + sqrt(d^2 + e^2)),  d = a_qq - a_pp, e = 2 a_pq
+          // t = sgn(d) e / u with u = |d| + sqrt(d^2 + e^2),  d = a_qq - a_pp, e = 2 a_pq;
+          // c = u / sqrt(u^2 + e^2), s = sgn(d) e / sqrt(u^2 + e^2): two dependent special
+          // functions (sqrt, then rsqrt and the division in parallel)
           const double d = aqq - app, e2 = 2.0 * apq;
-          const double rr = sqrt(fma(d, d, e2 * e2));
-          tt = (d >= 0.0 ? e2 : -e2) / (fabs(d) + rr);
-          c = rsqrt(fma(tt, tt, 1.0));
-          sn = tt * c;
+          const double es = d >= 0.0 ? e2 : -e2;
+          const double u = fabs(d) + sqrt(fma(d, d, e2 * e2));
+          const double rn = rsqrt(fma(u, u, e2 * e2));
+          tt = es / u;
+          c = u * rn;
+          sn = es * rn;
           act = 1;
           my_off = fmax(my_off, fabs(apq) * rsqrt(fmax(fabs(app * aqq), 1e-300)));
         }

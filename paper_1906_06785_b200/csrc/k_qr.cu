@@ -29,16 +29,29 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Factor the m x jb panel P (row-major, leading dimension ld, in global memory) in place.
-// Outputs: Vout (m x QB row-major, unit lower trapezoidal, zero padded), Tout (QB x QB).
-__global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restrict__ P,
-                                                 int64_t ld, double* __restrict__ Vout,
+// Factor the m x jb panel P (row-major, leading dimension ld).  SMEM: the panel is staged in
+// shared memory (stride QB+1: conflict-free column access); otherwise it is worked on in global
+// memory in place.  Outputs: Vout (m x QB row-major, unit lower trapezoidal, zero padded) and
+// Tout (QB x QB).  The R factor is not needed (only Q is used) and is not written back.
+template <bool SMEM>
+__global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restrict__ Pg,
+                                                 int64_t ldg, double* __restrict__ Vout,
                                                  double* __restrict__ Tout) {
+  extern __shared__ double psm[];
   __shared__ double red[QT / 32][QB + 1];
   __shared__ double s_tau[QB], s_w[QB], s_beta, s_scale;
   __shared__ double Ts[QB][QB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* P = SMEM ? psm : Pg;
+  const int64_t ld = SMEM ? (QB + 1) : ldg;
+  if (SMEM) {
+    for (int e = tid; e < m * QB; e += blockDim.x) {
+      const int i = e / QB, j = e % QB;
+      psm[i * (QB + 1) + j] = (j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
+    }
+  }
   for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
+  __syncthreads();
   for (int c = 0; c < jb; c++) {
     // ---- norm of x = P[c:, c]
     double s = 0.0;
@@ -54,16 +67,11 @@ __global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restri
       for (int w = 0; w < nw; w++) sig += red[w][0];
       double alpha = P[(int64_t)c * ld + c];
       double tau = 0.0, scale = 0.0, beta = alpha;
-      if (sig > 0.0 || alpha < 0.0) {
+      if (sig > 0.0) {
         double nrm = sqrt(alpha * alpha + sig);
         beta = alpha >= 0.0 ? -nrm : nrm;
         tau = (beta - alpha) / beta;
         scale = 1.0 / (alpha - beta);
-      }
-      if (c < m && sig == 0.0 && alpha >= 0.0) {
-        tau = 0.0;
-        scale = 0.0;
-        beta = alpha;
       }
       s_tau[c] = tau;
       s_beta = beta;
@@ -71,35 +79,29 @@ __global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restri
     }
     __syncthreads();
     const double tau = s_tau[c], scale = s_scale;
-    // ---- v = [1; x[1:] * scale] into P[c:, c] (below diagonal) and R diag
+    // ---- v = [1; x[1:] * scale] into P[c:, c] (below diagonal)
     for (int i = c + 1 + tid; i < m; i += blockDim.x) P[(int64_t)i * ld + c] *= scale;
     if (tid == 0) P[(int64_t)c * ld + c] = s_beta;
     __syncthreads();
     // ---- w_j = v^T P[c:, j] for j > c  and  z_l = V[:, l]^T v for l < c (T column)
-    // warp-parallel partial sums over rows, reduced through shared memory
     {
       double accw[QB], accz[QB];
 #pragma unroll
       for (int j = 0; j < QB; j++) accw[j] = accz[j] = 0.0;
       for (int i = c + tid; i < m; i += blockDim.x) {
-        const double vi = (i == c) ? 1.0 : P[(int64_t)i * ld + c];
         const double* row = P + (int64_t)i * ld;
+        const double vi = (i == c) ? 1.0 : row[c];
 #pragma unroll
         for (int j = 0; j < QB; j++) {
           if (j > c && j < jb) accw[j] += vi * row[j];
-          if (j < c) {
-            const double vl = (i == j) ? 1.0 : (i > j ? row[j] : 0.0);
-            accz[j] += vl * vi;
-          }
+          if (j < c) accz[j] += (i == j ? 1.0 : row[j]) * vi;
         }
       }
 #pragma unroll
       for (int j = 0; j < QB; j++) {
         double a = warp_sum(accw[j]);
         double b = warp_sum(accz[j]);
-        if (lane == 0) {
-          red[warp][j] = (j > c) ? a : b;
-        }
+        if (lane == 0) red[warp][j] = (j > c) ? a : b;
       }
     }
     __syncthreads();
@@ -117,14 +119,12 @@ __global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restri
       P[(int64_t)i * ld + j] -= tau * vi * s_w[j];
     }
     // ---- T column c (dlarft, forward, columnwise): T[0:c, c] = -tau T[0:c, 0:c] z
-    if (tid == 0) {
-      for (int l = 0; l < c; l++) {
-        double t = 0.0;
-        for (int q = l; q < c; q++) t += Ts[l][q] * s_w[q];
-        Ts[l][c] = -tau * t;
-      }
-      Ts[c][c] = tau;
+    if (tid < c) {
+      double t = 0.0;
+      for (int q = tid; q < c; q++) t += Ts[tid][q] * s_w[q];
+      Ts[tid][c] = -tau * t;
     }
+    if (tid == 0) Ts[c][c] = tau;
     __syncthreads();
   }
   // ---- export V (unit lower trapezoidal) and T
@@ -162,7 +162,19 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     double* Vp = Vb.p + (size_t)p * n * QB;
     double* Tp = Tb.p + (size_t)p * QB * QB;
     const int pid = tk_prof_begin(ctx, "qr_panel", 2.0 * m * (double)jb * jb, 0.0);
-    qr_panel_k<<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+    const size_t psmem = (size_t)m * (QB + 1) * sizeof(double);
+    if (psmem <= 200 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(qr_panel_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+      }
+      qr_panel_k<true><<<1, QT, psmem, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp,
+                                                       Tp);
+    } else {
+      qr_panel_k<false><<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+    }
     TK_LAUNCH_CHECK(ctx);
     tk_prof_end(ctx, pid);
     const int nt = n - (j0 + jb);
