@@ -63,6 +63,8 @@ class Clocks:
         self.lines = []
 
     def __enter__(self):
+        if self.gpu < 0:
+            return self
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -242,11 +244,11 @@ def run_ours(args, cfg, op, x):
     if world > 1:
         tdist.barrier()
     L = ttkmod.lib()
-    L.tk_ctx_profile(ctx._h, 1)
+    L.tk_ctx_profile(ctx._h, 0 if os.environ.get('TTK_BENCH_NOPROF') else 1)
     launches0 = ctx.launches
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    with Clocks(local) as clk:
+    with Clocks(-1 if os.environ.get('TTK_BENCH_NOCLOCKS') else local) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
             if flush is not None:
