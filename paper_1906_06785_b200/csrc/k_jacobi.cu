@@ -56,6 +56,10 @@ struct JacArgs {
   int* stats;           // rotation count per sweep
   unsigned long long* offmax;  // per sweep: max |a_pq|/sqrt(a_pp a_qq) over applied rotations
   double stop_rel;      // stop after a sweep whose offmax <= stop_rel (0: only when no rotation)
+  int n;                // real (unpadded) size
+  double rs_tol;        // rank-aware skip: tol of the rank rule (<= 0: off)
+  long long rs_rmax;    // rank cap of the rank rule (<= 0: none)
+  double* lskip_io;     // nullable: [0] in: static cluster threshold / out: effective one
   unsigned long long* tstamp;  // nullable: per-phase time sums of CTA 0 (TTK_DEBUG)
   int* sweeps_out;
 };
@@ -133,12 +137,24 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
   double my_off = 0.0;     // warp 0 lanes: largest relative coupling rotated away
   for (int sweep = 0; sweep < a.max_inner; sweep++) {
     int sweep_rot = 0;
-    for (int ir = 0; ir < JS - 1; ir++) {
+    // The first outer round of a sweep (r == 0, every block appears once) runs the full
+    // 63-round inner sweep; later rounds only rotate the 32 x 32 cross pairs (i in I, j in J):
+    // 32 inner rounds of 32 disjoint pairs.  Every index pair is still visited once per sweep.
+    const bool cross = (r != 0) && (a.npairs > 1);
+    const int nrounds = cross ? JB : JS - 1;
+    for (int ir = 0; ir < nrounds; ir++) {
       if (tid == 0) t_a = clock64();
       if (tid < JB) {
         const int k = tid;
-        const int pa = rr_player(k, ir, JS), pb = rr_player(JS - 1 - k, ir, JS);
-        const int p = min(pa, pb), q = max(pa, pb);
+        int p, q;
+        if (cross) {
+          p = k;
+          q = JB + (k + ir) % JB;
+        } else {
+          const int pa = rr_player(k, ir, JS), pb = rr_player(JS - 1 - k, ir, JS);
+          p = min(pa, pb);
+          q = max(pa, pb);
+        }
         const double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
         double c = 1.0, sn = 0.0, tt = 0.0;
         int act = 0;
@@ -358,11 +374,54 @@ __device__ void row_tile(const JacArgs& a, int col0, int t, int r, double* sm) {
   __syncthreads();
 }
 
+// CTA 0: lskip = (r + 32)-th largest diagonal entry, r = rank rule (tail of the clamped
+// diagonal <= delta^2 = tol^2 trace / 2, capped at rmax) — written to a.lskip_io[0].
+__device__ void rank_skip_update(const JacArgs& a, double* sm, double& sh_out) {
+  const int n = a.n;
+  double* d = sm;       // n values
+  double* srt = sm + n; // n values, descending
+  if (2 * n > 2 * JS * JLD) {
+    if (threadIdx.x == 0) a.lskip_io[0] = -1.0;
+    __syncthreads();
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    d[i] = fmax(a.G[(int64_t)i * a.n_pad + i], 0.0);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rk = 0;
+    const double di = d[i];
+    for (int j = 0; j < n; j++) rk += (d[j] > di) || (d[j] == di && j < i);
+    srt[rk] = di;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = n - 1; i >= 0; i--) tr += srt[i];
+    const double d2 = a.rs_tol * a.rs_tol * tr * 0.5;
+    int r = n;
+    double tail = 0.0;
+    for (int cand = n; cand >= 1; cand--) {
+      if (tail <= d2)
+        r = cand;
+      else
+        break;
+      tail += srt[cand - 1];
+    }
+    if (a.rs_rmax > 0 && r > a.rs_rmax) r = (int)a.rs_rmax;
+    const int idx = r + 32;
+    a.lskip_io[0] = idx < n ? srt[idx] : -1.0;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
   extern __shared__ double sm[];
   __shared__ InnerShared sh;
   const double abs_tol = fmax(a.abs_scale * a.d_maxdiag[0], 1e-300);
-  const double lsk = a.lskip ? a.lskip[0] : -1.0;
+  const double lsk_static = a.lskip ? a.lskip[0] : -1.0;
+  double lsk = lsk_static;
+  __shared__ double sh_lsk;
   const int rtiles = a.n_pad / JS;
   unsigned long long tsum[6] = {0, 0, 0, 0, 0, 0}, tprev = 0;
   const bool rec = a.tstamp && blockIdx.x == 0 && threadIdx.x == 0;
@@ -376,6 +435,14 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
   };
   int sweep = 0;
   for (; sweep < a.max_sweeps; sweep++) {
+    if (a.rs_tol > 0.0 && sweep > 0 && a.lskip_io) {
+      // rank-aware skip: indices whose diagonal lies below the (r + 32)-th largest current
+      // diagonal, r the rank rule applied to the current diagonal, only matter through their
+      // trace; their mutual rotations are skipped from now on (checked after convergence)
+      if (blockIdx.x == 0) rank_skip_update(a, sm, sh_lsk);
+      if (coop) cg::this_grid().sync(); else __syncthreads();
+      lsk = fmax(lsk_static, *((volatile double*)a.lskip_io));
+    }
     JacArgs as = a;
     as.stats = a.stats + sweep;
     as.offmax = a.offmax + sweep;
@@ -411,7 +478,10 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
       break;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.sweeps_out[0] = sweep;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.sweeps_out[0] = sweep;
+    if (a.lskip_io) a.lskip_io[0] = lsk;  // effective final threshold
+  }
   if (rec)
     for (int k = 0; k < 6; k++) a.tstamp[k] = tsum[k];  // [6], [7]: inner phase cycles
 }
@@ -459,7 +529,7 @@ __global__ void max_abs_diag_k(int n, const double* A, double* out) {
 // lskip = largest diagonal value of the set of smallest diagonal entries whose total is
 // <= frac * delta^2, delta^2 = tol^2 * trace / 2  (-1 if that set is empty).
 __global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, double frac,
-                               double* out) {
+                               long long rmax, double* out) {
   extern __shared__ double d[];
   __shared__ double tr;
   for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = fmax(A[(int64_t)i * n + i], 0.0);
@@ -478,7 +548,23 @@ __global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const double lim = frac * tol * tol * tr * 0.5;
+    double lim = frac * tol * tol * tr * 0.5;
+    // when rmax binds the kept set ends near the rmax-th largest value, which can lie below
+    // delta^2: keep the cluster's mass (a bound on its largest eigenvalue) under a quarter of
+    // the current rmax-th largest diagonal entry as well
+    if (rmax > 0 && rmax <= n) lim = fmin(lim, 0.25 * d[n + (n - rmax)]);
+    // if the rank rule on the current diagonal already exceeds rmax, rmax will bind and the
+    // kept set may reach below any useful cluster: no skip (the redo would cost more)
+    if (rmax > 0) {
+      const double d2 = tol * tol * tr * 0.5;
+      double c2 = 0.0;
+      int cnt = 0;
+      while (cnt < n && c2 + d[n + cnt] <= d2) c2 += d[n + cnt++];
+      if (n - cnt > rmax) {
+        out[0] = -1.0;
+        return;
+      }
+    }
     double cum = 0.0, l = -1.0;
     for (int i = 0; i < n; i++) {
       cum += d[n + i];
@@ -489,9 +575,60 @@ __global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, 
   }
 }
 
+// Safety check of a skipped run: the kept eigenvalues (diagonal > lskip) must all exceed the
+// Gershgorin bound of the unresolved block (diagonal <= lskip), so that the kept set is the
+// dominant invariant subspace.  io[1] = 1.0 if so (or nothing was skipped), else 0.0.
+__global__ void __launch_bounds__(512) skip_check_k(int n, int n_pad,
+                                                    const double* __restrict__ G, double* io) {
+  // lambda_max(D) <= min(max Gershgorin radius, trace(D), ||D||_F) for the PSD block D
+  __shared__ double r_mn[512], r_g[512], r_tr[512], r_fr[512];
+  const double l = io[0];
+  double mn = 1e308, gx = -1e308, tr = 0.0, fr = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double di = G[(int64_t)i * n_pad + i];
+    if (di > l) {
+      mn = fmin(mn, di);
+    } else {
+      double g = di;
+      tr += fmax(di, 0.0);
+      fr += di * di;
+      for (int j = 0; j < n; j++) {
+        if (j == i) continue;
+        const double dj = G[(int64_t)j * n_pad + j];
+        if (dj <= l) {
+          const double v = G[(int64_t)i * n_pad + j];
+          g += fabs(v);
+          fr += v * v;
+        }
+      }
+      gx = fmax(gx, g);
+    }
+  }
+  r_mn[threadIdx.x] = mn;
+  r_g[threadIdx.x] = gx;
+  r_tr[threadIdx.x] = tr;
+  r_fr[threadIdx.x] = fr;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      r_mn[threadIdx.x] = fmin(r_mn[threadIdx.x], r_mn[threadIdx.x + st]);
+      r_g[threadIdx.x] = fmax(r_g[threadIdx.x], r_g[threadIdx.x + st]);
+      r_tr[threadIdx.x] += r_tr[threadIdx.x + st];
+      r_fr[threadIdx.x] += r_fr[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const bool nod = r_g[0] == -1e308;
+    const double bound = fmin(r_g[0], fmin(r_tr[0], sqrt(r_fr[0])));
+    io[1] = (l < 0.0 || nod || r_mn[0] > bound) ? 1.0 : 0.0;
+  }
+}
+
 }  // namespace
 
-int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev) {
+int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev,
+                    int64_t rmax) {
   size_t smem = 2 * (size_t)n * sizeof(double);
   if (smem > 200 * 1024) {
     // too large for the shared-memory sort: no skipping (always safe)
@@ -499,13 +636,14 @@ int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lsk
   }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(cluster_skip_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cluster_skip_k<<<1, 512, smem, ctx->stream>>>(n, A, tol, 0.25, lskip_dev);
+  cluster_skip_k<<<1, 512, smem, ctx->stream>>>(n, A, tol, 0.25, (long long)rmax, lskip_dev);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
 
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
-                  double rel_tol, int max_sweeps, int* sweeps_out, const double* lskip_dev) {
+                  double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev,
+                  double rs_tol, int64_t rs_rmax) {
   if (n <= 0) return TK_OK;
   const int n_pad = ((n + JS - 1) / JS) * JS;
   const int nb = n_pad / JB;
@@ -552,6 +690,10 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   a.abs_scale = abs_tol_scale;
   a.rel_tol = rel_tol;
   a.lskip = lskip_dev;
+  a.lskip_io = lskip_dev;
+  a.n = n;
+  a.rs_tol = (lskip_dev && getenv("TTK_RANK_SKIP")) ? rs_tol : 0.0;
+  a.rs_rmax = rs_rmax;
   a.offmax = offmax;
   // relative mode: a sweep whose largest applied relative coupling is <= 1e-10 leaves
   // couplings of O(1e-20) behind (quadratic convergence): stop after it
@@ -584,6 +726,10 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   int sg = (int)std::min<int64_t>((n + 127) / 128, 4LL * ctx->num_sms);
   eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, Gp.p, Vp.p, lam, V);
   TK_LAUNCH_CHECK(ctx);
+  if (lskip_dev) {
+    skip_check_k<<<1, 512, 0, ctx->stream>>>(n, n_pad, Gp.p, lskip_dev);
+    TK_LAUNCH_CHECK(ctx);
+  }
   tk_prof_end(ctx, prof_id);
   if (sweeps_out || getenv("TTK_DEBUG")) {
     int sw = 0;

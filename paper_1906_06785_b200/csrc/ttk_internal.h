@@ -127,14 +127,18 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   A: n x n symmetric (device, row-major, ld = n), destroyed.
 //   lam: n eigenvalues sorted DESCENDING; V: n x n eigenvectors (columns), row-major.
 //   A rotation on (p,q) is skipped when |a_pq| <= max(abs_tol, rel_tol*sqrt(|a_pp a_qq|)).
-//   lskip_dev (nullable device double): rotations between two indices whose diagonal entries
-//   are both <= *lskip_dev are skipped (cluster skip of the bond SVDs, see k_jacobi.cu).
+//   lskip_dev (nullable device double[2]): rotations between two indices whose diagonal
+//   entries are both <= the skip threshold are skipped (cluster skip of the bond SVDs, see
+//   k_jacobi.cu).  In: [0] static threshold.  With rs_tol > 0 the threshold is also raised
+//   each sweep to the (r + 32)-th largest diagonal (r = rank rule with rs_tol, rs_rmax).
+//   Out: [0] effective threshold, [1] 1.0 if the kept set passed the Gershgorin check.
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
-                  double rel_tol, int max_sweeps, int* sweeps_out,
-                  const double* lskip_dev = nullptr);
+                  double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev = nullptr,
+                  double rs_tol = 0.0, int64_t rs_rmax = 0);
 // lskip for the cluster skip: the diagonal mass of A below it is <= delta^2/4,
 // delta^2 = tol^2 trace(A)/2.
-int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev);
+int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev,
+                    int64_t rmax = 0);
 
 // Q (n x n, row-major, exactly orthogonal) of the blocked Householder QR of A (n x n).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
