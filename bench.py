@@ -203,6 +203,22 @@ def run_reference(args, cfg, op, x):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- multi-rank
+def max_over_ranks(value: float, device: str) -> float:
+    """All-reduce MAX of a per-rank timing (the slowest replica defines the job time)."""
+    import torch
+    import torch.distributed as tdist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(world: int, steps: int, max_total_ms: float) -> float:
+    """Whole-job ops/s of N independent replicas: every rank ran `steps` ops; the job took the
+    max-over-ranks time (weak scaling)."""
+    return world * 1000.0 * steps / max_total_ms
+
+
 # ----------------------------------------------------------------------------- our arm
 def workload_config(cfg, op):
     return {"workload": f"{cfg.name}: apply+round", "n_x": op.n_x, "n_xi": op.n_xi, "n_t": op.n_t,
@@ -264,9 +280,7 @@ def run_ours(args, cfg, op, x):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms, "cuda")
         tdist.barrier()
     ranks_out = y.ranks
 
@@ -360,7 +374,7 @@ def run_ours(args, cfg, op, x):
     if rank == 0:
         ms_per_step = total_ms / args.steps
         line = {
-            "metric": METRIC, "value": world * 1000.0 * args.steps / total_ms, "unit": UNIT,
+            "metric": METRIC, "value": replica_throughput(world, args.steps, total_ms), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(cfg, op), "ranks_out": list(ranks_out),

@@ -1,0 +1,95 @@
+"""Full-size (BASELINE.json config c4) checks, in the launch configuration bench.py times.
+
+The CPU oracle cannot round c4 in test time (~4 minutes on 8 cores), so:
+  * apply: sampled outputs the oracle computes one by one — rows of Y1 = [K_k U1] at random
+    spatial indices, and the small cores Y2, Y3 in full — compared element by element;
+  * round: properties that hold at any size — orthonormal U1 and reshape(U2), the norm
+    identity ||x||^2 = ||x~||^2 + disc_1^2 + disc_2^2 (nested orthogonal projections), the
+    error bound sqrt(disc_1^2 + disc_2^2) <= tol ||x|| unless rmax binds, the rank rule on the
+    reported singular values (R4), descending kept singular values, ranks <= rmax;
+  * the reported ||x|| equals sqrt(<y, y>) computed by the oracle from the GPU apply output's
+    own cores (oracle dot on exact-parity cores).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1906_06785_b200 as ttk  # noqa: E402
+from oracle import tt as otT  # noqa: E402
+from synth.configs import CONFIGS  # noqa: E402
+from synth.operator import build_operator  # noqa: E402
+from synth.tt import make_input_tt  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def c4():
+    cfg = CONFIGS["c4"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    gop = ttk.Operator.from_kronsum(op)
+    y = ttk.tt_apply_op(gop, ttk.TT.from_cores(*x))
+    torch.cuda.synchronize()
+    return cfg, op, x, gop, y
+
+
+def test_c4_apply_sampled_rows(c4):
+    cfg, op, x, gop, y = c4
+    r1 = cfg.ranks[0]
+    rng = np.random.default_rng(4)
+    rows = np.unique(np.concatenate([rng.integers(0, op.n_x, 256), [0, op.n_x - 1]]))
+    Y1 = y.U1[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    for k, term in enumerate(op.terms):
+        ref = term.K[rows] @ x[0]                           # oracle: K_k[i, :] U1 row by row
+        got = Y1[:, k * r1:(k + 1) * r1]
+        assert np.max(np.abs(got - ref)) <= 1e-13 * max(np.max(np.abs(ref)), 1e-300), k
+    # small cores in full against the oracle's apply of the small factors
+    y2o = np.zeros((op.T * r1, op.n_xi, op.T * cfg.ranks[1]))
+    y3o = np.zeros((op.T * cfg.ranks[1], op.n_t))
+    r2 = cfg.ranks[1]
+    for k, term in enumerate(op.terms):
+        y2o[k * r1:(k + 1) * r1, :, k * r2:(k + 1) * r2] = np.einsum("ij,ajb->aib", term.G, x[1])
+        y3o[k * r2:(k + 1) * r2] = x[2] @ term.T_dense().T
+    assert np.max(np.abs(y.U2.cpu().numpy() - y2o)) <= 1e-13 * np.max(np.abs(y2o))
+    assert np.max(np.abs(y.U3.cpu().numpy() - y3o)) <= 1e-13 * np.max(np.abs(y3o))
+
+
+def test_c4_round_properties(c4):
+    cfg, op, x, gop, y = c4
+    ycores = y.cores_numpy()
+    nrm_o = otT.norm(ycores)                                 # oracle dot on the apply output
+    g = ttk.TT.from_cores(*ycores)
+    g, info = ttk.tt_round(g, cfg.tol, cfg.rmax, want_info=True)
+    r1, r2 = g.ranks
+    assert 1 <= r1 <= cfg.rmax and 1 <= r2 <= cfg.rmax
+    assert info.norm == pytest.approx(nrm_o, rel=1e-12)
+    u1 = g.U1
+    e1 = torch.linalg.matrix_norm(u1.T @ u1 - torch.eye(r1, dtype=torch.float64, device="cuda"),
+                                  ord=float("inf")).item()
+    m2 = g.U2.reshape(-1, r2)
+    e2 = torch.linalg.matrix_norm(m2.T @ m2 - torch.eye(r2, dtype=torch.float64, device="cuda"),
+                                  ord=float("inf")).item()
+    assert e1 <= 1e-10 and e2 <= 1e-10
+    # nested orthogonal projections: ||x||^2 = ||x~||^2 + disc1^2 + disc2^2
+    n_new = torch.linalg.norm(g.U3).item()
+    d1, d2 = info.discarded
+    assert n_new ** 2 + d1 ** 2 + d2 ** 2 == pytest.approx(nrm_o ** 2, rel=1e-10)
+    # rank rule on the reported spectra (R4), with the rmax cap
+    delta = cfg.tol * info.norm / math.sqrt(2.0)
+    for s, r in ((info.sigma1, r1), (info.sigma2, r2)):
+        s = np.asarray(s)
+        s = s[s > 0]
+        assert np.all(np.diff(s[:r]) <= 1e-12 * s[0])        # descending kept values
+        tail_r = math.sqrt(float(np.sum(s[r:] ** 2)))
+        if r < cfg.rmax:
+            assert tail_r <= delta * (1 + 1e-12)
+            if r > 1:
+                assert math.sqrt(float(np.sum(s[r - 1:] ** 2))) > delta * (1 - 1e-12)
+    if r1 < cfg.rmax and r2 < cfg.rmax:
+        assert math.sqrt(d1 ** 2 + d2 ** 2) <= cfg.tol * info.norm * (1 + 1e-12)
