@@ -50,6 +50,7 @@ struct JacArgs {
   double* Qb;
   double* Sb;
   const double* d_maxdiag;
+  const double* abs_floor;  // nullable: absolute skip floor (rounding-noise level of the data)
   double abs_scale, rel_tol;
   const double* lskip;  // nullable
   int max_inner, max_sweeps;
@@ -418,7 +419,8 @@ __device__ void rank_skip_update(const JacArgs& a, double* sm, double& sh_out) {
 __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
   extern __shared__ double sm[];
   __shared__ InnerShared sh;
-  const double abs_tol = fmax(a.abs_scale * a.d_maxdiag[0], 1e-300);
+  const double abs_tol =
+      fmax(fmax(a.abs_scale * a.d_maxdiag[0], a.abs_floor ? a.abs_floor[0] : 0.0), 1e-300);
   const double lsk_static = a.lskip ? a.lskip[0] : -1.0;
   double lsk = lsk_static;
   __shared__ double sh_lsk;
@@ -643,7 +645,7 @@ int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lsk
 
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev,
-                  double rs_tol, int64_t rs_rmax) {
+                  double rs_tol, int64_t rs_rmax, const double* abs_floor_dev) {
   if (n <= 0) return TK_OK;
   const int n_pad = ((n + JS - 1) / JS) * JS;
   const int nb = n_pad / JB;
@@ -687,6 +689,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   a.Qb = Qb.p;
   a.Sb = Sb.p;
   a.d_maxdiag = d_maxdiag;
+  a.abs_floor = abs_floor_dev;
   a.abs_scale = abs_tol_scale;
   a.rel_tol = rel_tol;
   a.lskip = lskip_dev;

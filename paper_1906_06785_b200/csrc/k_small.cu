@@ -172,6 +172,32 @@ __global__ void dot_final_k(int64_t n, const double* __restrict__ a, const doubl
 }
 
 __global__ void set_scalar_k(double* dst, double v) { dst[0] = v; }
+
+// trace of an n x n matrix (row-major) and ||P||_F^2 (nP entries), then the noise floor
+__global__ void noise_floor_k(const double* __restrict__ G, int64_t n, double gscale,
+                              const double* __restrict__ P, int64_t nP, int64_t K, int64_t k,
+                              double* out) {
+  __shared__ double r1[256], r2[256];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += G[i * n + i];
+  if (P)
+    for (int64_t i = threadIdx.x; i < nP; i += blockDim.x) b += P[i] * P[i];
+  r1[threadIdx.x] = a;
+  r2[threadIdx.x] = b;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      r1[threadIdx.x] += r1[threadIdx.x + st];
+      r2[threadIdx.x] += r2[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double eps = 2.220446049250313e-16;
+    const double pf2 = P ? r2[0] : (double)k;
+    out[0] = 16.0 * eps * eps * (double)K * (gscale * r1[0]) * pf2 / (double)k;
+  }
+}
 __global__ void neg_scalar_k(const double* src, double* dst) { dst[0] = -src[0]; }
 
 __global__ void transpose_k(int64_t rows, int64_t cols, const double* __restrict__ src,
@@ -207,6 +233,12 @@ __global__ void symmetrize_k(int64_t n, double* A) {
 
 }  // namespace
 
+int tk_noise_floor(tk_ctx* ctx, const double* trG_src, int64_t n_trG, double trG_scale,
+                   const double* P, int64_t nP, int64_t K, int64_t k, double* out) {
+  noise_floor_k<<<1, 256, 0, ctx->stream>>>(trG_src, n_trG, trG_scale, P, nP, K, k, out);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
 int tk_neg_scalar(tk_ctx* ctx, const double* src, double* dst) {
   neg_scalar_k<<<1, 1, 0, ctx->stream>>>(src, dst);
   TK_LAUNCH_CHECK(ctx);

@@ -342,12 +342,15 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
   // W = A^T V  (N x R)
   TK_TRY(W.get(ctx, N * R));
   TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
-  // pass 2: GW = W^T W, relative eigen-decomposition
+  // pass 2: GW = W^T W, relative eigen-decomposition down to the rounding-noise floor of W
   TK_TRY(GW.get(ctx, R * R));
   TK_TRY(tk_dgemm(ctx, true, false, R, R, N, 1.0, W.p, R, W.p, R, 0.0, GW.p, R, true));
   TK_TRY(V2.get(ctx, R * R));
+  DevBuf floor;
+  TK_TRY(floor.get(ctx, 1));
+  TK_TRY(tk_noise_floor(ctx, G.p, R, 1.0, nullptr, 0, R, R, floor.p));
   TK_TRY(tk_jacobi_eig(ctx, (int)R, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel,
-                       kMaxSweeps, nullptr));
+                       kMaxSweeps, nullptr, nullptr, 0.0, 0, floor.p));
   TK_TRY(sig.get(ctx, R));
   TK_TRY(scr.get(ctx, 8));
   int* info = (int*)scr.p;
@@ -375,16 +378,26 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
 // k = R) by two-pass Gram-Jacobi, first part: pass 1 basis V (k x k, orthogonal),
 // W = Z V (M x k) and its Gram GW = W^T W.  pass2() finishes: lam (k, descending
 // eigenvalues of GW = squared singular values of Z), V2 (k x k), Vt = V V2.
+// floor (out, 1 device double): rounding-noise level of G_W entries for pass 2's skip test.
 int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const double* Lm,
-                 int64_t k, DevBuf& W, DevBuf& GW, DevBuf& V) {
+                 int64_t k, DevBuf& W, DevBuf& GW, DevBuf& V, DevBuf& floor) {
   DevBuf GY, GZ, T1, P, lam;
   TK_TRY(GZ.get(ctx, k * k));
+  TK_TRY(floor.get(ctx, 1));
+  int64_t s = 1;
   TagScope tag0(ctx, Lm ? "bond1.small" : "bond2.small");
   if (Lm) {
     TK_TRY(GY.get(ctx, R * R));
     {
+      // Pass 1 only has to supply an orthogonal basis that roughly follows the dominant
+      // directions (accuracy comes from pass 2 on the explicit W), so its Gram is taken over
+      // a strided sample of >= 8R rows (every s-th spatial row, s <= 16): 1/s of the flops
+      // with the same pass-2 convergence.
+      static const bool full = getenv("TTK_FULL_PASS1_GRAM") != nullptr;
+      s = full ? 1 : std::max<int64_t>(1, std::min<int64_t>(16, M / (8 * R)));
       TagScope t(ctx, "bond1.gram_Y");
-      TK_TRY(tk_dgemm(ctx, true, false, R, R, M, 1.0, Y, R, Y, R, 0.0, GY.p, R, true));
+      TK_TRY(tk_dgemm(ctx, true, false, R, R, (M + s - 1) / s, 1.0, Y, R * s, Y, R * s, 0.0, GY.p,
+                      R, true));
     }
     TK_TRY(T1.get(ctx, R * k));
     TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, GY.p, R, Lm, k, 0.0, T1.p, k));
@@ -397,14 +410,18 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
   TK_TRY(V.get(ctx, k * k));
   TK_TRY(lam.get(ctx, k));
   TK_TRY(pass1_basis(ctx, (int)k, GZ.p, lam.p, V.p));
-  GZ.release();
   // W = Y (L V)
   const double* PV = V.p;
   if (Lm) {
     TK_TRY(P.get(ctx, R * k));
     TK_TRY(tk_dgemm(ctx, false, false, R, k, k, 1.0, Lm, k, V.p, k, 0.0, P.p, k));
     PV = P.p;
+    // ||Y||_F^2 ~ s * trace(sampled Gram); P = L V
+    TK_TRY(tk_noise_floor(ctx, GY.p, R, (double)s, P.p, R * k, R, k, floor.p));
+  } else {
+    TK_TRY(tk_noise_floor(ctx, GZ.p, k, 1.0, nullptr, 0, R, k, floor.p));  // P = V orthogonal
   }
+  GZ.release();
   TK_TRY(W.get(ctx, M * k));
   {
     TagScope t(ctx, Lm ? "bond1.form_W" : "bond2.form_W");
@@ -419,11 +436,12 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
 }
 
 int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double* lskip,
-          double rs_tol, int64_t rs_rmax, DevBuf& lam, DevBuf& V2, DevBuf& Vt) {
+          double rs_tol, int64_t rs_rmax, const double* floor, DevBuf& lam, DevBuf& V2,
+          DevBuf& Vt) {
   TK_TRY(lam.get(ctx, k));
   TK_TRY(V2.get(ctx, k * k));
   TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
-                       nullptr, lskip, rs_tol, rs_rmax));
+                       nullptr, lskip, rs_tol, rs_rmax, floor));
   TK_TRY(Vt.get(ctx, k * k));
   TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
   return TK_OK;
@@ -432,9 +450,10 @@ int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double* lsk
 // pass 2 with the cluster skip and the rank-aware skip (k_jacobi.cu), then the rank rule.  If
 // the chosen rank falls inside the skipped set, or the kept set fails the Gershgorin check,
 // pass 2 is redone without any skip.
-int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double tol,
-                   const double* delta_dev, int64_t rmax, DevBuf& lam, DevBuf& V2, DevBuf& Vt,
-                   DevBuf& sig, int* info, double* dinfo, int hinfo[3], double hd[3]) {
+int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V,
+                   const DevBuf& floor, double tol, const double* delta_dev, int64_t rmax,
+                   DevBuf& lam, DevBuf& V2, DevBuf& Vt, DevBuf& sig, int* info, double* dinfo,
+                   int hinfo[3], double hd[3]) {
   // The cluster skip is opt-in (TTK_CLUSTER_SKIP=1): on the c4 spectra its certificate
   // (kept eigenvalues above the skipped block's Gershgorin/trace/Frobenius bound) fails often
   // enough that the redo costs more than the skip saves (profiles/r01/README.md).
@@ -449,7 +468,7 @@ int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, do
   }
   TK_TRY(sig.get(ctx, k));
   for (int attempt = 0; attempt < 2; attempt++) {
-    TK_TRY(pass2(ctx, k, GW, V, lskip, no_rank_skip ? 0.0 : tol, rmax, lam, V2, Vt));
+    TK_TRY(pass2(ctx, k, GW, V, lskip, no_rank_skip ? 0.0 : tol, rmax, floor.p, lam, V2, Vt));
     TK_TRY(tk_rank_select(ctx, (int)k, lam.p, sig.p, tol, delta_dev, rmax, kDropThr, info, dinfo,
                           lskip));
     TK_TRY(sync_read(ctx, hinfo, info, 3 * sizeof(int)));
@@ -513,8 +532,8 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
     q2_id = false;
   }
   // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
-  DevBuf W, GW1, V1, V2, Vt, lam;
-  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1));
+  DevBuf W, GW1, V1, V2, Vt, lam, fl1;
+  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1, fl1));
   DevBuf sig1, scr;
   TK_TRY(scr.get(ctx, 16));
   int* info1 = (int*)scr.p;
@@ -523,8 +542,8 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
   double* dinfo2 = scr.p + 8;
   int hi1[3];
   double hd1[3];
-  TK_TRY(pass2_and_rank(ctx, k2, GW1, V1, tol, nullptr, rmax, lam, V2, Vt, sig1, info1, dinfo1,
-                        hi1, hd1));
+  TK_TRY(pass2_and_rank(ctx, k2, GW1, V1, fl1, tol, nullptr, rmax, lam, V2, Vt, sig1, info1,
+                        dinfo1, hi1, hd1));
   GW1.release();
   V1.release();
   if (!std::isfinite(hd1[0])) {
@@ -564,14 +583,14 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
     TK_TRY(tk_dgemm(ctx, true, true, r1, N2, k2, 1.0, S1.p, r1, Q2c.p, k2, 0.0, C.p, N2));
   }
   // ---- step E: SVD of C as (r1 n_xi) x k3, time bond truncation
-  DevBuf W2, GW2, V21, V22, Vt2, lam2;
+  DevBuf W2, GW2, V21, V22, Vt2, lam2, fl2;
   const int64_t M2 = r1 * n_xi;
-  TK_TRY(svd_two_pass(ctx, M2, k3, C.p, nullptr, k3, W2, GW2, V21));
+  TK_TRY(svd_two_pass(ctx, M2, k3, C.p, nullptr, k3, W2, GW2, V21, fl2));
   DevBuf sig2;
   int hi2[3];
   double hd2[3];
-  TK_TRY(pass2_and_rank(ctx, k3, GW2, V21, tol, dinfo1 + 1, rmax, lam2, V22, Vt2, sig2, info2,
-                        dinfo2, hi2, hd2));
+  TK_TRY(pass2_and_rank(ctx, k3, GW2, V21, fl2, tol, dinfo1 + 1, rmax, lam2, V22, Vt2, sig2,
+                        info2, dinfo2, hi2, hd2));
   const int64_t r2 = hi2[0];
   if (sigma2_out) {
     std::vector<double> s(k3);

@@ -134,7 +134,13 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   Out: [0] effective threshold, [1] 1.0 if the kept set passed the Gershgorin check.
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev = nullptr,
-                  double rs_tol = 0.0, int64_t rs_rmax = 0);
+                  double rs_tol = 0.0, int64_t rs_rmax = 0,
+                  const double* abs_floor_dev = nullptr);
+// Rounding-noise floor of a pass-2 Gram W^T W with W = fl(Y P) (K = inner dimension, k = its
+// columns): tau = (4 eps)^2 K (trG_scale * trG[0]) ||P||_F^2 / k, written to out[0] (device).
+// P == nullptr means an orthogonal P (||P||_F^2 = k).
+int tk_noise_floor(tk_ctx* ctx, const double* trG_src, int64_t n_trG, double trG_scale,
+                   const double* P, int64_t nP, int64_t K, int64_t k, double* out);
 // lskip for the cluster skip: the diagonal mass of A below it is <= delta^2/4,
 // delta^2 = tol^2 trace(A)/2.
 int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev,
