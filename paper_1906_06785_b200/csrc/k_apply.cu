@@ -18,7 +18,7 @@
 namespace {
 
 template <int RPL>
-__global__ void __launch_bounds__(256) spmm_multi_k(int64_t n_x, int T, int r,
+__global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t n_x, int T, int r,
                                                     const int32_t* __restrict__ rowptr,
                                                     const int32_t* __restrict__ col,
                                                     const double* __restrict__ val,
@@ -30,39 +30,106 @@ __global__ void __launch_bounds__(256) spmm_multi_k(int64_t n_x, int T, int r,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t R = (int64_t)T * r;
   constexpr int CW = 32 * RPL;  // columns per chunk
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int UNR = 4;        // entries whose U1 rows are loaded together (memory-level parallelism)
   for (int64_t i = warp; i < n_x; i += nwarps) {
     double* yrow = Y1 + i * R;
-    for (int k = 0; k < T; k++) {
-      const int32_t* rp = rowptr + (int64_t)k * (n_x + 1);
-      const int64_t base = nnz_off[k];
-      const int beg = rp[i], end = rp[i + 1];
+    // Terms in groups of 32: lane k fetches the CSR extent of term kg0 + k for this row, so the
+    // T row-pointer loads are issued in parallel instead of as T dependent chains.
+    for (int kg0 = 0; kg0 < T; kg0 += 32) {
+      const int kn = min(32, T - kg0);
+      int64_t mybeg = 0;
+      int mycnt = 0;
+      if (lane < kn) {
+        const int32_t* rp = rowptr + (int64_t)(kg0 + lane) * (n_x + 1);
+        const int b = __ldg(rp + i), e = __ldg(rp + i + 1);
+        mybeg = nnz_off[kg0 + lane] + b;
+        mycnt = e - b;
+      }
+      int myoff = mycnt;  // inclusive scan -> exclusive offsets of each term's entries
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, myoff, o);
+        if (lane >= o) myoff += t;
+      }
+      const int E = __shfl_sync(FULL, myoff, 31);
+      myoff -= mycnt;
       for (int c0 = 0; c0 < r; c0 += CW) {
         double acc[RPL];
 #pragma unroll
         for (int u = 0; u < RPL; u++) acc[u] = 0.0;
-        for (int e0 = beg; e0 < end; e0 += 32) {
+        int cur = -1;  // term (within the group) whose sum is in acc
+        for (int e0 = 0; e0 < E; e0 += 32) {
+          // lane j gathers entry e0 + j of the row's concatenated term lists
+          const int g = e0 + lane;
+          int myk = kn;
+          int64_t src = 0;
+          for (int k = 0; k < kn; k++) {
+            const int ok = __shfl_sync(FULL, myoff, k), ck = __shfl_sync(FULL, mycnt, k);
+            const int64_t bk = __shfl_sync(FULL, mybeg, k);
+            if (g >= ok && g < ok + ck) {
+              myk = k;
+              src = bk + (g - ok);
+            }
+          }
           int myc = 0;
           double myv = 0.0;
-          if (e0 + lane < end) {
-            myc = __ldg(col + base + e0 + lane);
-            myv = __ldg(val + base + e0 + lane);
+          if (g < E) {
+            myc = __ldg(col + src);
+            myv = __ldg(val + src);
           }
-          const int cnt = min(32, end - e0);
-          for (int q = 0; q < cnt; q++) {
-            const int c = __shfl_sync(0xffffffffu, myc, q);
-            const double v = __shfl_sync(0xffffffffu, myv, q);
-            const double* urow = U1 + (int64_t)c * r + c0;
+          const int cnt = min(32, E - e0);
+          for (int q0 = 0; q0 < cnt; q0 += UNR) {
+            double uv[UNR][RPL];
+            double vv[UNR];
+            int kk[UNR];
 #pragma unroll
-            for (int u = 0; u < RPL; u++) {
-              const int cc = lane + 32 * u;
-              if (c0 + cc < r) acc[u] = fma(v, __ldg(urow + cc), acc[u]);
+            for (int s = 0; s < UNR; s++) {
+              const int q = min(q0 + s, 31);
+              const int c = __shfl_sync(FULL, myc, q);
+              vv[s] = __shfl_sync(FULL, myv, q);
+              kk[s] = (q0 + s < cnt) ? __shfl_sync(FULL, myk, q) : -2;
+              const double* urow = U1 + (int64_t)c * r + c0;
+#pragma unroll
+              for (int u = 0; u < RPL; u++) {
+                const int cc = lane + 32 * u;
+                uv[s][u] = (kk[s] >= 0 && c0 + cc < r) ? __ldg(urow + cc) : 0.0;
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < UNR; s++) {
+              if (kk[s] == -2) break;
+              if (kk[s] != cur) {
+                if (cur >= 0) {
+#pragma unroll
+                  for (int u = 0; u < RPL; u++) {
+                    const int cc = lane + 32 * u;
+                    if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + cur) * r + c0 + cc, acc[u]);
+                    acc[u] = 0.0;
+                  }
+                }
+                cur = kk[s];
+              }
+#pragma unroll
+              for (int u = 0; u < RPL; u++) acc[u] = fma(vv[s], uv[s][u], acc[u]);
             }
           }
         }
+        if (cur >= 0) {
 #pragma unroll
-        for (int u = 0; u < RPL; u++) {
-          const int cc = lane + 32 * u;
-          if (c0 + cc < r) yrow[(int64_t)k * r + c0 + cc] = acc[u];
+          for (int u = 0; u < RPL; u++) {
+            const int cc = lane + 32 * u;
+            if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + cur) * r + c0 + cc, acc[u]);
+          }
+        }
+        // terms with no entry in this row
+        for (int k = 0; k < kn; k++) {
+          if (__shfl_sync(FULL, mycnt, k) != 0) continue;
+#pragma unroll
+          for (int u = 0; u < RPL; u++) {
+            const int cc = lane + 32 * u;
+            if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + k) * r + c0 + cc, 0.0);
+          }
         }
       }
     }

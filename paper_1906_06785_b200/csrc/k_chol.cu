@@ -1,0 +1,298 @@
+// Pivoted Cholesky (diagonal pivoting, LAPACK dpstrf semantics) of a symmetric positive
+// semi-definite fp64 matrix, and the small triangular helpers of the CholeskyQR2 basis used by
+// orth_rows:
+//
+//   H = P R^T R P^T      R: k x n upper trapezoidal in pivot order, k = numerical rank
+//
+// R is returned in ORIGINAL column indexing, Ro[t, piv[c]] = R[t, c], so that the trailing
+// update never moves data: Ro P = R, and H ~ Ro^T Ro.  The factorisation stops when the largest
+// remaining Schur-complement diagonal is <= tol.
+//
+// Blocked right-looking: a panel of nb pivot steps runs in ONE CTA (the Schur diagonal and the
+// panel's rows of Ro live in shared memory); a step is an argmax and one row
+//     Ro[j, c] = (Hw[p, c] - sum_{t in panel, t < j} Ro[t, p] Ro[t, c]) / sqrt(d_p)
+// ), then the whole working matrix takes the panel's rank-NB update Hw -= Ro_panel^T Ro_panel
+// on the DMMA GEMM (symmetric mode).  Rows of the pivots already taken receive meaningless
+// updates but are never read again (their d is retired).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <math.h>
+
+#include <algorithm>
+
+#include "ttk_internal.h"
+
+namespace {
+
+constexpr int PT = 512;  // threads of the panel kernel
+
+// Panel of nb pivot steps (one CTA).  Shared memory: the panel's rows of Ro for every column
+// (sR[t * n + c], t < nb), the live Schur diagonal sd[c] and the retired flags.
+__global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int pivot,
+                                                    const double* __restrict__ Hw,
+                                                    double* __restrict__ Ro, int* __restrict__ piv,
+                                                    int* __restrict__ state,
+                                                    const double* __restrict__ tol_dev) {
+  // state[0]: rank so far / final (k); state[1]: 1 once stopped; state[2 + c]: retired flags
+  extern __shared__ double psm[];
+  double* sR = psm;                 // nb x n
+  double* sd = psm + (int64_t)nb * n;  // n
+  __shared__ double s_val[PT / 32];
+  __shared__ int s_idx[PT / 32];
+  __shared__ int s_p;
+  __shared__ double s_dmax;
+  if (state[1]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = tol_dev[0];
+  int* retired = state + 2;
+  // retired columns carry d = -inf, so they never win the argmax
+  for (int c = tid; c < n; c += PT) sd[c] = retired[c] ? -INFINITY : Hw[(int64_t)c * n + c];
+  __syncthreads();
+  for (int s = 0; s < nb; s++) {
+    const int j = j0 + s;
+    if (j >= n) break;
+    // (a) pivot: argmax of the live Schur diagonal (ties -> smaller index); without pivoting
+    // the next index in order
+    double bv = -INFINITY;
+    int bi = 0x7fffffff;
+    if (!pivot) {
+      if (tid == 0) {
+        s_p = j;
+        s_dmax = sd[j];
+      }
+      __syncthreads();
+    }
+    for (int c = tid; pivot && c < n; c += PT) {
+      const double v = sd[c];
+      if (v > bv) {  // ascending c per thread: strict > keeps the smaller index on ties
+        bv = v;
+        bi = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (pivot && lane == 0) {
+      s_val[warp] = bv;
+      s_idx[warp] = bi;
+    }
+    if (pivot) __syncthreads();
+    if (pivot && warp == 0) {
+      bv = lane < PT / 32 ? s_val[lane] : -INFINITY;
+      bi = lane < PT / 32 ? s_idx[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        s_dmax = bv;
+      }
+    }
+    if (pivot) __syncthreads();
+    const int p = s_p;
+    const double dmax = s_dmax;
+    if (!(dmax > tol) || p >= n) {  // uniform: rank reached (or nothing left / non-finite)
+      if (tid == 0) {
+        state[0] = j;
+        state[1] = 1;
+      }
+      return;
+    }
+    const double r = sqrt(dmax), rinv = 1.0 / r;
+    // (b) row j of Ro:  Ro[j, c] = (Hw[p, c] - sum_{t < s} sR[t, p] sR[t, c]) / r
+    const double* hrow = Hw + (int64_t)p * n;
+    double* orow = Ro + (int64_t)j * n;
+    for (int c = tid; c < n; c += PT) {
+      double out;
+      if (c == p) {
+        out = r;
+      } else if (sd[c] == -INFINITY) {
+        out = 0.0;
+      } else {
+        double v = hrow[c];
+        for (int t = 0; t < s; t++) v = fma(-sR[t * n + p], sR[t * n + c], v);
+        out = v * rinv;
+        sd[c] = fma(-out, out, sd[c]);
+      }
+      orow[c] = out;
+      sR[s * n + c] = out;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      sd[p] = -INFINITY;
+      retired[p] = 1;
+      piv[j] = p;
+      state[0] = j + 1;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void max_diag_tol_k(int n, const double* __restrict__ H, double rel,
+                               const double* __restrict__ abs_dev, double* __restrict__ tol) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, H[(int64_t)i * n + i]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double t = rel * red[0];
+    if (abs_dev) t = fmax(t, abs_dev[0]);
+    // strictly positive: a zero pivot never enters
+    tol[0] = fmax(t, 1e-300);
+  }
+}
+
+// X = R^{-1} for the k x k upper triangular R (row-major, leading dimension ldr); one warp per
+// column j of X (back substitution, the column kept in shared memory).  X is upper triangular,
+// written in full (zeros below the diagonal).
+constexpr int TI_WARPS = 4;
+__global__ void __launch_bounds__(32 * TI_WARPS) tri_inv_k(int k, const double* __restrict__ R,
+                                                           int64_t ldr, double* __restrict__ X,
+                                                           int64_t ldx) {
+  extern __shared__ double xcol[];  // TI_WARPS columns of length k
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * TI_WARPS + w;
+  if (j >= k) return;
+  double* x = xcol + (int64_t)w * k;
+  for (int i = lane; i < k; i += 32) x[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) x[j] = 1.0 / R[(int64_t)j * ldr + j];
+  __syncwarp();
+  for (int i = j - 1; i >= 0; i--) {
+    const double* ri = R + (int64_t)i * ldr;
+    double s = 0.0;
+    for (int l = i + 1 + lane; l <= j; l += 32) s = fma(ri[l], x[l], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[i] = -s / ri[i];
+    __syncwarp();
+  }
+  for (int i = lane; i < k; i += 32) X[(int64_t)i * ldx + j] = x[i];
+}
+
+// gather columns: out[t, c] = Ro[t, piv[c]]   (rows x k)
+__global__ void gather_cols_k(int64_t rows, int k, const double* __restrict__ Ro, int64_t ldr,
+                              const int* __restrict__ piv, double* __restrict__ out) {
+  const int64_t total = rows * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / k;
+    const int c = (int)(e % k);
+    out[e] = Ro[t * ldr + piv[c]];
+  }
+}
+
+// scatter rows: S[piv[i], :] = X[i, :] for i < k, other rows of S zero  (S: n x cols)
+__global__ void scatter_rows_k(int64_t n, int k, int64_t cols, const double* __restrict__ X,
+                               const int* __restrict__ piv, double* __restrict__ S) {
+  const int64_t total = (int64_t)k * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols);
+    const int64_t c = e % cols;
+    S[(int64_t)piv[i] * cols + c] = X[e];
+  }
+}
+
+int grid_for(tk_ctx* ctx, int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 8LL * ctx->num_sms));
+}
+
+}  // namespace
+
+int tk_pchol_max_n() { return 4096; }
+
+int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* tol_abs_dev,
+             double* Ro, int* piv, int* state, bool pivot) {
+  if (n <= 0) return TK_OK;
+  if (n > tk_pchol_max_n()) {
+    ctx->err = "tk_pchol: n too large";
+    return TK_EARG;
+  }
+  TagScope tag(ctx, "pchol");
+  DevBuf Hw, tol;
+  TK_TRY(Hw.get(ctx, (size_t)n * n));
+  TK_TRY(tol.get(ctx, 1));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(Hw.p, H, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemsetAsync(Ro, 0, sizeof(double) * n * n, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemsetAsync(state, 0, (2 + (size_t)n) * sizeof(int), ctx->stream));
+  max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
+  TK_LAUNCH_CHECK(ctx);
+  // panel width: the panel rows of Ro (nb x n) and the diagonal stay in shared memory
+  const int nb = (int)std::max<int64_t>(4, std::min<int64_t>(32, (200 * 1024 / 8) / n - 1));
+  const size_t smem = ((size_t)nb + 1) * n * sizeof(double);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaFuncSetAttribute(pchol_panel_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
+  for (int j0 = 0; j0 < n; j0 += nb) {
+    pchol_panel_k<<<1, PT, smem, ctx->stream>>>(n, j0, nb, pivot ? 1 : 0, Hw.p, Ro, piv,
+                                                  state, tol.p);
+    TK_LAUNCH_CHECK(ctx);
+    const int jb = std::min(nb, n - j0);
+    if (j0 + jb < n) {
+      // Hw -= Ro[j0:j0+jb, :]^T Ro[j0:j0+jb, :]   (rows of a stopped panel are zero: no-op)
+      TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
+                      Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true));
+    }
+  }
+  tk_prof_end(ctx, pid);
+  return TK_OK;
+}
+
+int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx) {
+  if (k <= 0) return TK_OK;
+  const size_t smem = (size_t)TI_WARPS * k * sizeof(double);
+  if (smem > 200 * 1024) {
+    ctx->err = "tk_tri_inv: k too large";
+    return TK_EARG;
+  }
+  static int attr = 0;
+  if (smem > 48 * 1024 && (size_t)attr < smem) {
+    cudaFuncSetAttribute(tri_inv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = (int)smem;
+  }
+  tri_inv_k<<<(k + TI_WARPS - 1) / TI_WARPS, 32 * TI_WARPS, smem, ctx->stream>>>(k, R, ldr, X,
+                                                                                  ldx);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+int tk_gather_cols(tk_ctx* ctx, int64_t rows, int k, const double* Ro, int64_t ldr, const int* piv,
+                   double* out) {
+  if (rows <= 0 || k <= 0) return TK_OK;
+  gather_cols_k<<<grid_for(ctx, rows * k), 256, 0, ctx->stream>>>(rows, k, Ro, ldr, piv, out);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+
+int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X, const int* piv,
+                    double* S) {
+  if (n <= 0 || cols <= 0) return TK_OK;
+  TK_CUDA_TRY(ctx, cudaMemsetAsync(S, 0, sizeof(double) * n * cols, ctx->stream));
+  if (k <= 0) return TK_OK;
+  scatter_rows_k<<<grid_for(ctx, (int64_t)k * cols), 256, 0, ctx->stream>>>(n, k, cols, X, piv, S);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

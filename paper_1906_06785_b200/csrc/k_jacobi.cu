@@ -31,6 +31,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ttk_internal.h"
 
@@ -577,20 +578,20 @@ __global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, 
   }
 }
 
-// Safety check of a skipped run: the kept eigenvalues (diagonal > lskip) must all exceed the
-// Gershgorin bound of the unresolved block (diagonal <= lskip), so that the kept set is the
-// dominant invariant subspace.  io[1] = 1.0 if so (or nothing was skipped), else 0.0.
+// Safety check of a skipped run: io[1] = an upper bound on the largest eigenvalue of the
+// unresolved block D (indices with diagonal <= lskip), or -1 if nothing was skipped.  The caller
+// accepts the run iff every KEPT eigenvalue (the r chosen by the rank rule, all resolved)
+// exceeds it: then the kept set is the dominant invariant subspace and the discarded tail,
+// which contains all of D, is exact through trace(D).
 __global__ void __launch_bounds__(512) skip_check_k(int n, int n_pad,
                                                     const double* __restrict__ G, double* io) {
   // lambda_max(D) <= min(max Gershgorin radius, trace(D), ||D||_F) for the PSD block D
-  __shared__ double r_mn[512], r_g[512], r_tr[512], r_fr[512];
+  __shared__ double r_g[512], r_tr[512], r_fr[512];
   const double l = io[0];
-  double mn = 1e308, gx = -1e308, tr = 0.0, fr = 0.0;
+  double gx = -1e308, tr = 0.0, fr = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double di = G[(int64_t)i * n_pad + i];
-    if (di > l) {
-      mn = fmin(mn, di);
-    } else {
+    if (di <= l) {
       double g = di;
       tr += fmax(di, 0.0);
       fr += di * di;
@@ -606,14 +607,12 @@ __global__ void __launch_bounds__(512) skip_check_k(int n, int n_pad,
       gx = fmax(gx, g);
     }
   }
-  r_mn[threadIdx.x] = mn;
   r_g[threadIdx.x] = gx;
   r_tr[threadIdx.x] = tr;
   r_fr[threadIdx.x] = fr;
   __syncthreads();
   for (int st = blockDim.x / 2; st > 0; st >>= 1) {
     if (threadIdx.x < st) {
-      r_mn[threadIdx.x] = fmin(r_mn[threadIdx.x], r_mn[threadIdx.x + st]);
       r_g[threadIdx.x] = fmax(r_g[threadIdx.x], r_g[threadIdx.x + st]);
       r_tr[threadIdx.x] += r_tr[threadIdx.x + st];
       r_fr[threadIdx.x] += r_fr[threadIdx.x + st];
@@ -623,7 +622,7 @@ __global__ void __launch_bounds__(512) skip_check_k(int n, int n_pad,
   if (threadIdx.x == 0) {
     const bool nod = r_g[0] == -1e308;
     const double bound = fmin(r_g[0], fmin(r_tr[0], sqrt(r_fr[0])));
-    io[1] = (l < 0.0 || nod || r_mn[0] > bound) ? 1.0 : 0.0;
+    io[1] = (l < 0.0 || nod) ? -1.0 : bound;
   }
 }
 
@@ -753,6 +752,13 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
               ts[5] / rounds / 1e3);
       fprintf(stderr, "[ttk]    inner round cycles: params %.0f  update %.0f\n",
               ts[6] / rounds / 63.0, ts[7] / rounds / 63.0);
+      std::vector<int> rot(sw);
+      std::vector<double> om(sw);
+      TK_CUDA_TRY(ctx, cudaMemcpy(rot.data(), stats, sizeof(int) * sw, cudaMemcpyDeviceToHost));
+      TK_CUDA_TRY(ctx, cudaMemcpy(om.data(), offmax, sizeof(double) * sw, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[ttk]    per sweep rotations/offmax:");
+      for (int s = 0; s < sw; s++) fprintf(stderr, " %d/%.1e", rot[s], om[s]);
+      fprintf(stderr, "\n");
     }
   }
   return TK_OK;

@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -25,10 +26,32 @@ int tk_alloc(tk_ctx* ctx, void** p, size_t bytes) {
     *p = nullptr;
     return TK_ECUDA;
   }
+  ctx->live[*p] = bytes;
+  ctx->live_bytes += bytes;
+  ctx->high_bytes = std::max(ctx->high_bytes, ctx->live_bytes);
   return TK_OK;
 }
 void tk_free(tk_ctx* ctx, void* p) {
-  if (p) cudaFreeAsync(p, ctx->stream);
+  if (!p) return;
+  auto it = ctx->live.find(p);
+  if (it != ctx->live.end()) {
+    ctx->live_bytes -= it->second;
+    ctx->live.erase(it);
+  }
+  cudaFreeAsync(p, ctx->stream);
+}
+
+// Called at the end of the top-level entry points.  Once the scratch high-water mark of a call
+// is known, the stream-ordered pool is given one free block of 1.5x that size: later calls
+// carve their scratch from it instead of mapping new memory mid-call (a pool growth costs
+// hundreds of ms at the c4 sizes and showed up as step-time outliers, profiles/r01/README.md).
+static void pool_settle(tk_ctx* ctx) {
+  if (ctx->high_bytes <= ctx->reserved_for) return;
+  const size_t want = ctx->high_bytes + ctx->high_bytes / 2;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess) cudaFreeAsync(p, ctx->stream);
+  cudaGetLastError();  // a failed reservation is not an error: growth just stays on demand
+  ctx->reserved_for = want;
 }
 
 // ============================================================================ context
@@ -342,9 +365,68 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
   // W = A^T V  (N x R)
   TK_TRY(W.get(ctx, N * R));
   TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
-  // pass 2: GW = W^T W, relative eigen-decomposition down to the rounding-noise floor of W
   TK_TRY(GW.get(ctx, R * R));
   TK_TRY(tk_dgemm(ctx, true, false, R, R, N, 1.0, W.p, R, W.p, R, 0.0, GW.p, R, true));
+  static const bool jac2 = getenv("TTK_ORTH_JACOBI") != nullptr;
+  if (!jac2 && R <= tk_pchol_max_n()) {
+    // pass 2: CholeskyQR2 with diagonal pivoting on the graded W:
+    //   W P1 = Q1 R1 (pivoted Cholesky of W^T W, truncated at the numerical rank k1),
+    //   Q1 = W P1 R1^{-1},  Q1 = Q2 R2 (second pass: restores orthonormality to O(eps)),
+    //   A = L Q2^T  with  L = V (Ro2 Ro1)^T  (Ro = R P^T in original column indexing).
+    DevBuf Ro1, pv1, st1, R11, X1, S1, Q1, G2, Ro2, pv2, st2, R22, X2, S2, M;
+    TK_TRY(Ro1.get(ctx, R * R));
+    TK_TRY(pv1.get(ctx, (R + 1) / 2));
+    TK_TRY(st1.get(ctx, (R + 3) / 2));
+    TK_TRY(tk_pchol(ctx, (int)R, GW.p, kDropThr * kDropThr, nullptr, Ro1.p, (int*)pv1.p,
+                    (int*)st1.p));
+    int k1 = 0;
+    TK_TRY(sync_read(ctx, &k1, st1.p, sizeof(int)));
+    if (k1 > 0) {
+      TK_TRY(R11.get(ctx, (int64_t)k1 * k1));
+      TK_TRY(tk_gather_cols(ctx, k1, k1, Ro1.p, R, (const int*)pv1.p, R11.p));
+      TK_TRY(X1.get(ctx, (int64_t)k1 * k1));
+      TK_TRY(tk_tri_inv(ctx, k1, R11.p, k1, X1.p, k1));
+      TK_TRY(S1.get(ctx, R * k1));
+      TK_TRY(tk_scatter_rows(ctx, R, k1, k1, X1.p, (const int*)pv1.p, S1.p));
+      TK_TRY(Q1.get(ctx, N * k1));
+      TK_TRY(tk_dgemm(ctx, false, false, N, k1, R, 1.0, W.p, R, S1.p, k1, 0.0, Q1.p, k1));
+      W.release();
+      TK_TRY(G2.get(ctx, (int64_t)k1 * k1));
+      TK_TRY(tk_dgemm(ctx, true, false, k1, k1, N, 1.0, Q1.p, k1, Q1.p, k1, 0.0, G2.p, k1, true));
+      TK_TRY(Ro2.get(ctx, (int64_t)k1 * k1));
+      TK_TRY(pv2.get(ctx, (k1 + 1) / 2));
+      TK_TRY(st2.get(ctx, (k1 + 3) / 2));
+      // no pivoting in the second pass: Q1's columns are already in the importance order of
+      // the first pass, which L = V (Ro2 Ro1)^T inherits (bond 1's pass 1 relies on it)
+      TK_TRY(tk_pchol(ctx, k1, G2.p, kDropThr * kDropThr, nullptr, Ro2.p, (int*)pv2.p,
+                      (int*)st2.p, false));
+      int k2 = 0;
+      TK_TRY(sync_read(ctx, &k2, st2.p, sizeof(int)));
+      if (k2 > 0) {
+        TK_TRY(R22.get(ctx, (int64_t)k2 * k2));
+        TK_TRY(tk_gather_cols(ctx, k2, k2, Ro2.p, k1, (const int*)pv2.p, R22.p));
+        TK_TRY(X2.get(ctx, (int64_t)k2 * k2));
+        TK_TRY(tk_tri_inv(ctx, k2, R22.p, k2, X2.p, k2));
+        TK_TRY(S2.get(ctx, (int64_t)k1 * k2));
+        TK_TRY(tk_scatter_rows(ctx, k1, k2, k2, X2.p, (const int*)pv2.p, S2.p));
+        TK_TRY(Qc.get(ctx, N * k2));
+        TK_TRY(tk_dgemm(ctx, false, false, N, k2, k1, 1.0, Q1.p, k1, S2.p, k2, 0.0, Qc.p, k2));
+        // M = Ro2[:k2] Ro1[:k1]  (k2 x R);  L = V M^T  (R x k2)
+        TK_TRY(M.get(ctx, (int64_t)k2 * R));
+        TK_TRY(tk_dgemm(ctx, false, false, k2, R, k1, 1.0, Ro2.p, k1, Ro1.p, R, 0.0, M.p, R));
+        TK_TRY(L.get(ctx, R * k2));
+        TK_TRY(tk_dgemm(ctx, false, true, R, k2, R, 1.0, V.p, R, M.p, R, 0.0, L.p, k2));
+        *k_out = k2;
+        return TK_OK;
+      }
+    }
+    // zero (or numerically zero) A: the Jacobi path below handles it as before
+    if (!W.p) {
+      TK_TRY(W.get(ctx, N * R));
+      TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
+    }
+  }
+  // pass 2: relative eigen-decomposition of GW down to the rounding-noise floor of W
   TK_TRY(V2.get(ctx, R * R));
   DevBuf floor;
   TK_TRY(floor.get(ctx, 1));
@@ -474,14 +556,20 @@ int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V,
     TK_TRY(sync_read(ctx, hinfo, info, 3 * sizeof(int)));
     TK_TRY(sync_read(ctx, hd, dinfo, 3 * sizeof(double)));
     if (!lskip) break;
-    double io[2];
+    double io[2], lam_r = 0.0;
     TK_TRY(sync_read(ctx, io, lskip, sizeof(io)));
-    if (hinfo[0] <= hinfo[2] && io[1] == 1.0) break;
+    if (hinfo[0] >= 1) TK_TRY(sync_read(ctx, &lam_r, lam.p + (hinfo[0] - 1), sizeof(double)));
+    // accept iff the kept eigenvalues are all resolved and all exceed the unresolved block's
+    // largest eigenvalue (bound io[1]; -1 when nothing was skipped)
+    if (hinfo[0] <= hinfo[2] && (io[1] < 0.0 || lam_r > io[1])) break;
     if (getenv("TTK_DEBUG"))
-      fprintf(stderr, "[ttk] skip check failed (r=%d resolved=%d gersh_ok=%g): redo\n", hinfo[0],
-              hinfo[2], io[1]);
+      fprintf(stderr, "[ttk] skip check failed (r=%d resolved=%d lam_r=%.3e bound=%.3e): redo\n",
+              hinfo[0], hinfo[2], lam_r, io[1]);
     lskip = nullptr;  // resolve everything
   }
+  if (getenv("TTK_DEBUG"))
+    fprintf(stderr, "[ttk] pass2 k=%lld r=%d numerical_dim=%d resolved=%d skip=%d\n",
+            (long long)k, hinfo[0], hinfo[1], hinfo[2], lskip ? 1 : 0);
   return TK_OK;
 }
 
@@ -496,9 +584,19 @@ int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
 
 }  // namespace
 
+static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                      double* sigma2_out, double* discarded_out, double* norm_out);
+
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
   if (!ctx) return TK_EARG;
+  const int st = round_impl(ctx, x, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out);
+  pool_settle(ctx);
+  return st;
+}
+
+static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                      double* sigma2_out, double* discarded_out, double* norm_out) {
   TK_TRY(check_tt(ctx, x, "tk_round"));
   if (!(tol >= 0.0) || !std::isfinite(tol)) {
     ctx->err = "tk_round: tol must be finite and >= 0";

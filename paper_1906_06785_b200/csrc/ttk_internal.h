@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ttk.h"
@@ -31,6 +32,9 @@ struct tk_ctx {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  // scratch accounting (tk_alloc / tk_free) and the pool reservation made from it
+  std::unordered_map<void*, size_t> live;
+  size_t live_bytes = 0, high_bytes = 0, reserved_for = 0;
 };
 
 // Scoped phase tag for profiling records.
@@ -148,6 +152,21 @@ int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lsk
 
 // Q (n x n, row-major, exactly orthogonal) of the blocked Householder QR of A (n x n).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
+// Pivoted Cholesky H = P R^T R P^T of the n x n PSD H (k_chol.cu).  Ro (n x n, zeroed rows
+// >= k): R in ORIGINAL column indexing, Ro[t, piv[c]] = R[t, c], so H ~ Ro^T Ro.  Stops when the
+// largest remaining Schur diagonal <= max(tol_rel * max diag(H), *tol_abs_dev).  piv (n ints):
+// pivot order (identity when !pivot).  state (2 + n ints, device): state[0] = k on completion.
+int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* tol_abs_dev,
+             double* Ro, int* piv, int* state, bool pivot = true);
+int tk_pchol_max_n();
+// X = R^{-1} for the k x k upper triangular R.
+int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx);
+// out[t, c] = Ro[t, piv[c]]  (rows x k, ld k)
+int tk_gather_cols(tk_ctx* ctx, int64_t rows, int k, const double* Ro, int64_t ldr, const int* piv,
+                   double* out);
+// S (n x cols) = 0 except S[piv[i], :] = X[i, :] for i < k
+int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X, const int* piv,
+                    double* S);
 
 // Apply kernels
 int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1);
