@@ -7,9 +7,9 @@
 // orthogonality of Q matters for accuracy (Householder: ||Q^T Q - I|| = O(eps)).
 //
 // Panel (width QB = 16) factorised by one CTA (LAPACK dgeqr2 + dlarft: reflectors v_c, tau_c
-// and the compact-WY factor T with H_1..H_QB = I - V T V^T); trailing update and the
-// backward accumulation of Q use the DMMA GEMM (tk_dgemm):
-//   A[j0:, j1:] -= V (T^T (V^T A[j0:, j1:]))        Q[j0:, j0:] -= V (T (V^T Q[j0:, j0:]))
+// and the compact-WY factor T with H_1..H_QB = I - V T V^T; the panel kernel also emits V T and
+// V T^T); trailing update and the backward accumulation of Q are two DMMA GEMMs each:
+//   A[j0:, j1:] -= (V T^T) (V^T A[j0:, j1:])        Q[j0:, j0:] -= (V T) (V^T Q[j0:, j0:])
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -142,61 +142,165 @@ __global__ void __launch_bounds__(QT) qr_panel_k(int m, int jb, double* __restri
   for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
 }
 
+// Warp-per-column panel factorisation (panel staged in shared memory, stride QB+1): warp j owns
+// column j.  Per column c: warp c forms the reflector (norm, tau, v = x / (alpha - beta)); after
+// one barrier every warp j > c computes w_j = v^T P[c:, j] and updates its own column, and every
+// warp j < c computes z_j = V[:, j]^T v for the T factor (dlarft); after a second barrier warp 0
+// forms T[0:c, c] = -tau T[0:c, 0:c] z.  Two barriers per column, no block-wide reductions.
+__global__ void __launch_bounds__(32 * QB)
+    qr_panel_warp_k(int m, int jb, const double* __restrict__ Pg, int64_t ldg,
+                    double* __restrict__ Vout, double* __restrict__ Tout,
+                    double* __restrict__ VTout, double* __restrict__ VTtout) {
+  extern __shared__ double psm[];
+  __shared__ double s_tau[QB], s_z[QB];
+  __shared__ double Ts[QB][QB + 1];
+  constexpr int LD = QB + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < m * QB; e += blockDim.x) {
+    const int i = e / QB, j = e % QB;
+    psm[i * LD + j] = (j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
+  }
+  for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < jb; c++) {
+    if (warp == c) {
+      double s = 0.0;
+      for (int i = c + 1 + lane; i < m; i += 32) {
+        const double v = psm[i * LD + c];
+        s = fma(v, v, s);
+      }
+      s = warp_sum(s);
+      const double alpha = psm[c * LD + c];
+      double tau = 0.0, scale = 0.0, beta = alpha;
+      if (s > 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, s));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int i = c + 1 + lane; i < m; i += 32) psm[i * LD + c] *= scale;
+      if (lane == 0) {
+        psm[c * LD + c] = beta;  // R entry (unused); v_c = 1 is implicit below
+        s_tau[c] = tau;
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau[c];
+    if (warp > c && warp < jb) {
+      const int j = warp;
+      double w = lane == 0 ? psm[c * LD + j] : 0.0;  // row c (v_c = 1), counted once
+      for (int i = c + 1 + lane; i < m; i += 32) w = fma(psm[i * LD + c], psm[i * LD + j], w);
+      w = warp_sum(w) * tau;
+      if (lane == 0) psm[c * LD + j] -= w;
+      for (int i = c + 1 + lane; i < m; i += 32) psm[i * LD + j] = fma(-w, psm[i * LD + c], psm[i * LD + j]);
+    } else if (warp < c) {
+      const int j = warp;
+      // z_j = V[:, j]^T v over rows >= c (v is zero above c; V[c, j] is stored below diag j)
+      double z = lane == 0 ? psm[c * LD + j] : 0.0;  // row c (v_c = 1), counted once
+      for (int i = c + 1 + lane; i < m; i += 32) z = fma(psm[i * LD + j], psm[i * LD + c], z);
+      z = warp_sum(z);
+      if (lane == 0) s_z[j] = z;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane < c) {
+        double t = 0.0;
+        for (int q = lane; q < c; q++) t = fma(Ts[lane][q], s_z[q], t);
+        Ts[lane][c] = -tau * t;
+      }
+      if (lane == 0) Ts[c][c] = tau;
+    }
+  }
+  __syncthreads();
+  // V (unit lower trapezoidal) into shared memory in place, then V, V T and V T^T out
+  for (int e = tid; e < m * QB; e += blockDim.x) {
+    const int i = e / QB, j = e % QB;
+    double v = 0.0;
+    if (j < jb) {
+      if (i == j)
+        v = 1.0;
+      else if (i > j)
+        v = psm[i * LD + j];
+    }
+    psm[i * LD + j] = v;
+    Vout[e] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * QB; e += blockDim.x) {
+    const int i = e / QB, j = e % QB;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int q = 0; q < QB; q++) {
+      const double v = psm[i * LD + q];
+      a = fma(v, Ts[q][j], a);
+      b = fma(v, Ts[j][q], b);
+    }
+    VTout[e] = a;
+    VTtout[e] = b;
+  }
+  for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
+}
+
 }  // namespace
 
 // Q (n x n, row-major) from the Householder QR of A (n x n, row-major; A is not modified).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   if (n <= 0) return TK_OK;
   TagScope tag(ctx, "qr_pass1.gemm");
-  DevBuf Aw, Vb, Tb, W1, W2;
+  DevBuf Aw, Vb, Tb, VTb, VTtb, W1;
   TK_TRY(Aw.get(ctx, (size_t)n * n));
   TK_CUDA_TRY(ctx, cudaMemcpyAsync(Aw.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
                                    ctx->stream));
   const int np = (n + QB - 1) / QB;
-  TK_TRY(Vb.get(ctx, (size_t)np * n * QB));  // panel p: (n - j0) x QB at offset p*n*QB
+  // panel p: V, V T, V T^T as (n - j0) x QB at offset p*n*QB;  T: QB x QB
+  TK_TRY(Vb.get(ctx, (size_t)np * n * QB));
+  TK_TRY(VTb.get(ctx, (size_t)np * n * QB));
+  TK_TRY(VTtb.get(ctx, (size_t)np * n * QB));
   TK_TRY(Tb.get(ctx, (size_t)np * QB * QB));
   TK_TRY(W1.get(ctx, (size_t)QB * n));
-  TK_TRY(W2.get(ctx, (size_t)QB * n));
   for (int p = 0; p < np; p++) {
     const int j0 = p * QB, jb = std::min(QB, n - j0), m = n - j0;
     double* Vp = Vb.p + (size_t)p * n * QB;
+    double* VTp = VTb.p + (size_t)p * n * QB;
+    double* VTtp = VTtb.p + (size_t)p * n * QB;
     double* Tp = Tb.p + (size_t)p * QB * QB;
     const int pid = tk_prof_begin(ctx, "qr_panel", 2.0 * m * (double)jb * jb, 0.0);
     const size_t psmem = (size_t)m * (QB + 1) * sizeof(double);
     if (psmem <= 200 * 1024) {
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(qr_panel_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(qr_panel_warp_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
         attr = true;
       }
-      qr_panel_k<true><<<1, QT, psmem, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp,
-                                                       Tp);
+      qr_panel_warp_k<<<1, 32 * QB, psmem, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n,
+                                                          Vp, Tp, VTp, VTtp);
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
     } else {
       qr_panel_k<false><<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
+      TK_TRY(tk_dgemm(ctx, false, false, m, QB, QB, 1.0, Vp, QB, Tp, QB, 0.0, VTp, QB));
+      TK_TRY(tk_dgemm(ctx, false, true, m, QB, QB, 1.0, Vp, QB, Tp, QB, 0.0, VTtp, QB));
     }
-    TK_LAUNCH_CHECK(ctx);
-    tk_prof_end(ctx, pid);
     const int nt = n - (j0 + jb);
     if (nt > 0) {
+      // A_t <- H_p^T A_t = A_t - (V T^T) (V^T A_t)
       double* At = Aw.p + (int64_t)j0 * n + j0 + jb;
-      // W1 = V^T A_t (QB x nt);  W2 = T^T W1;  A_t -= V W2
       TK_TRY(tk_dgemm(ctx, true, false, QB, nt, m, 1.0, Vp, QB, At, n, 0.0, W1.p, nt));
-      TK_TRY(tk_dgemm(ctx, true, false, QB, nt, QB, 1.0, Tp, QB, W1.p, nt, 0.0, W2.p, nt));
-      TK_TRY(tk_dgemm(ctx, false, false, m, nt, QB, -1.0, Vp, QB, W2.p, nt, 1.0, At, n));
+      TK_TRY(tk_dgemm(ctx, false, false, m, nt, QB, -1.0, VTtp, QB, W1.p, nt, 1.0, At, n));
     }
   }
-  // Q = H_1 ... H_np : backward accumulation from the identity
+  // Q = H_1 ... H_np : backward accumulation from the identity, Qs <- Qs - (V T) (V^T Qs)
   TK_TRY(tk_eye(ctx, Q, n));
   for (int p = np - 1; p >= 0; p--) {
     const int j0 = p * QB, m = n - j0;
     double* Vp = Vb.p + (size_t)p * n * QB;
-    double* Tp = Tb.p + (size_t)p * QB * QB;
+    double* VTp = VTb.p + (size_t)p * n * QB;
     double* Qs = Q + (int64_t)j0 * n + j0;
-    // W1 = V^T Qs (QB x m);  W2 = T W1;  Qs -= V W2
     TK_TRY(tk_dgemm(ctx, true, false, QB, m, m, 1.0, Vp, QB, Qs, n, 0.0, W1.p, m));
-    TK_TRY(tk_dgemm(ctx, false, false, QB, m, QB, 1.0, Tp, QB, W1.p, m, 0.0, W2.p, m));
-    TK_TRY(tk_dgemm(ctx, false, false, m, m, QB, -1.0, Vp, QB, W2.p, m, 1.0, Qs, n));
+    TK_TRY(tk_dgemm(ctx, false, false, m, m, QB, -1.0, VTp, QB, W1.p, m, 1.0, Qs, n));
   }
   return TK_OK;
 }
