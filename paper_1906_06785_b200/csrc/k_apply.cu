@@ -17,7 +17,9 @@
 
 namespace {
 
-template <int RPL>
+// V2: lane owns column pairs (16-byte loads/stores; needs r even and RPL even), else single
+// columns lane + 32 u.
+template <int RPL, bool V2>
 __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t n_x, int T, int r,
                                                     const int32_t* __restrict__ rowptr,
                                                     const int32_t* __restrict__ col,
@@ -32,6 +34,19 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
   constexpr int CW = 32 * RPL;  // columns per chunk
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int UNR = 4;        // entries whose U1 rows are loaded together (memory-level parallelism)
+  constexpr int STEP = V2 ? 2 : 1;
+  auto colof = [lane](int u) { return V2 ? (64 * (u >> 1) + 2 * lane + (u & 1)) : (lane + 32 * u); };
+  auto put = [&](double* dst, const double* acc, int lim) {  // dst: column c0; lim = r - c0
+#pragma unroll
+    for (int u = 0; u < RPL; u += STEP) {
+      const int cc = colof(u);
+      if (V2) {
+        if (cc < lim) __stcs((double2*)(dst + cc), make_double2(acc[u], acc[u + 1]));
+      } else {
+        if (cc < lim) __stcs(dst + cc, acc[u]);
+      }
+    }
+  };
   for (int64_t i = warp; i < n_x; i += nwarps) {
     double* yrow = Y1 + i * R;
     // Terms in groups of 32: lane k fetches the CSR extent of term kg0 + k for this row, so the
@@ -91,9 +106,16 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
               kk[s] = (q0 + s < cnt) ? __shfl_sync(FULL, myk, q) : -2;
               const double* urow = U1 + (int64_t)c * r + c0;
 #pragma unroll
-              for (int u = 0; u < RPL; u++) {
-                const int cc = lane + 32 * u;
-                uv[s][u] = (kk[s] >= 0 && c0 + cc < r) ? __ldg(urow + cc) : 0.0;
+              for (int u = 0; u < RPL; u += STEP) {
+                const int cc = colof(u);
+                const bool ok = kk[s] >= 0 && c0 + cc < r;
+                if (V2) {
+                  const double2 t = ok ? __ldg((const double2*)(urow + cc)) : make_double2(0.0, 0.0);
+                  uv[s][u] = t.x;
+                  uv[s][u + 1] = t.y;
+                } else {
+                  uv[s][u] = ok ? __ldg(urow + cc) : 0.0;
+                }
               }
             }
 #pragma unroll
@@ -101,12 +123,9 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
               if (kk[s] == -2) break;
               if (kk[s] != cur) {
                 if (cur >= 0) {
+                  put(yrow + (int64_t)(kg0 + cur) * r + c0, acc, r - c0);
 #pragma unroll
-                  for (int u = 0; u < RPL; u++) {
-                    const int cc = lane + 32 * u;
-                    if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + cur) * r + c0 + cc, acc[u]);
-                    acc[u] = 0.0;
-                  }
+                  for (int u = 0; u < RPL; u++) acc[u] = 0.0;
                 }
                 cur = kk[s];
               }
@@ -115,46 +134,39 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
             }
           }
         }
-        if (cur >= 0) {
-#pragma unroll
-          for (int u = 0; u < RPL; u++) {
-            const int cc = lane + 32 * u;
-            if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + cur) * r + c0 + cc, acc[u]);
-          }
-        }
+        if (cur >= 0) put(yrow + (int64_t)(kg0 + cur) * r + c0, acc, r - c0);
         // terms with no entry in this row
         for (int k = 0; k < kn; k++) {
           if (__shfl_sync(FULL, mycnt, k) != 0) continue;
+          double z[RPL];
 #pragma unroll
-          for (int u = 0; u < RPL; u++) {
-            const int cc = lane + 32 * u;
-            if (c0 + cc < r) __stcs(yrow + (int64_t)(kg0 + k) * r + c0 + cc, 0.0);
-          }
+          for (int u = 0; u < RPL; u++) z[u] = 0.0;
+          put(yrow + (int64_t)(kg0 + k) * r + c0, z, r - c0);
         }
       }
     }
   }
 }
 
+// The diagonal blocks only (the rest of Y2 is zeroed by a memset first):
+//   Y2[k r1 + a, i, k r2 + b] = sum_j G_k[i, j] U2[a, j, b]
+// blockIdx.y = row k r1 + a; threads over (i, b), b fastest (coalesced U2 reads and Y2 writes,
+// G_k[i, :] broadcast within a warp when r2 >= 32).
 __global__ void stoch_apply_k(int T, int r1, int n_xi, int r2, const double* __restrict__ G,
                               const double* __restrict__ U2, double* __restrict__ Y2) {
+  const int row = blockIdx.y;
+  const int k = row / r1, a = row % r1;
   const int64_t R2 = (int64_t)T * r2;
-  const int64_t rowlen = (int64_t)n_xi * R2;
-  for (int64_t row = blockIdx.x; row < (int64_t)T * r1; row += gridDim.x) {
-    const int k = (int)(row / r1), a = (int)(row % r1);
-    const double* g = G + (int64_t)k * n_xi * n_xi;
-    const double* u = U2 + (int64_t)a * n_xi * r2;
-    double* y = Y2 + row * rowlen;
-    for (int64_t e = threadIdx.x; e < rowlen; e += blockDim.x) {
-      const int i = (int)(e / R2);
-      const int64_t bb = e % R2;
-      double v = 0.0;
-      if (bb >= (int64_t)k * r2 && bb < (int64_t)(k + 1) * r2) {
-        const int b = (int)(bb - (int64_t)k * r2);
-        for (int j = 0; j < n_xi; j++) v = fma(g[(int64_t)i * n_xi + j], u[(int64_t)j * r2 + b], v);
-      }
-      y[e] = v;
-    }
+  const double* g = G + (int64_t)k * n_xi * n_xi;
+  const double* u = U2 + (int64_t)a * n_xi * r2;
+  double* y = Y2 + (int64_t)row * n_xi * R2 + (int64_t)k * r2;
+  const int n = n_xi * r2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int i = e / r2, b = e - i * r2;
+    const double* gi = g + (int64_t)i * n_xi;
+    double v = 0.0;
+    for (int j = 0; j < n_xi; j++) v = fma(__ldg(gi + j), __ldg(u + (int64_t)j * r2 + b), v);
+    y[(int64_t)i * R2 + b] = v;
   }
 }
 
@@ -186,19 +198,28 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
   const int rpl = (r + 31) / 32;
-#define TK_SPMM(R)                                                                          \
-  spmm_multi_k<R><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                           \
+#define TK_SPMM(R, V)                                                                       \
+  spmm_multi_k<R, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                        \
       n_x, op->T, r, op->rowptr, op->col, op->val, op->nnz_off, U1, Y1)
-  if (rpl <= 1)
-    TK_SPMM(1);
+  // 16-byte path: r even (row starts stay 16-byte aligned) and 16-byte aligned bases
+  const bool v2 = (r % 2 == 0) && (((uintptr_t)U1 & 15) == 0) && (((uintptr_t)Y1 & 15) == 0);
+  if (v2) {
+    if (rpl <= 2)
+      TK_SPMM(2, true);
+    else if (rpl <= 4)
+      TK_SPMM(4, true);
+    else
+      TK_SPMM(8, true);
+  } else if (rpl <= 1)
+    TK_SPMM(1, false);
   else if (rpl == 2)
-    TK_SPMM(2);
+    TK_SPMM(2, false);
   else if (rpl == 3)
-    TK_SPMM(3);
+    TK_SPMM(3, false);
   else if (rpl == 4)
-    TK_SPMM(4);
+    TK_SPMM(4, false);
   else
-    TK_SPMM(8);
+    TK_SPMM(8, false);
 #undef TK_SPMM
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
@@ -206,9 +227,17 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
 
 int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
                           double* Y2) {
-  int64_t rows = (int64_t)op->T * r1;
-  int blocks = (int)std::min<int64_t>(rows, 16LL * ctx->num_sms);
-  stoch_apply_k<<<blocks, 256, 0, ctx->stream>>>(op->T, r1, (int)op->n_xi, r2, op->G, U2, Y2);
+  const int64_t rows = (int64_t)op->T * r1;
+  const int64_t total = rows * op->n_xi * op->T * r2;
+  TK_CUDA_TRY(ctx, cudaMemsetAsync(Y2, 0, sizeof(double) * total, ctx->stream));
+  const int n = (int)(op->n_xi * r2);
+  const int bx = std::max(1, std::min((n + 255) / 256, 8));
+  if (rows > 65535) {
+    ctx->err = "tk_apply_op: T * r1 exceeds the stochastic kernel's grid limit";
+    return TK_EARG;
+  }
+  stoch_apply_k<<<dim3(bx, (unsigned)rows), 256, 0, ctx->stream>>>(op->T, r1, (int)op->n_xi, r2,
+                                                                    op->G, U2, Y2);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }

@@ -160,32 +160,39 @@ __global__ void max_diag_tol_k(int n, const double* __restrict__ H, double rel,
   }
 }
 
-// X = R^{-1} for the k x k upper triangular R (row-major, leading dimension ldr); one warp per
-// column j of X (back substitution, the column kept in shared memory).  X is upper triangular,
-// written in full (zeros below the diagonal).
-constexpr int TI_WARPS = 4;
-__global__ void __launch_bounds__(32 * TI_WARPS) tri_inv_k(int k, const double* __restrict__ R,
-                                                           int64_t ldr, double* __restrict__ X,
-                                                           int64_t ldx) {
-  extern __shared__ double xcol[];  // TI_WARPS columns of length k
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = blockIdx.x * TI_WARPS + w;
-  if (j >= k) return;
-  double* x = xcol + (int64_t)w * k;
-  for (int i = lane; i < k; i += 32) x[i] = 0.0;
-  __syncwarp();
-  if (lane == 0) x[j] = 1.0 / R[(int64_t)j * ldr + j];
-  __syncwarp();
-  for (int i = j - 1; i >= 0; i--) {
-    const double* ri = R + (int64_t)i * ldr;
-    double s = 0.0;
-    for (int l = i + 1 + lane; l <= j; l += 32) s = fma(ri[l], x[l], s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) x[i] = -s / ri[i];
-    __syncwarp();
+// X[i0:i0+h, c0:c0+w] <- Rd^{-1} X[i0:i0+h, c0:c0+w] for the h x h (h <= 64) upper triangular
+// diagonal block Rd = R[i0:i0+h, i0:i0+h]: back substitution, one thread per column (the block
+// of R and the columns in shared memory).
+constexpr int TS_H = 64, TS_W = 128;
+__global__ void __launch_bounds__(TS_W) trsm_diag_k(int h, int i0, int ncols, int c0,
+                                                    const double* __restrict__ R, int64_t ldr,
+                                                    double* __restrict__ X, int64_t ldx) {
+  extern __shared__ double tsm[];
+  double(*Rs)[TS_H] = reinterpret_cast<double(*)[TS_H]>(tsm);            // broadcast reads
+  double(*xs)[TS_W] = reinterpret_cast<double(*)[TS_W]>(tsm + TS_H * TS_H);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < h * h; e += blockDim.x) {
+    const int i = e / h, l = e % h;
+    Rs[i][l] = R[(int64_t)(i0 + i) * ldr + i0 + l];
   }
-  for (int i = lane; i < k; i += 32) X[(int64_t)i * ldx + j] = x[i];
+  const int c = c0 + blockIdx.x * TS_W + tid;
+  const bool live = c < c0 + ncols;
+  for (int i = 0; i < h; i++) xs[i][tid] = live ? X[(int64_t)(i0 + i) * ldx + c] : 0.0;
+  __syncthreads();
+  for (int i = h - 1; i >= 0; i--) {
+    double s = xs[i][tid];
+    for (int l = i + 1; l < h; l++) s = fma(-Rs[i][l], xs[l][tid], s);
+    xs[i][tid] = s / Rs[i][i];
+  }
+  if (live)
+    for (int i = 0; i < h; i++) X[(int64_t)(i0 + i) * ldx + c] = xs[i][tid];
+}
+
+__global__ void eye_block_k(int h, int i0, double* __restrict__ X, int64_t ldx) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < h * h; e += gridDim.x * blockDim.x) {
+    const int i = e / h, l = e % h;
+    X[(int64_t)(i0 + i) * ldx + i0 + l] = (i == l) ? 1.0 : 0.0;
+  }
 }
 
 // gather columns: out[t, c] = Ro[t, piv[c]]   (rows x k)
@@ -261,21 +268,35 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   return TK_OK;
 }
 
+// X = R^{-1} (k x k upper triangular), blocked back substitution from the bottom block row:
+//   X[I, J>I] = -R[I, I]^{-1} R[I, >I] X[>I, J],   X[I, I] = R[I, I]^{-1}
+// (one DMMA GEMM and one diagonal-block solve per 64-row block).
 int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx) {
   if (k <= 0) return TK_OK;
-  const size_t smem = (size_t)TI_WARPS * k * sizeof(double);
-  if (smem > 200 * 1024) {
-    ctx->err = "tk_tri_inv: k too large";
-    return TK_EARG;
+  TagScope tag(ctx, "tri_inv");
+  for (int64_t i = 0; i < k; i++)
+    TK_CUDA_TRY(ctx, cudaMemsetAsync(X + i * ldx, 0, sizeof(double) * k, ctx->stream));
+  const int nbk = (k + TS_H - 1) / TS_H;
+  for (int b = nbk - 1; b >= 0; b--) {
+    const int i0 = b * TS_H, i1 = std::min(k, i0 + TS_H), h = i1 - i0;
+    eye_block_k<<<(h * h + 255) / 256, 256, 0, ctx->stream>>>(h, i0, X, ldx);
+    TK_LAUNCH_CHECK(ctx);
+    if (i1 < k) {
+      // X[i0:i1, i1:k] = -R[i0:i1, i1:k] X[i1:k, i1:k]
+      TK_TRY(tk_dgemm(ctx, false, false, h, k - i1, k - i1, -1.0, R + (int64_t)i0 * ldr + i1, ldr,
+                      X + (int64_t)i1 * ldx + i1, ldx, 0.0, X + (int64_t)i0 * ldx + i1, ldx));
+    }
+    const int ncols = k - i0;
+    const size_t smem = sizeof(double) * (TS_H * TS_H + TS_H * TS_W);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(trsm_diag_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    trsm_diag_k<<<(ncols + TS_W - 1) / TS_W, TS_W, smem, ctx->stream>>>(h, i0, ncols, i0, R, ldr,
+                                                                         X, ldx);
+    TK_LAUNCH_CHECK(ctx);
   }
-  static int attr = 0;
-  if (smem > 48 * 1024 && (size_t)attr < smem) {
-    cudaFuncSetAttribute(tri_inv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = (int)smem;
-  }
-  tri_inv_k<<<(k + TI_WARPS - 1) / TI_WARPS, 32 * TI_WARPS, smem, ctx->stream>>>(k, R, ldr, X,
-                                                                                  ldx);
-  TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
 

@@ -8,14 +8,14 @@
 // Layout: the matrix is embedded in an n_pad x n_pad buffer (n_pad = 64 * ceil(n/64), zero
 // padding — padded indices never rotate since their couplings are 0), split into
 // nb = n_pad/32 blocks of 32 rows/cols.  One sweep = nb-1 rounds of a round-robin
-// tournament over blocks; a round handles nb/2 disjoint block pairs (I, J) in three phases
+// tournament over blocks; a round handles nb/2 disjoint block pairs (I, J) in two phases
 // separated by grid-wide barriers:
 //   inner  one CTA per pair: S = G[I u J, I u J] (64 x 64) in shared memory, one scalar
 //          cyclic Jacobi sweep (parallel ordering, Rutishauser updates of each 2x2 pivot)
 //          accumulating Q (64 x 64); Q and the rotated S go to global memory.
-//   cols   G[:, I u J] <- G[:, I u J] Q  and  V[:, I u J] <- V[:, I u J] Q   (64 x 64 tiles)
-//   rows   G[I u J, :] <- Q^T G[I u J, :]  (the pair's own block takes the inner S, so its
-//          annihilated entries stay exactly 0)
+//   update G[IJ_t, IJ_s] <- Q_t^T G[IJ_t, IJ_s] Q_s for t < s (written to both triangles: G
+//          stays exactly symmetric), G[IJ_t, IJ_t] <- S_t (the inner result, so annihilated
+//          entries stay exactly 0), and V[:, IJ_t] <- V[:, IJ_t] Q_t   (64 x 64 DMMA tiles)
 // Rotation counts per sweep end the loop (all CTAs read the counter after the barrier).
 //
 // Cluster skip (bond SVDs only): when lskip >= 0, rotations between two indices whose
@@ -137,12 +137,23 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
   long long pa_sum = 0, pb_sum = 0, t_a = 0;
   int my_rot = 0;          // warp 0 lanes: rotations applied (this call)
   double my_off = 0.0;     // warp 0 lanes: largest relative coupling rotated away
+  // The first outer round of a sweep (r == 0, every block appears once) runs the full
+  // 63-round inner sweep; later rounds only rotate the 32 x 32 cross pairs (i in I, j in J):
+  // 32 inner rounds of 32 disjoint pairs.  Every index pair is still visited once per sweep.
+  const bool cross = (r != 0) && (a.npairs > 1);
+  // Cross rounds keep Q in registers: thread (warp w, lane l) holds rows w + 16 m of column
+  // l (qr_p) and of column 32 + (l + ir) % 32 (qr_q), the partner of l in inner round ir; after
+  // each round the partner columns move one lane down (a shuffle), so Q never touches shared
+  // memory until the end (it was half of the update phase's shared-memory traffic).
+  const int lane = tid & 31, wq = tid >> 5;
+  double qr_p[4], qr_q[4];
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    qr_p[m] = (wq + 16 * m == lane) ? 1.0 : 0.0;
+    qr_q[m] = (wq + 16 * m == JB + lane) ? 1.0 : 0.0;
+  }
   for (int sweep = 0; sweep < a.max_inner; sweep++) {
     int sweep_rot = 0;
-    // The first outer round of a sweep (r == 0, every block appears once) runs the full
-    // 63-round inner sweep; later rounds only rotate the 32 x 32 cross pairs (i in I, j in J):
-    // 32 inner rounds of 32 disjoint pairs.  Every index pair is still visited once per sweep.
-    const bool cross = (r != 0) && (a.npairs > 1);
     const int nrounds = cross ? JB : JS - 1;
     for (int ir = 0; ir < nrounds; ir++) {
       if (tid == 0) t_a = clock64();
@@ -195,7 +206,6 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
       // Thread map: P2 = lane (parameters loaded once), P1 = warp and warp + 16; Q rows
       // warp + 16 m (m < 4) of pair lane.
       {
-        const int lane = tid & 31, wq = tid >> 5;
         const double c2 = sh.rc[lane], s2 = sh.rs[lane];
         const int p2 = sh.rp[lane], q2 = sh.rq[lane], act2 = sh.ract[lane];
 #pragma unroll
@@ -222,7 +232,17 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
           S[p1 * JLD + q2] = c1 * y01 - s1 * y11;
           S[q1 * JLD + q2] = s1 * y01 + c1 * y11;
         }
-        if (act2) {
+        if (cross) {
+#pragma unroll
+          for (int m = 0; m < 4; m++) {
+            if (act2) {
+              const double qp = qr_p[m], qq = qr_q[m];
+              qr_p[m] = c2 * qp - s2 * qq;
+              qr_q[m] = s2 * qp + c2 * qq;
+            }
+            qr_q[m] = __shfl_sync(0xffffffffu, qr_q[m], (lane + 1) & 31);
+          }
+        } else if (act2) {
 #pragma unroll
           for (int m = 0; m < 4; m++) {
             const int i = wq + 16 * m;
@@ -247,6 +267,16 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
     const bool done = (sh.nrot == 0);
     __syncthreads();
     if (done) break;
+  }
+  if (cross) {
+    // after JB rounds lane l holds column JB + l again
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      const int i = wq + 16 * m;
+      Q[i * JLD + lane] = qr_p[m];
+      Q[i * JLD + JB + lane] = qr_q[m];
+    }
+    __syncthreads();
   }
   double* Qo = a.Qb + (int64_t)t * JS * JS;
   double* So = a.Sb + (int64_t)t * JS * JS;
@@ -341,26 +371,50 @@ __device__ void col_tile(const JacArgs& a, double* M, int row0, int t, int r, do
   __syncthreads();
 }
 
-// 64-column tile of G[I u J, :] <- Q^T G[I u J, :]; the pair's own columns take S  (DMMA)
-__device__ void row_tile(const JacArgs& a, int col0, int t, int r, double* sm) {
-  double* Qs = sm;
-  double* Ts = sm + JS * TLD;
-  int I, J;
-  pair_blocks(t, r, a.nb, I, J);
-  const double* Q = a.Qb + (int64_t)t * JS * JS;
-  const double* S = a.Sb + (int64_t)t * JS * JS;
+// Two-sided block of G for pairs t < s:  G[IJ_t, IJ_s] <- Q_t^T G[IJ_t, IJ_s] Q_s, written to
+// both G[IJ_t, IJ_s] and (transposed) G[IJ_s, IJ_t]; for t == s the block is the inner solve's S.
+// One work item per unordered pair of pairs replaces the former column phase on G and the row
+// phase (G stays exactly symmetric, one grid barrier less per round).
+__device__ void sym_tile(const JacArgs& a, int t, int s, int r, double* sm) {
   double* G = a.G;
   const int n_pad = a.n_pad;
+  int It, Jt, Is, Js;
+  pair_blocks(t, r, a.nb, It, Jt);
+  pair_blocks(s, r, a.nb, Is, Js);
+  if (t == s) {
+    const double* S = a.Sb + (int64_t)t * JS * JS;
+    for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+      const int i = e / JS, j = e % JS;
+      G[(int64_t)gidx(i, It, Jt) * n_pad + gidx(j, It, Jt)] = S[e];
+    }
+    return;
+  }
+  double* Qs = sm;                 // Q_s
+  double* Xs = sm + JS * TLD;      // G block, then G block Q_s
+  double* Qt = sm + 2 * JS * TLD;  // Q_t
+  const double* Qsg = a.Qb + (int64_t)s * JS * JS;
+  const double* Qtg = a.Qb + (int64_t)t * JS * JS;
   for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    Qs[i * TLD + j] = Q[e];
-    Ts[i * TLD + j] = G[(int64_t)gidx(i, I, J) * n_pad + col0 + j];
+    const int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = Qsg[e];
+    Qt[i * TLD + j] = Qtg[e];
+    Xs[i * TLD + j] = G[(int64_t)gidx(i, It, Jt) * n_pad + gidx(j, Is, Js)];
   }
   __syncthreads();
   double acc[2][2][2];
-  tile_mma(Qs, true, Ts, acc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+  tile_mma(Xs, false, Qs, acc);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        Xs[(wm + 8 * i + (lane >> 2)) * TLD + wn + 8 * j + 2 * (lane & 3) + h] = acc[i][j][h];
+  __syncthreads();
+  tile_mma(Qt, true, Xs, acc);
 #pragma unroll
   for (int i = 0; i < 2; i++)
 #pragma unroll
@@ -368,10 +422,9 @@ __device__ void row_tile(const JacArgs& a, int col0, int t, int r, double* sm) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
-        const int gc = col0 + n, bc = gc / JB;
-        double v = acc[i][j][h];
-        if (bc == I || bc == J) v = S[m * JS + ((bc == I) ? gc - I * JB : JB + gc - J * JB)];
-        G[(int64_t)gidx(m, I, J) * n_pad + gc] = v;
+        const int gm = gidx(m, It, Jt), gn = gidx(n, Is, Js);
+        G[(int64_t)gm * n_pad + gn] = acc[i][j][h];
+        G[(int64_t)gn * n_pad + gm] = acc[i][j][h];
       }
   __syncthreads();
 }
@@ -455,22 +508,27 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
       mark(0);
       if (coop) cg::this_grid().sync(); else __syncthreads();
       mark(1);
-      const int nct = rtiles * a.npairs * 2;
-      for (int w = blockIdx.x; w < nct; w += gridDim.x) {
-        const int which = w / (rtiles * a.npairs), rem = w % (rtiles * a.npairs);
-        const int t = rem / rtiles, rt = rem % rtiles;
-        col_tile(as, which ? a.V : a.G, rt * JS, t, r, sm);
+      // G: two-sided blocks for t <= s (heavier items first); V: column tiles V[:, IJ_t] Q_t
+      const int nsym = a.npairs * (a.npairs + 1) / 2;
+      const int nitems = nsym + rtiles * a.npairs;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        if (w < nsym) {
+          // w -> (t, s), t <= s, row-major over the upper triangle
+          int t = 0, rem = w;
+          while (rem >= a.npairs - t) {
+            rem -= a.npairs - t;
+            t++;
+          }
+          sym_tile(as, t, t + rem, r, sm);
+        } else {
+          const int v = w - nsym;
+          col_tile(as, a.V, (v % rtiles) * JS, v / rtiles, r, sm);
+        }
       }
       mark(2);
       if (coop) cg::this_grid().sync(); else __syncthreads();
       mark(3);
-      const int nrt = rtiles * a.npairs;
-      for (int w = blockIdx.x; w < nrt; w += gridDim.x) {
-        const int t = w / rtiles, ct = w % rtiles;
-        row_tile(as, ct * JS, t, r, sm);
-      }
       mark(4);
-      if (coop) cg::this_grid().sync(); else __syncthreads();
       mark(5);
     }
     const int rot = *((volatile int*)(a.stats + sweep));
@@ -670,7 +728,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
     embed_k<<<g, 256, 0, ctx->stream>>>(n, n_pad, A, Gp.p, Vp.p);
     TK_LAUNCH_CHECK(ctx);
   }
-  const size_t smem = 2 * (size_t)JS * TLD * sizeof(double);
+  const size_t smem = 3 * (size_t)JS * TLD * sizeof(double);
   static int max_grid = -1;
   if (max_grid < 0) {
     cudaFuncSetAttribute(jacobi_persistent_k, cudaFuncAttributeMaxDynamicSharedMemorySize,

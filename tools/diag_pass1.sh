@@ -8,5 +8,6 @@ for v in ${VARIANTS:-base}; do
     jac) env TTK_DEBUG=1 TTK_PASS1=jacobi $B ;;
     cskip) env TTK_DEBUG=1 TTK_CLUSTER_SKIP=1 $B ;;
     rskip) env TTK_DEBUG=1 TTK_CLUSTER_SKIP=1 TTK_RANK_SKIP=1 $B ;;
+    b1id) env TTK_DEBUG=1 TTK_BOND1_PASS1_ID=1 $B ;;
   esac > gpurun_out/d_$v.json 2> gpurun_out/d_$v.err
 done
