@@ -297,7 +297,8 @@ def run_ours(args, cfg, op, x):
     fp64_peak = peaks["bf16_tflops"] * (45.0 / 2250.0)  # bf16 measured x nominal fp64/bf16 ratio
     # group the phase records by KERNEL FUNCTION: every phase tag that is not one of the
     # named kernels below is a launch of the DMMA GEMM (dgemm_kernel + its split-K reduce)
-    named = {"jacobi": "jacobi_persistent_k", "qr_panel": "qr_panel_k",
+    named = {"jacobi": "jacobi_persistent_k", "qr_panel": "qr_panel_warp_k",
+             "qr_reflector": "apply_reflector_k", "pchol_panel": "pchol_panel_k",
              "spmm_multi": "spmm_multi_k", "stoch_apply": "stoch_apply_k",
              "time_apply": "time_apply_k"}
     kernels = {}

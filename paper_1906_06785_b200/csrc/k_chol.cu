@@ -122,9 +122,17 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
       } else if (sd[c] == -INFINITY) {
         out = 0.0;
       } else {
-        double v = hrow[c];
-        for (int t = 0; t < s; t++) v = fma(-sR[t * n + p], sR[t * n + c], v);
-        out = v * rinv;
+        // four independent partial sums (the shared-memory latency bounds a single chain)
+        double v0 = hrow[c], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int t = 0;
+        for (; t + 3 < s; t += 4) {
+          v0 = fma(-sR[t * n + p], sR[t * n + c], v0);
+          v1 = fma(-sR[(t + 1) * n + p], sR[(t + 1) * n + c], v1);
+          v2 = fma(-sR[(t + 2) * n + p], sR[(t + 2) * n + c], v2);
+          v3 = fma(-sR[(t + 3) * n + p], sR[(t + 3) * n + c], v3);
+        }
+        for (; t < s; t++) v0 = fma(-sR[t * n + p], sR[t * n + c], v0);
+        out = ((v0 + v1) + (v2 + v3)) * rinv;
         sd[c] = fma(-out, out, sd[c]);
       }
       orow[c] = out;
@@ -252,11 +260,12 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     cudaFuncSetAttribute(pchol_panel_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
   for (int j0 = 0; j0 < n; j0 += nb) {
+    const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
     pchol_panel_k<<<1, PT, smem, ctx->stream>>>(n, j0, nb, pivot ? 1 : 0, Hw.p, Ro, piv,
                                                   state, tol.p);
     TK_LAUNCH_CHECK(ctx);
+    tk_prof_end(ctx, pid);
     const int jb = std::min(nb, n - j0);
     if (j0 + jb < n) {
       // Hw -= Ro[j0:j0+jb, :]^T Ro[j0:j0+jb, :]   (rows of a stopped panel are zero: no-op)
@@ -264,7 +273,6 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
                       Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true));
     }
   }
-  tk_prof_end(ctx, pid);
   return TK_OK;
 }
 

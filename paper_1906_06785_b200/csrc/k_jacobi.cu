@@ -78,6 +78,10 @@ __device__ __forceinline__ void pair_blocks(int t, int r, int nb, int& I, int& J
 __device__ __forceinline__ int gidx(int l, int I, int J) {
   return l < JB ? I * JB + l : J * JB + (l - JB);
 }
+// upper-triangle position of (i, j) in the inner solve's shared S
+__device__ __forceinline__ int uidx(int i, int j) {
+  return i <= j ? i * JLD + j : j * JLD + i;
+}
 
 struct InnerShared {
   double rc[JB], rs[JB], rt[JB], rapp[JB], raqq[JB], rapq[JB];
@@ -128,7 +132,7 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
       double* So = a.Sb + (int64_t)t * JS * JS;
       for (int e = tid; e < JS * JS; e += blockDim.x) {
         Qo[e] = Q[(e / JS) * JLD + e % JS];
-        So[e] = S[(e / JS) * JLD + e % JS];
+        So[e] = S[uidx(e / JS, e % JS)];
       }
       __syncthreads();
       return;
@@ -183,7 +187,6 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
           c = u * rn;
           sn = es * rn;
           act = 1;
-          my_off = fmax(my_off, fabs(apq) * rsqrt(fmax(fabs(app * aqq), 1e-300)));
         }
         sh.rc[k] = c;
         sh.rs[k] = sn;
@@ -202,15 +205,22 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
         pa_sum += now - t_a;
         t_a = now;
       }
-      // S <- J^T S J on 2x2 blocks (pair P1 rows, pair P2 cols) and Q <- Q J.
+      // S <- J^T S J on 2x2 blocks (pair P1 rows, pair P2 cols) and Q <- Q J.  Only the upper
+      // triangle of S is kept (uidx): block (P1, P2) for P1 <= P2 covers each element once, and
+      // half the shared-memory traffic of the full two-sided update goes away.
       // Thread map: P2 = lane (parameters loaded once), P1 = warp and warp + 16; Q rows
       // warp + 16 m (m < 4) of pair lane.
       {
         const double c2 = sh.rc[lane], s2 = sh.rs[lane];
         const int p2 = sh.rp[lane], q2 = sh.rq[lane], act2 = sh.ract[lane];
+        // largest relative coupling rotated away (off the parameter phase's critical path)
+        if (wq == 0 && act2)
+          my_off = fmax(my_off, fabs(sh.rapq[lane]) *
+                                    rsqrt(fmax(fabs(sh.rapp[lane] * sh.raqq[lane]), 1e-300)));
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int P1 = wq + 16 * h;
+          if (P1 > lane) continue;
           const int act1 = sh.ract[P1];
           if (!act1 && !act2) continue;
           const int p1 = sh.rp[P1], q1 = sh.rq[P1];
@@ -218,19 +228,18 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
             const double t1 = sh.rt[P1], a1 = sh.rapq[P1];
             S[p1 * JLD + p1] = sh.rapp[P1] - t1 * a1;
             S[q1 * JLD + q1] = sh.raqq[P1] + t1 * a1;
-            S[p1 * JLD + q1] = 0.0;
-            S[q1 * JLD + p1] = 0.0;
+            S[p1 * JLD + q1] = 0.0;  // p1 < q1
             continue;
           }
           const double c1 = sh.rc[P1], s1 = sh.rs[P1];
-          const double x00 = S[p1 * JLD + p2], x01 = S[p1 * JLD + q2];
-          const double x10 = S[q1 * JLD + p2], x11 = S[q1 * JLD + q2];
+          const int i00 = uidx(p1, p2), i01 = uidx(p1, q2), i10 = uidx(q1, p2), i11 = uidx(q1, q2);
+          const double x00 = S[i00], x01 = S[i01], x10 = S[i10], x11 = S[i11];
           const double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
           const double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
-          S[p1 * JLD + p2] = c1 * y00 - s1 * y10;
-          S[q1 * JLD + p2] = s1 * y00 + c1 * y10;
-          S[p1 * JLD + q2] = c1 * y01 - s1 * y11;
-          S[q1 * JLD + q2] = s1 * y01 + c1 * y11;
+          S[i00] = c1 * y00 - s1 * y10;
+          S[i10] = s1 * y00 + c1 * y10;
+          S[i01] = c1 * y01 - s1 * y11;
+          S[i11] = s1 * y01 + c1 * y11;
         }
         if (cross) {
 #pragma unroll
@@ -282,7 +291,7 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
   double* So = a.Sb + (int64_t)t * JS * JS;
   for (int e = tid; e < JS * JS; e += blockDim.x) {
     Qo[e] = Q[(e / JS) * JLD + e % JS];
-    So[e] = S[(e / JS) * JLD + e % JS];
+    So[e] = S[uidx(e / JS, e % JS)];
   }
   if (tid < JB) {
     int v = my_rot;

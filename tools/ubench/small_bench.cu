@@ -1,0 +1,84 @@
+// Stand-alone timing of the latency-bound internal routines of libttk (Householder pass 1,
+// pivoted Cholesky, triangular inverse, Jacobi) on synthetic SPD matrices, through the library's
+// own (non-ABI, internal) entry points.  Diagnostic only.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../paper_1906_06785_b200/csrc/ttk_internal.h"
+
+static void spd(int n, std::vector<double>& H, double span) {
+  // H = B diag(d) B^T with B random, d graded over `span` decades
+  std::vector<double> B((size_t)n * n);
+  srand(1);
+  for (auto& v : B) v = (rand() / (double)RAND_MAX) - 0.5;
+  H.assign((size_t)n * n, 0.0);
+  std::vector<double> d(n);
+  for (int i = 0; i < n; i++) d[i] = pow(10.0, -span * i / n);
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j <= i; j++) {
+      double s = 0;
+      for (int k = 0; k < n; k++) s += B[(size_t)i * n + k] * d[k] * B[(size_t)j * n + k];
+      H[(size_t)i * n + j] = H[(size_t)j * n + i] = s;
+    }
+}
+
+int main(int argc, char** argv) {
+  int n = argc > 1 ? atoi(argv[1]) : 896;
+  const char* what = argc > 2 ? argv[2] : "qr";
+  tk_ctx* ctx;
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  tk_ctx_create(&ctx, st);
+  std::vector<double> H;
+  spd(n, H, 12.0);
+  double *dH, *dQ, *dR;
+  int *piv, *state;
+  cudaMalloc(&dH, sizeof(double) * n * n);
+  cudaMalloc(&dQ, sizeof(double) * n * n);
+  cudaMalloc(&dR, sizeof(double) * n * n);
+  cudaMalloc(&piv, sizeof(int) * (n + 2) * 2);
+  cudaMalloc(&state, sizeof(int) * (n + 2));
+  cudaMemcpy(dH, H.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; rep++) {
+    tk_ctx_profile(ctx, 1);
+    cudaEventRecord(a, st);
+    int rc = 0;
+    if (!strcmp(what, "qr")) rc = tk_householder_q(ctx, n, dH, dQ);
+    else if (!strcmp(what, "pchol")) rc = tk_pchol(ctx, n, dH, 1e-28, nullptr, dR, piv, state, true);
+    else if (!strcmp(what, "triinv")) {
+      tk_pchol(ctx, n, dH, 1e-28, nullptr, dR, piv, state, false);
+      cudaEventRecord(a, st);
+      rc = tk_tri_inv(ctx, n, dR, n, dQ, n);
+    }
+    cudaEventRecord(b, st);
+    cudaStreamSynchronize(st);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("%s n=%d rc=%d total %.3f ms\n", what, n, rc, ms);
+    if (rep == 2) {
+      static char buf[1 << 22];
+      tk_ctx_profile_dump(ctx, buf, sizeof(buf));
+      // aggregate by category
+      std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+      char* line = strtok(buf, "\n");
+      while (line) {
+        char cat[128];
+        double t;
+        if (sscanf(line, "%127s %lf", cat, &t) == 2) {
+          bool f = false;
+          for (auto& x : agg)
+            if (x.first == cat) { x.second.first += t; x.second.second++; f = true; }
+          if (!f) agg.push_back({cat, {t, 1}});
+        }
+        line = strtok(nullptr, "\n");
+      }
+      for (auto& x : agg) printf("   %-16s n=%5d %8.3f ms\n", x.first.c_str(), x.second.second, x.second.first);
+    }
+  }
+  return 0;
+}
