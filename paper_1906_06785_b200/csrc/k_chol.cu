@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
                                                     const double* __restrict__ Hw,
                                                     double* __restrict__ Ro, int* __restrict__ piv,
                                                     int* __restrict__ state,
-                                                    const double* __restrict__ tol_dev) {
+                                                    const double* __restrict__ tol_dev,
+                                                    double* __restrict__ rem_out) {
   // state[0]: rank so far / final (k); state[1]: 1 once stopped; state[2 + c]: retired flags
   extern __shared__ double psm[];
   double* sR = psm;                 // nb x n
@@ -108,6 +109,22 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
       if (tid == 0) {
         state[0] = j;
         state[1] = 1;
+      }
+      if (rem_out) {
+        // trace of the dropped Schur complement (its eigenvalues' sum: part of the tail)
+        double t = 0.0;
+        for (int c = tid; c < n; c += PT)
+          if (sd[c] != -INFINITY) t += fmax(sd[c], 0.0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        __syncthreads();
+        if (lane == 0) s_val[warp] = t;
+        __syncthreads();
+        if (tid == 0) {
+          double tt = 0.0;
+          for (int w = 0; w < PT / 32; w++) tt += s_val[w];
+          rem_out[0] = tt;
+        }
       }
       return;
     }
@@ -236,7 +253,7 @@ int grid_for(tk_ctx* ctx, int64_t total) {
 int tk_pchol_max_n() { return 4096; }
 
 int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* tol_abs_dev,
-             double* Ro, int* piv, int* state, bool pivot) {
+             double* Ro, int* piv, int* state, bool pivot, double* rem_out) {
   if (n <= 0) return TK_OK;
   if (n > tk_pchol_max_n()) {
     ctx->err = "tk_pchol: n too large";
@@ -250,6 +267,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
                                    ctx->stream));
   TK_CUDA_TRY(ctx, cudaMemsetAsync(Ro, 0, sizeof(double) * n * n, ctx->stream));
   TK_CUDA_TRY(ctx, cudaMemsetAsync(state, 0, (2 + (size_t)n) * sizeof(int), ctx->stream));
+  if (rem_out) TK_CUDA_TRY(ctx, cudaMemsetAsync(rem_out, 0, sizeof(double), ctx->stream));
   max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
   TK_LAUNCH_CHECK(ctx);
   // panel width: the panel rows of Ro (nb x n) and the diagonal stay in shared memory
@@ -263,7 +281,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   for (int j0 = 0; j0 < n; j0 += nb) {
     const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
     pchol_panel_k<<<1, PT, smem, ctx->stream>>>(n, j0, nb, pivot ? 1 : 0, Hw.p, Ro, piv,
-                                                  state, tol.p);
+                                                  state, tol.p, rem_out);
     TK_LAUNCH_CHECK(ctx);
     tk_prof_end(ctx, pid);
     const int jb = std::min(nb, n - j0);

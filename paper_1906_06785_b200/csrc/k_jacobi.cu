@@ -46,6 +46,7 @@ constexpr int JT = 512;       // threads per CTA
 
 struct JacArgs {
   int n_pad, nb, npairs;
+  int v_tiles;          // 64-row tiles of V (V is v_tiles*64 x n_pad, ld n_pad)
   double* G;
   double* V;
   double* Qb;
@@ -487,7 +488,6 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
   const double lsk_static = a.lskip ? a.lskip[0] : -1.0;
   double lsk = lsk_static;
   __shared__ double sh_lsk;
-  const int rtiles = a.n_pad / JS;
   unsigned long long tsum[6] = {0, 0, 0, 0, 0, 0}, tprev = 0;
   const bool rec = a.tstamp && blockIdx.x == 0 && threadIdx.x == 0;
   auto mark = [&](int k) {
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
       mark(1);
       // G: two-sided blocks for t <= s (heavier items first); V: column tiles V[:, IJ_t] Q_t
       const int nsym = a.npairs * (a.npairs + 1) / 2;
-      const int nitems = nsym + rtiles * a.npairs;
+      const int nitems = nsym + a.v_tiles * a.npairs;
       for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
         if (w < nsym) {
           // w -> (t, s), t <= s, row-major over the upper triangle
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
           sym_tile(as, t, t + rem, r, sm);
         } else {
           const int v = w - nsym;
-          col_tile(as, a.V, (v % rtiles) * JS, v / rtiles, r, sm);
+          col_tile(as, a.V, (v % a.v_tiles) * JS, v / a.v_tiles, r, sm);
         }
       }
       mark(2);
@@ -556,19 +556,22 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
     for (int k = 0; k < 6; k++) a.tstamp[k] = tsum[k];  // [6], [7]: inner phase cycles
 }
 
+// G <- A zero-padded to n_pad x n_pad; V <- V0 (mv x n, zero-padded to mv_pad x n_pad) or, when
+// V0 is null, the identity.
 __global__ void embed_k(int n, int n_pad, const double* __restrict__ A, double* __restrict__ G,
-                        double* __restrict__ V) {
-  int64_t nn = (int64_t)n_pad * n_pad;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn;
+                        double* __restrict__ V, const double* __restrict__ V0, int mv, int mv_pad) {
+  const int64_t nn = (int64_t)n_pad * n_pad, nv = (int64_t)mv_pad * n_pad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn || e < nv;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(e / n_pad), j = (int)(e % n_pad);
-    G[e] = (i < n && j < n) ? A[(int64_t)i * n + j] : 0.0;
-    V[e] = (i == j) ? 1.0 : 0.0;
+    const int i = (int)(e / n_pad), j = (int)(e % n_pad);
+    if (e < nn) G[e] = (i < n && j < n) ? A[(int64_t)i * n + j] : 0.0;
+    if (e < nv)
+      V[e] = V0 ? ((i < mv && j < n) ? V0[(int64_t)i * n + j] : 0.0) : ((i == j) ? 1.0 : 0.0);
   }
 }
 
 // Sort eigenvalues descending (stable by index) and permute eigenvector columns.
-__global__ void eig_sort_k(int n, int n_pad, const double* __restrict__ G,
+__global__ void eig_sort_k(int n, int n_pad, int mv, const double* __restrict__ G,
                            const double* __restrict__ Vp, double* __restrict__ lam,
                            double* __restrict__ Vout) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -579,7 +582,7 @@ __global__ void eig_sort_k(int n, int n_pad, const double* __restrict__ G,
       rank += (lj > li) || (lj == li && j < i);
     }
     lam[rank] = li;
-    for (int k = 0; k < n; k++) Vout[(int64_t)k * n + rank] = Vp[(int64_t)k * n_pad + i];
+    for (int k = 0; k < mv; k++) Vout[(int64_t)k * n + rank] = Vp[(int64_t)k * n_pad + i];
   }
 }
 
@@ -711,14 +714,17 @@ int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lsk
 
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev,
-                  double rs_tol, int64_t rs_rmax, const double* abs_floor_dev) {
+                  double rs_tol, int64_t rs_rmax, const double* abs_floor_dev, const double* V0,
+                  int mv) {
   if (n <= 0) return TK_OK;
   const int n_pad = ((n + JS - 1) / JS) * JS;
+  if (!V0) mv = n;
+  const int mv_pad = ((mv + JS - 1) / JS) * JS;
   const int nb = n_pad / JB;
   const int npairs = nb / 2;
   DevBuf Gp, Vp, Qb, Sb, scr;
   TK_TRY(Gp.get(ctx, (size_t)n_pad * n_pad));
-  TK_TRY(Vp.get(ctx, (size_t)n_pad * n_pad));
+  TK_TRY(Vp.get(ctx, (size_t)std::max(mv_pad, n_pad) * n_pad));
   TK_TRY(Qb.get(ctx, (size_t)npairs * JS * JS));
   TK_TRY(Sb.get(ctx, (size_t)npairs * JS * JS));
   TK_TRY(scr.get(ctx, 2 + 2 * (size_t)max_sweeps));
@@ -732,9 +738,9 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   max_abs_diag_k<<<1, 256, 0, ctx->stream>>>(n, A, d_maxdiag);
   TK_LAUNCH_CHECK(ctx);
   {
-    int64_t nn = (int64_t)n_pad * n_pad;
+    int64_t nn = (int64_t)std::max(mv_pad, n_pad) * n_pad;
     int g = (int)std::min<int64_t>((nn + 255) / 256, 8LL * ctx->num_sms);
-    embed_k<<<g, 256, 0, ctx->stream>>>(n, n_pad, A, Gp.p, Vp.p);
+    embed_k<<<g, 256, 0, ctx->stream>>>(n, n_pad, A, Gp.p, Vp.p, V0, mv, mv_pad);
     TK_LAUNCH_CHECK(ctx);
   }
   const size_t smem = 3 * (size_t)JS * TLD * sizeof(double);
@@ -748,6 +754,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   }
   JacArgs a;
   a.n_pad = n_pad;
+  a.v_tiles = mv_pad / JS;
   a.nb = nb;
   a.npairs = npairs;
   a.G = Gp.p;
@@ -780,7 +787,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   a.stats = stats;
   a.sweeps_out = d_sweeps;
   const int rtiles = n_pad / JS;
-  int grid = std::min(max_grid, std::max(npairs, rtiles * npairs * 2));
+  int grid = std::min(max_grid, std::max(npairs, (rtiles + mv_pad / JS) * npairs));
   grid = std::min(grid, ctx->num_sms);
   int coop = grid > 1 ? 1 : 0;
   if (coop) {
@@ -793,7 +800,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
     TK_LAUNCH_CHECK(ctx);
   }
   int sg = (int)std::min<int64_t>((n + 127) / 128, 4LL * ctx->num_sms);
-  eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, Gp.p, Vp.p, lam, V);
+  eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, mv, Gp.p, Vp.p, lam, V);
   TK_LAUNCH_CHECK(ctx);
   if (lskip_dev) {
     skip_check_k<<<1, 512, 0, ctx->stream>>>(n, n_pad, Gp.p, lskip_dev);

@@ -333,3 +333,29 @@ int tk_set_scalar(tk_ctx* ctx, double* dst, double v) {
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
+
+namespace {
+__global__ void col_norms_k(int64_t rows, int64_t cols, const double* __restrict__ A, int64_t lda,
+                            double* __restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double s0 = 0.0, s1 = 0.0;
+    int64_t r = 0;
+    for (; r + 1 < rows; r += 2) {
+      const double a = A[r * lda + c], b = A[(r + 1) * lda + c];
+      s0 = fma(a, a, s0);
+      s1 = fma(b, b, s1);
+    }
+    if (r < rows) s0 = fma(A[r * lda + c], A[r * lda + c], s0);
+    out[c] = sqrt(s0 + s1);
+  }
+}
+}  // namespace
+
+int tk_col_norms(tk_ctx* ctx, int64_t rows, int64_t cols, const double* A, int64_t lda,
+                 double* out) {
+  if (cols <= 0) return TK_OK;
+  col_norms_k<<<(int)((cols + 127) / 128), 128, 0, ctx->stream>>>(rows, cols, A, lda, out);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

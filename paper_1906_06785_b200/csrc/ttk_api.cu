@@ -517,11 +517,109 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
   return TK_OK;
 }
 
+// Q (rows x c) <- A (rows x c) R^{-1} with R from the unpivoted Cholesky of A^T A: one
+// CholeskyQR pass (used twice on an already well-conditioned basis).
+int cholqr_pass(tk_ctx* ctx, int64_t rows, int64_t c, const double* A, double* Q) {
+  DevBuf G, Ro, pv, st, X;
+  TK_TRY(G.get(ctx, c * c));
+  TK_TRY(tk_dgemm(ctx, true, false, c, c, rows, 1.0, A, c, A, c, 0.0, G.p, c, true));
+  TK_TRY(Ro.get(ctx, c * c));
+  TK_TRY(pv.get(ctx, (c + 1) / 2));
+  TK_TRY(st.get(ctx, (c + 3) / 2));
+  TK_TRY(tk_pchol(ctx, (int)c, G.p, 0.0, nullptr, Ro.p, (int*)pv.p, (int*)st.p, false));
+  TK_TRY(X.get(ctx, c * c));
+  TK_TRY(tk_tri_inv(ctx, (int)c, Ro.p, c, X.p, c));
+  TK_TRY(tk_dgemm(ctx, false, false, rows, c, c, 1.0, A, c, X.p, c, 0.0, Q, c));
+  return TK_OK;
+}
+
+// Pass 2 of a bond SVD, Cholesky-preconditioned:
+//   (1) pivoted Cholesky P^T G_W P = R^T R, truncated at the noise floor (rank kc; the dropped
+//       Schur trace `rem` stays in the tail);
+//   (2) relative Jacobi on X = R R^T (graded by the pivoting: 6-9 sweeps instead of 14-16), its
+//       rotations accumulated onto R^T, so the columns become sigma_i v_i (the eigenvectors of
+//       G_W, one-sided-Jacobi style) and are normalised;
+//   (3) that basis, made orthonormal by a CholeskyQR pass, turns G_W into Q^T G_W Q, which
+//       one more relative Jacobi (1-3 sweeps) diagonalises to the pass-2 accuracy; V2 = Q V2'.
+// lam (k): eigenvalues descending, then rem, then zeros; V2 (k x k): zero columns >= kc.
+// Returns TK_EARG (caller falls back to plain Jacobi) when the preconditioner does not apply.
+int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, DevBuf& lam,
+               DevBuf& V2) {
+  if (k > tk_pchol_max_n()) return TK_EARG;
+  TagScope tag(ctx, "pass2_chol");
+  DevBuf Ro, pv, st, rem, X, V0, Y, nrm, V1, Qv, T1, Gp, lam2, V2p;
+  TK_TRY(Ro.get(ctx, k * k));
+  TK_TRY(pv.get(ctx, (k + 1) / 2));
+  TK_TRY(st.get(ctx, (k + 3) / 2));
+  TK_TRY(rem.get(ctx, 1));
+  TK_TRY(tk_pchol(ctx, (int)k, GW.p, 0.0, floor, Ro.p, (int*)pv.p, (int*)st.p, true, rem.p));
+  int kc = 0;
+  TK_TRY(sync_read(ctx, &kc, st.p, sizeof(int)));
+  if (kc < 1) return TK_EARG;
+  // (2) X = Ro Ro^T (kc x kc; column order of Ro is irrelevant), V0 = Ro^T (k x kc)
+  TK_TRY(X.get(ctx, (int64_t)kc * kc));
+  TK_TRY(tk_dgemm(ctx, false, true, kc, kc, k, 1.0, Ro.p, k, Ro.p, k, 0.0, X.p, kc, true));
+  TK_TRY(V0.get(ctx, k * kc));
+  TK_TRY(tk_transpose(ctx, kc, k, Ro.p, k, V0.p, kc));
+  Ro.release();
+  TK_TRY(lam2.get(ctx, kc));
+  TK_TRY(Y.get(ctx, k * kc));
+  TK_TRY(tk_jacobi_eig(ctx, kc, X.p, lam2.p, Y.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
+                       nullptr, nullptr, 0.0, 0, floor, V0.p, (int)k));
+  TK_TRY(nrm.get(ctx, kc));
+  TK_TRY(tk_col_norms(ctx, k, kc, Y.p, kc, nrm.p));
+  TK_TRY(V1.get(ctx, k * kc));
+  TK_TRY(tk_col_scale(ctx, k, kc, Y.p, kc, V1.p, kc, nrm.p, 1));
+  // (3) orthonormal basis (columns in descending-sigma order), then the refinement Jacobi.  V1
+  // is already orthonormal up to ~1e-12 on the kept columns and O(0.1) overall, so one
+  // CholeskyQR pass gives O(eps) orthonormality (error ~ eps cond(V1)^2).
+  TK_TRY(Qv.get(ctx, k * kc));
+  TK_TRY(cholqr_pass(ctx, k, kc, V1.p, Qv.p));
+  TK_TRY(T1.get(ctx, k * kc));
+  TK_TRY(tk_dgemm(ctx, false, false, k, kc, k, 1.0, GW.p, k, Qv.p, kc, 0.0, T1.p, kc));
+  TK_TRY(Gp.get(ctx, (int64_t)kc * kc));
+  TK_TRY(tk_dgemm(ctx, true, false, kc, kc, k, 1.0, Qv.p, kc, T1.p, kc, 0.0, Gp.p, kc));
+  TK_TRY(tk_symmetrize(ctx, kc, Gp.p));
+  TK_TRY(V2p.get(ctx, (int64_t)kc * kc));
+  TK_TRY(tk_jacobi_eig(ctx, kc, Gp.p, lam2.p, V2p.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
+                       nullptr, nullptr, 0.0, 0, floor));
+  TK_TRY(lam.get(ctx, k));
+  TK_TRY(tk_fill(ctx, lam.p, k, 0.0));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(lam.p, lam2.p, sizeof(double) * kc, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+  if (kc < k)
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(lam.p + kc, rem.p, sizeof(double), cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+  TK_TRY(V2.get(ctx, k * k));
+  TK_TRY(tk_fill(ctx, V2.p, k * k, 0.0));
+  TK_TRY(tk_dgemm(ctx, false, false, k, kc, kc, 1.0, Qv.p, kc, V2p.p, kc, 0.0, V2.p, k));
+  return TK_OK;
+}
+
 int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double* lskip,
           double rs_tol, int64_t rs_rmax, const double* floor, DevBuf& lam, DevBuf& V2,
           DevBuf& Vt) {
+  static const bool plain = getenv("TTK_PASS2") && !strcmp(getenv("TTK_PASS2"), "jacobi");
+  if (!plain && !lskip && pass2_chol(ctx, k, GW, floor, lam, V2) == TK_OK) {
+    TK_TRY(Vt.get(ctx, k * k));
+    TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
+    return TK_OK;
+  }
   TK_TRY(lam.get(ctx, k));
   TK_TRY(V2.get(ctx, k * k));
+  if (const char* dump = getenv("TTK_DUMP_GW")) {
+    // diagnostic: the pass-2 Gram and its noise floor, raw fp64, to <dir>/gw_<k>_<count>.bin
+    static int cnt = 0;
+    std::vector<double> h((size_t)k * k + 1);
+    TK_TRY(sync_read(ctx, h.data(), GW.p, sizeof(double) * k * k));
+    TK_TRY(sync_read(ctx, h.data() + k * k, floor, sizeof(double)));
+    char fn[512];
+    snprintf(fn, sizeof(fn), "%s/gw_%lld_%d.bin", dump, (long long)k, cnt++);
+    if (FILE* f = fopen(fn, "wb")) {
+      fwrite(h.data(), sizeof(double), h.size(), f);
+      fclose(f);
+    }
+  }
   TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
                        nullptr, lskip, rs_tol, rs_rmax, floor));
   TK_TRY(Vt.get(ctx, k * k));

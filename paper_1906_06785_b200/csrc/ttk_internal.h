@@ -135,11 +135,14 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   entries are both <= the skip threshold are skipped (cluster skip of the bond SVDs, see
 //   k_jacobi.cu).  In: [0] static threshold.  With rs_tol > 0 the threshold is also raised
 //   each sweep to the (r + 32)-th largest diagonal (r = rank rule with rs_tol, rs_rmax).
-//   Out: [0] effective threshold, [1] 1.0 if the kept set passed the Gershgorin check.
+//   Out: [0] effective threshold, [1] bound on the unresolved block's largest eigenvalue.
+//   V0 (nullable, mv x n row-major): the rotations are accumulated onto V0 instead of the
+//   identity, and V (mv x n) returns V0 J with columns permuted like lam.
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev = nullptr,
                   double rs_tol = 0.0, int64_t rs_rmax = 0,
-                  const double* abs_floor_dev = nullptr);
+                  const double* abs_floor_dev = nullptr, const double* V0 = nullptr,
+                  int mv = 0);
 // Rounding-noise floor of a pass-2 Gram W^T W with W = fl(Y P) (K = inner dimension, k = its
 // columns): tau = (4 eps)^2 K (trG_scale * trG[0]) ||P||_F^2 / k, written to out[0] (device).
 // P == nullptr means an orthogonal P (||P||_F^2 = k).
@@ -156,8 +159,9 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
 // >= k): R in ORIGINAL column indexing, Ro[t, piv[c]] = R[t, c], so H ~ Ro^T Ro.  Stops when the
 // largest remaining Schur diagonal <= max(tol_rel * max diag(H), *tol_abs_dev).  piv (n ints):
 // pivot order (identity when !pivot).  state (2 + n ints, device): state[0] = k on completion.
+// rem_out (nullable, device): trace of the Schur complement left when it stopped (0 if full rank).
 int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* tol_abs_dev,
-             double* Ro, int* piv, int* state, bool pivot = true);
+             double* Ro, int* piv, int* state, bool pivot = true, double* rem_out = nullptr);
 int tk_pchol_max_n();
 // X = R^{-1} for the k x k upper triangular R.
 int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx);
@@ -201,3 +205,6 @@ int tk_neg_scalar(tk_ctx* ctx, const double* src, double* dst);
 int tk_transpose(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
                  double* dst, int64_t ldd);
 int tk_symmetrize(tk_ctx* ctx, int64_t n, double* A);
+// Euclidean norms of the columns of the rows x cols matrix A (ld lda) into out (device).
+int tk_col_norms(tk_ctx* ctx, int64_t rows, int64_t cols, const double* A, int64_t lda,
+                 double* out);
