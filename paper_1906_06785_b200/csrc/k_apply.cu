@@ -4,8 +4,9 @@
 //               One warp per row; the row's T*r1 outputs are written once, contiguously
 //               (the write stream is 87% of the apply's HBM bytes at c4).  U1 rows are
 //               gathered through the read-only path (L1/L2 reuse across neighbouring rows
-//               of the stencil-like K_k).  CSR (col, val) pairs are fetched 32 at a time by
-//               the warp and broadcast by shuffles.
+//               of the stencil-like K_k).  The row's CSR entries of all terms are staged
+//               in shared memory as (val, col | term << 32) pairs (lane k copies term k's) and
+//               read back as broadcasts: no per-entry shuffles on the MIO pipe.
 //  stoch_apply: Y2 = blockdiag_k (G_k x_2 U2), written densely (zeros off the blocks).
 //  time_apply : Y3[k r2 + b, :] = U3[b, :] T_k^T with T_k in LAPACK band storage.
 #include <cuda_runtime.h>
@@ -20,7 +21,7 @@ namespace {
 // V2: lane owns column pairs (16-byte loads/stores; needs r even and RPL even), else single
 // columns lane + 32 u.
 template <int RPL, bool V2>
-__global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t n_x, int T, int r,
+__global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm_multi_k(int64_t n_x, int T, int r,
                                                     const int32_t* __restrict__ rowptr,
                                                     const int32_t* __restrict__ col,
                                                     const double* __restrict__ val,
@@ -35,6 +36,9 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int UNR = 4;        // entries whose U1 rows are loaded together (memory-level parallelism)
   constexpr int STEP = V2 ? 2 : 1;
+  constexpr int ECAP = 128;     // staged entries per warp (rows with more take the slow path)
+  __shared__ double2 ent_all[256 / 32][ECAP];
+  double2* ent = ent_all[threadIdx.x >> 5];
   auto colof = [lane](int u) { return V2 ? (64 * (u >> 1) + 2 * lane + (u & 1)) : (lane + 32 * u); };
   auto put = [&](double* dst, const double* acc, int lim) {  // dst: column c0; lim = r - c0
 #pragma unroll
@@ -69,79 +73,77 @@ __global__ void __launch_bounds__(256, (RPL <= 3 ? 3 : 1)) spmm_multi_k(int64_t 
       }
       const int E = __shfl_sync(FULL, myoff, 31);
       myoff -= mycnt;
-      for (int c0 = 0; c0 < r; c0 += CW) {
-        double acc[RPL];
-#pragma unroll
-        for (int u = 0; u < RPL; u++) acc[u] = 0.0;
-        int cur = -1;  // term (within the group) whose sum is in acc
-        for (int e0 = 0; e0 < E; e0 += 32) {
-          // lane j gathers entry e0 + j of the row's concatenated term lists
-          const int g = e0 + lane;
-          int myk = kn;
-          int64_t src = 0;
-          for (int k = 0; k < kn; k++) {
-            const int ok = __shfl_sync(FULL, myoff, k), ck = __shfl_sync(FULL, mycnt, k);
-            const int64_t bk = __shfl_sync(FULL, mybeg, k);
-            if (g >= ok && g < ok + ck) {
-              myk = k;
-              src = bk + (g - ok);
-            }
-          }
-          int myc = 0;
-          double myv = 0.0;
-          if (g < E) {
-            myc = __ldg(col + src);
-            myv = __ldg(val + src);
-          }
-          const int cnt = min(32, E - e0);
-          for (int q0 = 0; q0 < cnt; q0 += UNR) {
-            double uv[UNR][RPL];
-            double vv[UNR];
-            int kk[UNR];
-#pragma unroll
-            for (int s = 0; s < UNR; s++) {
-              const int q = min(q0 + s, 31);
-              const int c = __shfl_sync(FULL, myc, q);
-              vv[s] = __shfl_sync(FULL, myv, q);
-              kk[s] = (q0 + s < cnt) ? __shfl_sync(FULL, myk, q) : -2;
-              const double* urow = U1 + (int64_t)c * r + c0;
-#pragma unroll
-              for (int u = 0; u < RPL; u += STEP) {
-                const int cc = colof(u);
-                const bool ok = kk[s] >= 0 && c0 + cc < r;
-                if (V2) {
-                  const double2 t = ok ? __ldg((const double2*)(urow + cc)) : make_double2(0.0, 0.0);
-                  uv[s][u] = t.x;
-                  uv[s][u + 1] = t.y;
-                } else {
-                  uv[s][u] = ok ? __ldg(urow + cc) : 0.0;
-                }
-              }
-            }
-#pragma unroll
-            for (int s = 0; s < UNR; s++) {
-              if (kk[s] == -2) break;
-              if (kk[s] != cur) {
-                if (cur >= 0) {
-                  put(yrow + (int64_t)(kg0 + cur) * r + c0, acc, r - c0);
-#pragma unroll
-                  for (int u = 0; u < RPL; u++) acc[u] = 0.0;
-                }
-                cur = kk[s];
-              }
-#pragma unroll
-              for (int u = 0; u < RPL; u++) acc[u] = fma(vv[s], uv[s][u], acc[u]);
-            }
+      if (E <= ECAP) {
+        // stage all of the row's entries (term-major order) in shared memory: lane k copies
+        // term k's (val, col) pairs; everyone reads them back as broadcasts
+        if (lane < kn) {
+          for (int g = 0; g < mycnt; g++) {
+            const int64_t src = mybeg + g;
+            ent[myoff + g] = make_double2(__ldg(val + src),
+                                          __longlong_as_double((long long)__ldg(col + src)));
           }
         }
-        if (cur >= 0) put(yrow + (int64_t)(kg0 + cur) * r + c0, acc, r - c0);
-        // terms with no entry in this row
-        for (int k = 0; k < kn; k++) {
-          if (__shfl_sync(FULL, mycnt, k) != 0) continue;
-          double z[RPL];
+        __syncwarp();
+        for (int c0 = 0; c0 < r; c0 += CW) {
+          for (int k = 0; k < kn; k++) {
+            const int ck = __shfl_sync(FULL, mycnt, k), ok = __shfl_sync(FULL, myoff, k);
+            double acc[RPL];
 #pragma unroll
-          for (int u = 0; u < RPL; u++) z[u] = 0.0;
-          put(yrow + (int64_t)(kg0 + k) * r + c0, z, r - c0);
+            for (int u = 0; u < RPL; u++) acc[u] = 0.0;
+            for (int q0 = 0; q0 < ck; q0 += UNR) {
+              double uv[UNR][RPL];
+              double vv[UNR];
+#pragma unroll
+              for (int s = 0; s < UNR; s++) {
+                const bool live = q0 + s < ck;  // warp-uniform
+                const double2 en = ent[ok + min(q0 + s, ck - 1)];
+                const int c = (int)__double_as_longlong(en.y);
+                vv[s] = live ? en.x : 0.0;
+                const double* urow = U1 + (int64_t)c * r + c0;
+#pragma unroll
+                for (int u = 0; u < RPL; u += STEP) {
+                  const int cc = colof(u);
+                  const bool okc = live && c0 + cc < r;
+                  if (V2) {
+                    const double2 t =
+                        okc ? __ldg((const double2*)(urow + cc)) : make_double2(0.0, 0.0);
+                    uv[s][u] = t.x;
+                    uv[s][u + 1] = t.y;
+                  } else {
+                    uv[s][u] = okc ? __ldg(urow + cc) : 0.0;
+                  }
+                }
+              }
+#pragma unroll
+              for (int s = 0; s < UNR; s++)
+#pragma unroll
+                for (int u = 0; u < RPL; u++) acc[u] = fma(vv[s], uv[s][u], acc[u]);
+            }
+            put(yrow + (int64_t)(kg0 + k) * r + c0, acc, r - c0);
+          }
+        }
+        __syncwarp();
+      } else {
+        // long row (more than ECAP entries over the group's terms): term by term from global
+        for (int c0 = 0; c0 < r; c0 += CW) {
+          for (int k = 0; k < kn; k++) {
+            const int ck = __shfl_sync(FULL, mycnt, k);
+            const int64_t bk = __shfl_sync(FULL, mybeg, k);
+            double acc[RPL];
+#pragma unroll
+            for (int u = 0; u < RPL; u++) acc[u] = 0.0;
+            for (int g = 0; g < ck; g++) {
+              const int c = __ldg(col + bk + g);
+              const double v = __ldg(val + bk + g);
+              const double* urow = U1 + (int64_t)c * r + c0;
+#pragma unroll
+              for (int u = 0; u < RPL; u++) {
+                const int cc = colof(u);
+                if (c0 + cc < r) acc[u] = fma(v, __ldg(urow + cc), acc[u]);
+              }
+            }
+            put(yrow + (int64_t)(kg0 + k) * r + c0, acc, r - c0);
+          }
         }
       }
     }
@@ -197,6 +199,7 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
   const int threads = 256;
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
+
   const int rpl = (r + 31) / 32;
 #define TK_SPMM(R, V)                                                                       \
   spmm_multi_k<R, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                        \

@@ -27,8 +27,50 @@ namespace {
 
 constexpr int PT = 512;  // threads of the panel kernel
 
+// Block-wide argmax of (v, idx) pairs (ties -> smaller index); result in (s_p, s_dmax) for all.
+__device__ __forceinline__ void block_argmax(double bv, int bi, double* s_val, int* s_idx,
+                                             int* s_p, double* s_dmax) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[warp] = bv;
+    s_idx[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? s_val[lane] : -INFINITY;
+    bi = lane < nw ? s_idx[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      *s_p = bi;
+      *s_dmax = bv;
+    }
+  }
+  __syncthreads();
+}
+
 // Panel of nb pivot steps (one CTA).  Shared memory: the panel's rows of Ro for every column
-// (sR[t * n + c], t < nb), the live Schur diagonal sd[c] and the retired flags.
+// (sR[t * n + c], t < nb) and the live Schur diagonal sd[c] (-inf once retired).  A step: row
+// j of Ro for the pivot p, the Schur diagonal update, and — fused into the same pass over the
+// columns — each thread's candidate for the NEXT pivot, reduced block-wide (two barriers per
+// step; without pivoting the next index is simply j + 1).
 __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int pivot,
                                                     const double* __restrict__ Hw,
                                                     double* __restrict__ Ro, int* __restrict__ piv,
@@ -37,7 +79,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
                                                     double* __restrict__ rem_out) {
   // state[0]: rank so far / final (k); state[1]: 1 once stopped; state[2 + c]: retired flags
   extern __shared__ double psm[];
-  double* sR = psm;                 // nb x n
+  double* sR = psm;                    // nb x n
   double* sd = psm + (int64_t)nb * n;  // n
   __shared__ double s_val[PT / 32];
   __shared__ int s_idx[PT / 32];
@@ -48,61 +90,29 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
   const double tol = tol_dev[0];
   int* retired = state + 2;
   // retired columns carry d = -inf, so they never win the argmax
-  for (int c = tid; c < n; c += PT) sd[c] = retired[c] ? -INFINITY : Hw[(int64_t)c * n + c];
-  __syncthreads();
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = tid; c < n; c += blockDim.x) {
+    const double v = retired[c] ? -INFINITY : Hw[(int64_t)c * n + c];
+    sd[c] = v;
+    if (v > bv) {  // ascending c per thread: strict > keeps the smaller index on ties
+      bv = v;
+      bi = c;
+    }
+  }
+  if (pivot) {
+    block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);
+  } else {
+    __syncthreads();
+    if (tid == 0) {
+      s_p = j0;
+      s_dmax = j0 < n ? sd[j0] : -INFINITY;
+    }
+    __syncthreads();
+  }
   for (int s = 0; s < nb; s++) {
     const int j = j0 + s;
     if (j >= n) break;
-    // (a) pivot: argmax of the live Schur diagonal (ties -> smaller index); without pivoting
-    // the next index in order
-    double bv = -INFINITY;
-    int bi = 0x7fffffff;
-    if (!pivot) {
-      if (tid == 0) {
-        s_p = j;
-        s_dmax = sd[j];
-      }
-      __syncthreads();
-    }
-    for (int c = tid; pivot && c < n; c += PT) {
-      const double v = sd[c];
-      if (v > bv) {  // ascending c per thread: strict > keeps the smaller index on ties
-        bv = v;
-        bi = c;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (pivot && lane == 0) {
-      s_val[warp] = bv;
-      s_idx[warp] = bi;
-    }
-    if (pivot) __syncthreads();
-    if (pivot && warp == 0) {
-      bv = lane < PT / 32 ? s_val[lane] : -INFINITY;
-      bi = lane < PT / 32 ? s_idx[lane] : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if (lane == 0) {
-        s_p = bi;
-        s_dmax = bv;
-      }
-    }
-    if (pivot) __syncthreads();
     const int p = s_p;
     const double dmax = s_dmax;
     if (!(dmax > tol) || p >= n) {  // uniform: rank reached (or nothing left / non-finite)
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
       if (rem_out) {
         // trace of the dropped Schur complement (its eigenvalues' sum: part of the tail)
         double t = 0.0;
-        for (int c = tid; c < n; c += PT)
+        for (int c = tid; c < n; c += blockDim.x)
           if (sd[c] != -INFINITY) t += fmax(sd[c], 0.0);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -122,20 +132,25 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
         __syncthreads();
         if (tid == 0) {
           double tt = 0.0;
-          for (int w = 0; w < PT / 32; w++) tt += s_val[w];
+          for (int w = 0; w < (int)(blockDim.x >> 5); w++) tt += s_val[w];
           rem_out[0] = tt;
         }
       }
       return;
     }
     const double r = sqrt(dmax), rinv = 1.0 / r;
-    // (b) row j of Ro:  Ro[j, c] = (Hw[p, c] - sum_{t < s} sR[t, p] sR[t, c]) / r
+    // row j of Ro:  Ro[j, c] = (Hw[p, c] - sum_{t < s} sR[t, p] sR[t, c]) / r, then the next
+    // pivot candidate among the updated live columns
     const double* hrow = Hw + (int64_t)p * n;
     double* orow = Ro + (int64_t)j * n;
-    for (int c = tid; c < n; c += PT) {
+    bv = -INFINITY;
+    bi = 0x7fffffff;
+    for (int c = tid; c < n; c += blockDim.x) {
       double out;
       if (c == p) {
         out = r;
+        sd[c] = -INFINITY;
+        retired[c] = 1;
       } else if (sd[c] == -INFINITY) {
         out = 0.0;
       } else {
@@ -150,19 +165,30 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
         }
         for (; t < s; t++) v0 = fma(-sR[t * n + p], sR[t * n + c], v0);
         out = ((v0 + v1) + (v2 + v3)) * rinv;
-        sd[c] = fma(-out, out, sd[c]);
+        const double nd = fma(-out, out, sd[c]);
+        sd[c] = nd;
+        if (nd > bv) {
+          bv = nd;
+          bi = c;
+        }
       }
       orow[c] = out;
       sR[s * n + c] = out;
     }
-    __syncthreads();
     if (tid == 0) {
-      sd[p] = -INFINITY;
-      retired[p] = 1;
       piv[j] = p;
       state[0] = j + 1;
     }
-    __syncthreads();
+    if (pivot) {
+      block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);  // also orders this step's writes
+    } else {
+      __syncthreads();
+      if (tid == 0) {
+        s_p = j + 1;
+        s_dmax = j + 1 < n ? sd[j + 1] : -INFINITY;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -278,9 +304,12 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     cudaFuncSetAttribute(pchol_panel_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
+  // balanced column ownership: every thread handles the same number of columns
+  const int per = (n + PT - 1) / PT;
+  const int threads = std::min(PT, 32 * (((n + per - 1) / per + 31) / 32));
   for (int j0 = 0; j0 < n; j0 += nb) {
     const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
-    pchol_panel_k<<<1, PT, smem, ctx->stream>>>(n, j0, nb, pivot ? 1 : 0, Hw.p, Ro, piv,
+    pchol_panel_k<<<1, threads, smem, ctx->stream>>>(n, j0, nb, pivot ? 1 : 0, Hw.p, Ro, piv,
                                                   state, tol.p, rem_out);
     TK_LAUNCH_CHECK(ctx);
     tk_prof_end(ctx, pid);

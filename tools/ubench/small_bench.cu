@@ -38,7 +38,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&dH, sizeof(double) * n * n);
   cudaMalloc(&dQ, sizeof(double) * n * n);
   cudaMalloc(&dR, sizeof(double) * n * n);
-  cudaMalloc(&piv, sizeof(int) * (n + 2) * 2);
+  cudaMalloc(&piv, sizeof(double) * (n + 2) * 2);
   cudaMalloc(&state, sizeof(int) * (n + 2));
   cudaMemcpy(dH, H.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
   cudaEvent_t a, b;
@@ -50,7 +50,14 @@ int main(int argc, char** argv) {
     int rc = 0;
     if (!strcmp(what, "qr")) rc = tk_householder_q(ctx, n, dH, dQ);
     else if (!strcmp(what, "pchol")) rc = tk_pchol(ctx, n, dH, 1e-28, nullptr, dR, piv, state, true);
-    else if (!strcmp(what, "triinv")) {
+    else if (!strcmp(what, "jacobi")) {
+      // pass-2-like relative Jacobi on the graded SPD matrix (destroys dR's copy of H)
+      cudaMemcpyAsync(dR, dH, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st);
+      cudaEventRecord(a, st);
+      int sw = 0;
+      rc = tk_jacobi_eig(ctx, n, dR, (double*)piv, dQ, 4.93e-32, 32 * 2.220446049250313e-16, 40, &sw);
+      printf("  sweeps %d\n", sw);
+    } else if (!strcmp(what, "triinv")) {
       tk_pchol(ctx, n, dH, 1e-28, nullptr, dR, piv, state, false);
       cudaEventRecord(a, st);
       rc = tk_tri_inv(ctx, n, dR, n, dQ, n);
