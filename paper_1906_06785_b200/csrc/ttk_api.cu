@@ -545,7 +545,8 @@ int cholqr_pass(tk_ctx* ctx, int64_t rows, int64_t c, const double* A, double* Q
 // Returns TK_EARG (caller falls back to plain Jacobi) when the preconditioner does not apply.
 int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, DevBuf& lam,
                DevBuf& V2) {
-  if (k > tk_pchol_max_n()) return TK_EARG;
+  // small problems: one plain Jacobi (a single 64-wide block pair) is cheaper than two
+  if (k > tk_pchol_max_n() || k <= 128) return TK_EARG;
   TagScope tag(ctx, "pass2_chol");
   DevBuf Ro, pv, st, rem, X, V0, Y, nrm, V1, Qv, T1, Gp, lam2, V2p;
   TK_TRY(Ro.get(ctx, k * k));
