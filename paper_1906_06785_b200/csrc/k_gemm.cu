@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "ttk_internal.h"
@@ -273,11 +275,23 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   }
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
-  // split-K: aim for >= 4 CTAs per SM when the output is small and K is long
-  int64_t target = 4LL * ctx->num_sms;
+  // split-K for small outputs with a long K: about four waves of resident CTAs (SMs x CTAs/SM);
+  // measured at c4 (bond-1 Gram 640 x 640 x 786432): 1 wave 15.4 ms, 2 waves 11.5, 3-6 waves
+  // 11.2-11.3 (the former "4 CTAs per SM" target gave 14.0)
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    const size_t smem = (size_t)STAGES * 2 * BM * (BK + PADK) * sizeof(double);
+    cudaFuncSetAttribute(dgemm_kernel<true, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<true, true, true>, NT,
+                                                  smem);
+    per_sm = std::max(per_sm, 1);
+  }
+  static const int mult = getenv("TTK_SPLITK_MULT") ? atoi(getenv("TTK_SPLITK_MULT")) : 4;
+  const int64_t slots = (int64_t)per_sm * ctx->num_sms * mult;
   int64_t splits = 1;
-  if (tiles < target && K >= 8 * BK) {
-    splits = std::min<int64_t>((target + tiles - 1) / tiles, (K + 8 * BK - 1) / (8 * BK));
+  if (tiles < slots && K >= 8 * BK) {
+    splits = std::min<int64_t>(std::max<int64_t>(slots / tiles, 1), (K + 8 * BK - 1) / (8 * BK));
     splits = std::max<int64_t>(splits, 1);
   }
   int64_t kchunk = (K + splits - 1) / splits;
