@@ -126,11 +126,15 @@ __global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t
   double* As = smem;
   double* Bs = smem + STAGES * GA::SIZE;
 
+  // sym bit 0: symmetric Gram (upper tiles, mirrored); bit 1: B is upper triangular (row k of
+  // B is zero beyond column k), so tile column n0 only needs k < n0 + BN
+  const int triu = sym & 2;
+  sym &= 1;
   const int tile_m = blockIdx.y, tile_n = blockIdx.x;
   if (sym && tile_n < tile_m) return;
   const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t kend = min(K, kbeg + kchunk);
+  const int64_t kend = min(triu ? min(K, n0 + BN) : K, kbeg + kchunk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int lr = lane >> 2, lc = lane & 3;
@@ -258,7 +262,7 @@ int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const doub
 
 int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-             double beta, double* C, int64_t ldc, bool sym) {
+             double beta, double* C, int64_t ldc, bool sym, bool triu_b) {
   if (M <= 0 || N <= 0) return TK_OK;
   if (sym && M != N) {
     ctx->err = "tk_dgemm: sym requires M == N";
@@ -304,7 +308,9 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
     partial = pbuf.p;
   }
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
-  const double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
+  double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
+  if (triu_b)
+    flops = K >= N ? (double)M * N * (N + 1) : 2.0 * M * (K * (K + 1) / 2.0 + (double)(N - K) * K);
   const double bytes = 8.0 * ((double)M * K + (sym ? 0.0 : (double)K * N) + (double)M * N);
   const int prof_id = tk_prof_begin(ctx, ctx->tag, flops, bytes);
   const bool AK = transA, BKm = !transB;
@@ -315,7 +321,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 #define TK_GEMM_CASE(a, b, v)                                                             \
   if (AK == a && BKm == b && v2 == v)                                                     \
     st = launch_t<a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, \
-                           sym ? 1 : 0, partial);
+                           (sym ? 1 : 0) | (triu_b ? 2 : 0), partial);
   TK_GEMM_CASE(false, false, false)
   TK_GEMM_CASE(false, false, true)
   TK_GEMM_CASE(false, true, false)

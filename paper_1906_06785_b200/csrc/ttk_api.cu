@@ -373,7 +373,7 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
     //   W P1 = Q1 R1 (pivoted Cholesky of W^T W, truncated at the numerical rank k1),
     //   Q1 = W P1 R1^{-1},  Q1 = Q2 R2 (second pass: restores orthonormality to O(eps)),
     //   A = L Q2^T  with  L = V (Ro2 Ro1)^T  (Ro = R P^T in original column indexing).
-    DevBuf Ro1, pv1, st1, R11, X1, S1, Q1, G2, Ro2, pv2, st2, R22, X2, S2, M;
+    DevBuf Ro1, pv1, st1, R11, X1, S1, Q1, G2, Ro2, pv2, st2, R22, X2, M;
     TK_TRY(Ro1.get(ctx, R * R));
     TK_TRY(pv1.get(ctx, (R + 1) / 2));
     TK_TRY(st1.get(ctx, (R + 3) / 2));
@@ -386,11 +386,14 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
       TK_TRY(tk_gather_cols(ctx, k1, k1, Ro1.p, R, (const int*)pv1.p, R11.p));
       TK_TRY(X1.get(ctx, (int64_t)k1 * k1));
       TK_TRY(tk_tri_inv(ctx, k1, R11.p, k1, X1.p, k1));
-      TK_TRY(S1.get(ctx, R * k1));
-      TK_TRY(tk_scatter_rows(ctx, R, k1, k1, X1.p, (const int*)pv1.p, S1.p));
-      TK_TRY(Q1.get(ctx, N * k1));
-      TK_TRY(tk_dgemm(ctx, false, false, N, k1, R, 1.0, W.p, R, S1.p, k1, 0.0, Q1.p, k1));
+      // Q1 = W[:, piv1[:k1]] R11^{-1}: gather W's pivot columns, then a triangular product
+      TK_TRY(S1.get(ctx, N * k1));
+      TK_TRY(tk_gather_cols(ctx, N, k1, W.p, R, (const int*)pv1.p, S1.p));
       W.release();
+      TK_TRY(Q1.get(ctx, N * k1));
+      TK_TRY(tk_dgemm(ctx, false, false, N, k1, k1, 1.0, S1.p, k1, X1.p, k1, 0.0, Q1.p, k1, false,
+                      true));
+      S1.release();
       TK_TRY(G2.get(ctx, (int64_t)k1 * k1));
       TK_TRY(tk_dgemm(ctx, true, false, k1, k1, N, 1.0, Q1.p, k1, Q1.p, k1, 0.0, G2.p, k1, true));
       TK_TRY(Ro2.get(ctx, (int64_t)k1 * k1));
@@ -407,10 +410,10 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
         TK_TRY(tk_gather_cols(ctx, k2, k2, Ro2.p, k1, (const int*)pv2.p, R22.p));
         TK_TRY(X2.get(ctx, (int64_t)k2 * k2));
         TK_TRY(tk_tri_inv(ctx, k2, R22.p, k2, X2.p, k2));
-        TK_TRY(S2.get(ctx, (int64_t)k1 * k2));
-        TK_TRY(tk_scatter_rows(ctx, k1, k2, k2, X2.p, (const int*)pv2.p, S2.p));
+        // unpivoted second pass: piv2 is the identity and R2^{-1} is upper triangular
         TK_TRY(Qc.get(ctx, N * k2));
-        TK_TRY(tk_dgemm(ctx, false, false, N, k2, k1, 1.0, Q1.p, k1, S2.p, k2, 0.0, Qc.p, k2));
+        TK_TRY(tk_dgemm(ctx, false, false, N, k2, k2, 1.0, Q1.p, k1, X2.p, k2, 0.0, Qc.p, k2,
+                        false, true));
         // M = Ro2[:k2] Ro1[:k1]  (k2 x R);  L = V M^T  (R x k2)
         TK_TRY(M.get(ctx, (int64_t)k2 * R));
         TK_TRY(tk_dgemm(ctx, false, false, k2, R, k1, 1.0, Ro2.p, k1, Ro1.p, R, 0.0, M.p, R));
