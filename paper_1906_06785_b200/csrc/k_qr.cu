@@ -15,6 +15,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -189,64 +192,147 @@ __device__ __forceinline__ void make_reflector(double* psm, int c, int m, int la
 __global__ void __launch_bounds__(32 * QB)
     qr_panel_warp_k(int m, int jb, const double* __restrict__ Pg, int64_t ldg,
                     double* __restrict__ Vout, double* __restrict__ Tout,
-                    double* __restrict__ VTout, double* __restrict__ VTtout) {
-  extern __shared__ double psm[];
-  __shared__ double s_tau[QB], s_z[2][QB];
+                    double* __restrict__ VTout, double* __restrict__ VTtout,
+                    const double* __restrict__ Vprev, const double* __restrict__ VTtprev,
+                    unsigned long long* __restrict__ dbg) {
+  // Vprev / VTtprev (nullable): the previous panel's reflector block, still to be applied to
+  // this panel's columns (look-ahead without a separate launch).  Then Pg points QB rows higher
+  // (the previous panel's diagonal row) and m + QB rows are loaded; H_prev = I - V T V^T acts
+  // on all of them, and the factorisation proceeds on the lower m rows.
+  extern __shared__ double psm_all[];
+  __shared__ double s_tau[QB], s_z[QB][QB];
   __shared__ double Ts[QB][QB + 1];
+  __shared__ double s_w[QB][QB + 1];
+  auto stamp = [&](int k) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[k] = t;
+    }
+  };
+  stamp(0);
   constexpr int LD = QB + 1;
   constexpr int NT = 32 * QB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int off = Vprev ? QB : 0;  // extra leading rows (the previous panel's block rows)
+  const int mt = m + off;
   // panel -> shared memory, 8 loads in flight per thread (thread's column j = tid % QB is fixed)
   {
     const int j = tid % QB;
-    for (int i0 = tid / QB; i0 < m; i0 += 8 * (NT / QB)) {
+    for (int i0 = tid / QB; i0 < mt; i0 += 8 * (NT / QB)) {
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         const int i = i0 + u * (NT / QB);
-        v[u] = (i < m && j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
+        v[u] = (i < mt && j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         const int i = i0 + u * (NT / QB);
-        if (i < m) psm[i * LD + j] = v[u];
+        if (i < mt) psm_all[i * LD + j] = v[u];
       }
     }
   }
   for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
   __syncthreads();
+  if (Vprev) {
+    // W = V_prev^T C (QB x QB): warp q forms row q (lanes over rows, 16 column sums each)
+    {
+      const int q = warp;
+      double acc[QB];
+#pragma unroll
+      for (int j = 0; j < QB; j++) acc[j] = 0.0;
+      for (int i = lane; i < mt; i += 32) {
+        const double v = __ldg(Vprev + (int64_t)i * QB + q);
+#pragma unroll
+        for (int j = 0; j < QB; j++) acc[j] = fma(v, psm_all[i * LD + j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < QB; j++) {
+        const double t = warp_sum(acc[j]);
+        if (lane == 0) s_w[q][j] = t;
+      }
+    }
+    __syncthreads();
+    // C -= (V T^T) W
+    {
+      const int j = tid % QB;
+      double w[QB];
+#pragma unroll
+      for (int q = 0; q < QB; q++) w[q] = s_w[q][j];
+      for (int i = tid / QB; i < mt; i += NT / QB) {
+        const double2* xr = reinterpret_cast<const double2*>(VTtprev + (int64_t)i * QB);
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < QB / 2; q++) {
+          const double2 x = __ldg(xr + q);
+          d = fma(x.x, w[2 * q], d);
+          d = fma(x.y, w[2 * q + 1], d);
+        }
+        psm_all[i * LD + j] -= d;
+      }
+    }
+    __syncthreads();
+  }
+  double* psm = psm_all + off * LD;  // this panel's m rows
+  stamp(1);
   if (warp == 0 && jb > 0) make_reflector(psm, 0, m, lane, s_tau);
   __syncthreads();
+  stamp(2);
   for (int c = 0; c < jb; c++) {
     const double tau = s_tau[c];
     if (warp > c && warp < jb) {
       const int j = warp;
+      const bool fs = dbg && c == 4 && j == 5 && lane == 0;
+      auto fst = [&](int k) {
+        if (fs) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          dbg[k] = t;
+        }
+      };
+      fst(5);
       // row c counted once (v_c = 1)
       double w = col_dot<LD>(psm, c, j, c + 1, m, lane) + (lane == 0 ? psm[c * LD + j] : 0.0);
+      fst(6);
       w = warp_sum(w) * tau;
+      fst(7);
       if (lane == 0) psm[c * LD + j] -= w;
 #pragma unroll 4
       for (int i = c + 1 + lane; i < m; i += 32) psm[i * LD + j] = fma(-w, psm[i * LD + c], psm[i * LD + j]);
       __syncwarp();
+      fst(8);
       if (j == c + 1) make_reflector(psm, j, m, lane, s_tau);
+      fst(9);
     } else if (warp < c) {
       const int j = warp;
-      // z_j = V[:, j]^T v over rows >= c (v is zero above c; V[c, j] is stored below diag j)
+      // z_j = V[:, j]^T v_c over rows >= c (v_c is zero above c; V[c, j] is stored below diag j)
       double z = col_dot<LD>(psm, j, c, c + 1, m, lane) + (lane == 0 ? psm[c * LD + j] : 0.0);
       z = warp_sum(z);
-      if (lane == 0) s_z[c & 1][j] = z;
+      if (lane == 0) s_z[c][j] = z;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (dbg && c == 4 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[10] = t;
+    }
+  }
+  // T (dlarft, forward, columnwise) off the column loop's critical path:
+  //   T[0:c, c] = -tau_c T[0:c, 0:c] z_c,  T[c, c] = tau_c
+  if (warp == 0) {
+    for (int c = 0; c < jb; c++) {
       if (lane < c) {
         double t = 0.0;
-        for (int q = lane; q < c; q++) t = fma(Ts[lane][q], s_z[c & 1][q], t);
-        Ts[lane][c] = -tau * t;
+        for (int q = lane; q < c; q++) t = fma(Ts[lane][q], s_z[c][q], t);
+        Ts[lane][c] = -s_tau[c] * t;
       }
-      if (lane == 0) Ts[c][c] = tau;
+      if (lane == 0) Ts[c][c] = s_tau[c];
+      __syncwarp();
     }
   }
   __syncthreads();
+  stamp(3);
   // V (unit lower trapezoidal) into shared memory in place, then V, V T and V T^T out; the
   // thread's column j = tid % QB is fixed, so column j and row j of T stay in registers
   const int j = tid % QB;
@@ -282,6 +368,243 @@ __global__ void __launch_bounds__(32 * QB)
     VTtout[e] = b;
   }
   for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
+  __syncthreads();
+  stamp(4);
+}
+
+// Register-resident panel factorisation (m + off <= 32 * MAXR): warp j holds column j of the
+// panel in registers (lane l, slot k <-> row i = l + 32 k, rows counted from the first loaded
+// row), so the column loop touches shared memory only to publish each reflector v_c (double
+// buffered) — the shared-memory version above was bandwidth-bound on the 15 warps re-reading
+// v_c and their own columns every column (measured ~2.5 us per column at m ~ 450).
+// Same contract as qr_panel_warp_k (including the fused look-ahead application of H_prev).
+template <int MAXR>
+__global__ void __launch_bounds__(32 * QB)
+    qr_panel_reg_k(int m, int jb, const double* __restrict__ Pg, int64_t ldg,
+                   double* __restrict__ Vout, double* __restrict__ Tout,
+                   double* __restrict__ VTout, double* __restrict__ VTtout,
+                   const double* __restrict__ Vprev, const double* __restrict__ VTtprev,
+                   unsigned long long* __restrict__ dbg) {
+  auto stamp = [&](int k) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[k] = t;
+    }
+  };
+  stamp(0);
+  constexpr int LD = QB + 1;
+  constexpr int MR = 32 * MAXR;
+  constexpr int NT = 32 * QB;
+  __shared__ double vbuf[2][MR];
+  __shared__ double s_tau[QB], s_z[QB][QB];
+  __shared__ double Ts[QB][QB + 1];
+  __shared__ double s_w[2][QB][QB + 1];
+  // dynamic shared memory: the loaded panel (mt x LD) — staging for the look-ahead update and
+  // the register columns, reused at the end for the export of V (m x LD)
+  extern __shared__ double psm[];
+  const int tid = threadIdx.x, lane = tid & 31, j = tid >> 5;
+  const int off = Vprev ? QB : 0;
+  const int mt = m + off;
+  // panel -> shared memory (coalesced rows), 8 loads in flight per thread
+  {
+    const int jj = tid % QB;
+    for (int i0 = tid / QB; i0 < mt; i0 += 8 * (NT / QB)) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int i = i0 + u * (NT / QB);
+        v[u] = (i < mt && jj < jb) ? Pg[(int64_t)i * ldg + jj] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int i = i0 + u * (NT / QB);
+        if (i < mt) psm[i * LD + jj] = v[u];
+      }
+    }
+  }
+  for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
+  __syncthreads();
+  if (Vprev) {
+    // W = V_prev^T C (QB x QB): thread -> (q, jj, half); V_prev rows streamed from global
+    // (each warp reads two q's of a row: near-broadcast), C from shared memory
+    {
+      const int jj = tid % QB, q = (tid / QB) % QB, h = tid / (QB * QB);
+      double acc0 = 0.0, acc1 = 0.0;
+      int i = h;
+      for (; i + 2 < mt; i += 4) {
+        acc0 = fma(__ldg(Vprev + (int64_t)i * QB + q), psm[i * LD + jj], acc0);
+        acc1 = fma(__ldg(Vprev + (int64_t)(i + 2) * QB + q), psm[(i + 2) * LD + jj], acc1);
+      }
+      for (; i < mt; i += 2) acc0 = fma(__ldg(Vprev + (int64_t)i * QB + q), psm[i * LD + jj], acc0);
+      s_w[h][q][jj] = acc0 + acc1;
+    }
+    __syncthreads();
+    // C -= (V_prev T_prev^T) W
+    {
+      const int jj = tid % QB;
+      double w[QB];
+#pragma unroll
+      for (int q = 0; q < QB; q++) w[q] = s_w[0][q][jj] + s_w[1][q][jj];
+      for (int i = tid / QB; i < mt; i += NT / QB) {
+        const double2* xr = reinterpret_cast<const double2*>(VTtprev + (int64_t)i * QB);
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < QB / 2; q++) {
+          const double2 x = __ldg(xr + q);
+          d = fma(x.x, w[2 * q], d);
+          d = fma(x.y, w[2 * q + 1], d);
+        }
+        psm[i * LD + jj] -= d;
+      }
+    }
+    __syncthreads();
+  }
+  double c[MAXR];
+#pragma unroll
+  for (int k = 0; k < MAXR; k++) {
+    const int i = lane + 32 * k;
+    c[k] = (i < mt) ? psm[i * LD + j] : 0.0;
+  }
+  __syncthreads();  // psm is reused for the export below
+  stamp(1);
+  stamp(2);
+  // reflector of column j from its rows i >= r0 = j + off (register column), v -> vbuf[buf]
+  auto reflect = [&](int buf) {
+    const int r0 = j + off;
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXR; k++) {
+      const int i = lane + 32 * k;
+      if (i > r0 && i < mt) sq = fma(c[k], c[k], sq);
+    }
+    sq = warp_sum(sq);
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXR; k++)
+      if (lane + 32 * k == r0) a = c[k];
+    const double alpha = __shfl_sync(0xffffffffu, a, r0 & 31);
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (sq > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, sq));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+#pragma unroll
+    for (int k = 0; k < MAXR; k++) {
+      const int i = lane + 32 * k;
+      double v = 0.0;
+      if (i > r0 && i < mt) {
+        c[k] *= scale;
+        v = c[k];
+      } else if (i == r0) {
+        c[k] = 1.0;  // v_j(r0) = 1 (the R entry beta is not needed)
+        v = 1.0;
+      } else if (i < r0) {
+        c[k] = 0.0;
+      }
+      if (i < MR) vbuf[buf][i] = v;
+    }
+    if (lane == 0) s_tau[j] = tau;
+  };
+  if (j == 0 && jb > 0) reflect(0);
+  __syncthreads();
+  for (int cc = 0; cc < jb; cc++) {
+    const int buf = cc & 1;
+    const double tau = s_tau[cc];
+    const int r0 = cc + off;
+    if (j > cc && j < jb) {
+      const bool fs = dbg && cc == 4 && j == 5 && lane == 0;
+      auto fst = [&](int k) {
+        if (fs) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          dbg[k] = t;
+        }
+      };
+      fst(5);
+      // v_cc read once into registers (shared-memory bandwidth is the limit: every active
+      // warp needs all of v_cc each column), two partial sums
+      double vr[MAXR];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) {
+        const int i = lane + 32 * k;
+        vr[k] = (i >= r0 && i < mt) ? vbuf[buf][i] : 0.0;
+        if (k & 1)
+          w1 = fma(vr[k], c[k], w1);
+        else
+          w0 = fma(vr[k], c[k], w0);
+      }
+      fst(6);
+      const double w = warp_sum(w0 + w1) * tau;
+      fst(7);
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) c[k] = fma(-w, vr[k], c[k]);
+      fst(8);
+      if (j == cc + 1) reflect(buf ^ 1);
+      fst(9);
+    } else if (j < cc) {
+      // z_j = V[:, j]^T v_cc (register column j is v_j: zeros above its diagonal)
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) {
+        const int i = lane + 32 * k;
+        const double v = (i >= r0 && i < mt) ? vbuf[buf][i] : 0.0;
+        if (k & 1)
+          z1 = fma(v, c[k], z1);
+        else
+          z0 = fma(v, c[k], z0);
+      }
+      const double z = warp_sum(z0 + z1);
+      if (lane == 0) s_z[cc][j] = z;
+    }
+    __syncthreads();
+  }
+  // T (dlarft, forward, columnwise): T[0:c, c] = -tau_c T[0:c, 0:c] z_c, T[c, c] = tau_c
+  if (j == 0) {
+    for (int cc = 0; cc < jb; cc++) {
+      if (lane < cc) {
+        double t = 0.0;
+        for (int q = lane; q < cc; q++) t = fma(Ts[lane][q], s_z[cc][q], t);
+        Ts[lane][cc] = -s_tau[cc] * t;
+      }
+      if (lane == 0) Ts[cc][cc] = s_tau[cc];
+      __syncwarp();
+    }
+  }
+  stamp(3);
+  // V (rows off .. mt-1 of the register columns; zero columns beyond jb) to shared memory
+#pragma unroll
+  for (int k = 0; k < MAXR; k++) {
+    const int i = lane + 32 * k;
+    if (i >= off && i < mt) psm[(i - off) * LD + j] = (j < jb) ? c[k] : 0.0;
+  }
+  __syncthreads();
+  const int jj = tid % QB;
+  double tc[QB], tr[QB];
+#pragma unroll
+  for (int q = 0; q < QB; q++) {
+    tc[q] = Ts[q][jj];
+    tr[q] = Ts[jj][q];
+  }
+  for (int e = tid; e < m * QB; e += blockDim.x) {
+    const int i = e / QB;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int q = 0; q < QB; q++) {
+      const double v = psm[i * LD + q];
+      a = fma(v, tc[q], a);
+      b = fma(v, tr[q], b);
+    }
+    Vout[e] = psm[i * LD + jj];
+    VTout[e] = a;
+    VTtout[e] = b;
+  }
+  for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
+  __syncthreads();
+  stamp(4);
 }
 
 // C <- C - X (V^T C) for the m x nc block C (leading dimension ldc) and the m x QB panels V, X
@@ -359,6 +682,46 @@ __global__ void __launch_bounds__(AR_T) apply_reflector_k(int m, int nc, const d
   }
 }
 
+// C <- C H = C - (C V) (V T^T)^T for the n x m block C (leading dimension ldc): the forward
+// accumulation Q <- Q H_p of the orthogonal factor.  Rows are independent: one warp per row,
+// lanes over the columns; w = C[i, :] V (16 sums, warp-reduced), then C[i, c] -= w . VTt[c, :].
+__global__ void __launch_bounds__(256) apply_reflector_right_k(int n, int m,
+                                                               const double* __restrict__ V,
+                                                               const double* __restrict__ VTt,
+                                                               double* __restrict__ C,
+                                                               int64_t ldc) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n) return;
+  double* row = C + (int64_t)i * ldc;
+  double w[QB];
+#pragma unroll
+  for (int q = 0; q < QB; q++) w[q] = 0.0;
+  for (int c = lane; c < m; c += 32) {
+    const double x = row[c];
+    const double2* vr = reinterpret_cast<const double2*>(V + (int64_t)c * QB);
+#pragma unroll
+    for (int q = 0; q < QB / 2; q++) {
+      const double2 v = __ldg(vr + q);
+      w[2 * q] = fma(x, v.x, w[2 * q]);
+      w[2 * q + 1] = fma(x, v.y, w[2 * q + 1]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QB; q++) w[q] = warp_sum(w[q]);
+  for (int c = lane; c < m; c += 32) {
+    const double2* yr = reinterpret_cast<const double2*>(VTt + (int64_t)c * QB);
+    double d = 0.0;
+#pragma unroll
+    for (int q = 0; q < QB / 2; q++) {
+      const double2 y = __ldg(yr + q);
+      d = fma(w[2 * q], y.x, d);
+      d = fma(w[2 * q + 1], y.y, d);
+    }
+    row[c] -= d;
+  }
+}
+
 }  // namespace
 
 // Q (n x n, row-major) from the Householder QR of A (n x n, row-major; A is not modified).
@@ -374,53 +737,145 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   TK_TRY(VTb.get(ctx, (size_t)np * n * QB));
   TK_TRY(VTtb.get(ctx, (size_t)np * n * QB));
   TK_TRY(Tb.get(ctx, (size_t)np * QB * QB));
-  for (int p = 0; p < np; p++) {
+  TK_TRY(tk_eye(ctx, Q, n));
+  static const bool dbg = getenv("TTK_DEBUG_QR") != nullptr;
+  DevBuf dbgb;
+  if (dbg) TK_TRY(dbgb.get(ctx, 12 * (size_t)np));
+  // Streams: s0 (ctx->stream) carries the critical path  F_0, U_0', F_1, U_1', ...  where F_p
+  // factors panel p and U_p' applies H_p to panel p+1 only; s1 applies H_p to the columns
+  // beyond panel p+1 (overlapping F_{p+1}); s2 accumulates Q <- Q H_p forward (overlapping
+  // everything).  evF[p]: V_p ready; evR[p]: H_p applied beyond panel p+1.
+  TK_TRY(tk_aux_streams(ctx, 2 * (size_t)np + 2));
+  cudaStream_t s0 = ctx->stream, s1 = ctx->aux[0], s2 = ctx->aux[1];
+  static const bool serial = getenv("TTK_QR_SERIAL") != nullptr;
+  if (serial) s1 = s2 = s0;
+  cudaEvent_t* evF = ctx->fork_ev.data();
+  cudaEvent_t* evR = evF + np;
+  cudaEvent_t evStart = evF[2 * np], evEnd = evF[2 * np + 1];
+  TK_CUDA_TRY(ctx, cudaEventRecord(evStart, s0));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s1, evStart, 0));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s2, evStart, 0));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(qr_panel_warp_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  // factor(p): panel p; with look-ahead (p > 0) the kernel first applies H_{p-1} itself
+  auto factor = [&](int p) -> int {
     const int j0 = p * QB, jb = std::min(QB, n - j0), m = n - j0;
     double* Vp = Vb.p + (size_t)p * n * QB;
     double* VTp = VTb.p + (size_t)p * n * QB;
     double* VTtp = VTtb.p + (size_t)p * n * QB;
     double* Tp = Tb.p + (size_t)p * QB * QB;
     const int pid = tk_prof_begin(ctx, "qr_panel", 2.0 * m * (double)jb * jb, 0.0);
-    const size_t psmem = (size_t)m * (QB + 1) * sizeof(double);
+    const int off = p > 0 ? QB : 0;
+    const int mt = m + off;
+    const double* Vq0 = p > 0 ? Vb.p + (size_t)(p - 1) * n * QB : nullptr;
+    const double* VTtq0 = p > 0 ? VTtb.p + (size_t)(p - 1) * n * QB : nullptr;
+    if (mt <= 32 * 28) {
+      // register-resident columns
+      const size_t rsmem = sizeof(double) * (size_t)mt * (QB + 1);
+      const double* Pp = Aw.p + (int64_t)(j0 - off) * n + j0;
+#define TK_QR_REG(MR)                                                                        \
+  {                                                                                          \
+    static bool at = false;                                                                  \
+    if (!at) {                                                                               \
+      cudaFuncSetAttribute(qr_panel_reg_k<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           200 * 1024);                                                      \
+      at = true;                                                                             \
+    }                                                                                        \
+    qr_panel_reg_k<MR><<<1, 32 * QB, rsmem, s0>>>(m, jb, Pp, n, Vp, Tp, VTp, VTtp, Vq0, VTtq0, \
+        dbgb.p ? (unsigned long long*)dbgb.p + 12 * p : nullptr);                             \
+  }
+      if (mt <= 32 * 8)
+        TK_QR_REG(8)
+      else if (mt <= 32 * 16)
+        TK_QR_REG(16)
+      else
+        TK_QR_REG(28)
+#undef TK_QR_REG
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
+      TK_CUDA_TRY(ctx, cudaEventRecord(evF[p], s0));
+      return TK_OK;
+    }
+    const size_t psmem = (size_t)(m + off) * (QB + 1) * sizeof(double);
     if (psmem <= 200 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(qr_panel_warp_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attr = true;
-      }
-      qr_panel_warp_k<<<1, 32 * QB, psmem, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n,
-                                                          Vp, Tp, VTp, VTtp);
+      const double* Vq = p > 0 ? Vb.p + (size_t)(p - 1) * n * QB : nullptr;
+      const double* VTtq = p > 0 ? VTtb.p + (size_t)(p - 1) * n * QB : nullptr;
+      qr_panel_warp_k<<<1, 32 * QB, psmem, s0>>>(
+          m, jb, Aw.p + (int64_t)(j0 - off) * n + j0, n, Vp, Tp, VTp, VTtp, Vq, VTtq,
+          dbgb.p ? (unsigned long long*)dbgb.p + 12 * p : nullptr);
       TK_LAUNCH_CHECK(ctx);
       tk_prof_end(ctx, pid);
     } else {
-      qr_panel_k<false><<<1, QT, 0, ctx->stream>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+      if (p > 0) {
+        // no room for the fused look-ahead: apply H_{p-1} to this panel first
+        const int mp = m + QB;
+        apply_reflector_k<<<(jb + AR_W - 1) / AR_W, AR_T, 0, s0>>>(
+            mp, jb, Vb.p + (size_t)(p - 1) * n * QB, VTtb.p + (size_t)(p - 1) * n * QB,
+            Aw.p + (int64_t)(j0 - QB) * n + j0, n);
+        TK_LAUNCH_CHECK(ctx);
+      }
+      qr_panel_k<false><<<1, QT, 0, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
       TK_LAUNCH_CHECK(ctx);
       tk_prof_end(ctx, pid);
       TK_TRY(tk_dgemm(ctx, false, false, m, QB, QB, 1.0, Vp, QB, Tp, QB, 0.0, VTp, QB));
       TK_TRY(tk_dgemm(ctx, false, true, m, QB, QB, 1.0, Vp, QB, Tp, QB, 0.0, VTtp, QB));
     }
-    const int nt = n - (j0 + jb);
-    if (nt > 0) {
-      // A_t <- H_p^T A_t = A_t - (V T^T) (V^T A_t)
-      double* At = Aw.p + (int64_t)j0 * n + j0 + jb;
-      const int rid = tk_prof_begin(ctx, "qr_reflector", 4.0 * m * (double)nt * QB, 0.0);
-      apply_reflector_k<<<(nt + AR_W - 1) / AR_W, AR_T, 0, ctx->stream>>>(m, nt, Vp, VTtp, At, n);
+    TK_CUDA_TRY(ctx, cudaEventRecord(evF[p], s0));
+    return TK_OK;
+  };
+  TK_TRY(factor(0));
+  for (int p = 0; p < np; p++) {
+    const int j0 = p * QB, jb = std::min(QB, n - j0), m = n - j0;
+    const double* Vp = Vb.p + (size_t)p * n * QB;
+    const double* VTtp = VTtb.p + (size_t)p * n * QB;
+    const int c1 = j0 + jb;                     // first column of panel p+1
+    const int nnext = std::min(QB, n - c1);     // its width (<= 0 at the last panel)
+    const int c2 = c1 + std::max(nnext, 0);     // first column beyond panel p+1
+    // s1: H_p on the columns beyond panel p+1
+    TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s1, evF[p], 0));
+    if (n - c2 > 0) {
+      apply_reflector_k<<<(n - c2 + AR_W - 1) / AR_W, AR_T, 0, s1>>>(
+          m, n - c2, Vp, VTtp, Aw.p + (int64_t)j0 * n + c2, n);
       TK_LAUNCH_CHECK(ctx);
-      tk_prof_end(ctx, rid);
+    }
+    TK_CUDA_TRY(ctx, cudaEventRecord(evR[p], s1));
+    // s2: Q <- Q H_p (all n rows, columns j0..n)
+    TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s2, evF[p], 0));
+    apply_reflector_right_k<<<(n + 7) / 8, 256, 0, s2>>>(n, m, Vp, VTtp, Q + j0, n);
+    TK_LAUNCH_CHECK(ctx);
+    // s0: panel p+1 (its columns got H_{p-1} from s1; it applies H_p itself), then factor it
+    if (nnext > 0) {
+      if (p > 0) TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evR[p - 1], 0));
+      TK_TRY(factor(p + 1));
     }
   }
-  // Q = H_1 ... H_np : backward accumulation from the identity, Qs <- Qs - (V T) (V^T Qs)
-  TK_TRY(tk_eye(ctx, Q, n));
-  for (int p = np - 1; p >= 0; p--) {
-    const int j0 = p * QB, m = n - j0;
-    double* Vp = Vb.p + (size_t)p * n * QB;
-    double* VTp = VTb.p + (size_t)p * n * QB;
-    double* Qs = Q + (int64_t)j0 * n + j0;
-    const int rid = tk_prof_begin(ctx, "qr_reflector", 4.0 * m * (double)m * QB, 0.0);
-    apply_reflector_k<<<(m + AR_W - 1) / AR_W, AR_T, 0, ctx->stream>>>(m, m, Vp, VTp, Qs, n);
-    TK_LAUNCH_CHECK(ctx);
-    tk_prof_end(ctx, rid);
+  // join: everything on s1 / s2 before s0 continues (and before the scratch buffers are freed)
+  TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s1));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
+  TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s2));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
+  if (dbg) {
+    std::vector<unsigned long long> h(12 * (size_t)np);
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), dbgb.p, 8 * h.size(), cudaMemcpyDeviceToHost, s0));
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(s0));
+    double a[4] = {0, 0, 0, 0}, gap = 0, f[5] = {0, 0, 0, 0, 0};
+    int nf = 0;
+    for (int p = 0; p < np; p++) {
+      for (int k = 0; k < 4; k++) a[k] += (h[12 * p + k + 1] - h[12 * p + k]) * 1e-3;
+      if (p) gap += (h[12 * p] - h[12 * (p - 1) + 4]) * 1e-3;
+      if (n - p * QB > 6 * QB) {
+        for (int k = 0; k < 5; k++) f[k] += (h[12 * p + 6 + k] - h[12 * p + 5 + k]) * 1e-3;
+        nf++;
+      }
+    }
+    if (nf)
+      fprintf(stderr, "[ttk]   column 4, critical warp (us): dot %.2f warp_sum %.2f update %.2f reflector %.2f barrier %.2f\n",
+              f[0] / nf, f[1] / nf, f[2] / nf, f[3] / nf, f[4] / nf);
+    fprintf(stderr, "[ttk] qr n=%d per panel us: load %.1f refl0 %.1f columns %.1f export %.1f | gap between panels %.1f (nf %d, raw %llu %llu)\n",
+            n, a[0] / np, a[1] / np, a[2] / np, a[3] / np, gap / std::max(np - 1, 1), nf, h[5], h[10]);
   }
   return TK_OK;
 }

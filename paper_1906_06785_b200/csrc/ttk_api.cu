@@ -82,9 +82,26 @@ extern "C" int tk_ctx_create(tk_ctx** out, void* stream) {
   return TK_OK;
 }
 
+int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
+  for (auto& s : ctx->aux)
+    if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  while (ctx->fork_ev.size() < n_events) {
+    cudaEvent_t e;
+    TK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->fork_ev.push_back(e);
+  }
+  return TK_OK;
+}
+
 extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
   if (!ctx) return TK_OK;
   cudaStreamSynchronize(ctx->stream);
+  for (auto& s : ctx->aux)
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  for (auto e : ctx->fork_ev) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return TK_OK;

@@ -35,7 +35,13 @@ struct tk_ctx {
   // scratch accounting (tk_alloc / tk_free) and the pool reservation made from it
   std::unordered_map<void*, size_t> live;
   size_t live_bytes = 0, high_bytes = 0, reserved_for = 0;
+  // side streams for work that overlaps the latency-bound critical path (Householder pass 1),
+  // forked from / joined to `stream` with events; created on first use
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> fork_ev;
 };
+// Lazily created side streams and a pool of at least n sync events (timing disabled).
+int tk_aux_streams(tk_ctx* ctx, size_t n_events);
 
 // Scoped phase tag for profiling records.
 struct TagScope {

@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <algorithm>
+#include <cmath>
 #include <cuda_runtime.h>
 #include "../../paper_1906_06785_b200/csrc/ttk_internal.h"
 
@@ -67,6 +69,27 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     printf("%s n=%d rc=%d total %.3f ms\n", what, n, rc, ms);
+    if (rep == 2 && !strcmp(what, "qr")) {
+      // orthogonality of Q and the triangularity of Q^T H (first 64 columns), on the host
+      std::vector<double> hq((size_t)n * n);
+      cudaMemcpy(hq.data(), dQ, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      double eo = 0.0, et = 0.0;
+      for (int i = 0; i < n; i++)
+        for (int j = 0; j <= i; j++) {
+          double s = 0.0;
+          for (int k = 0; k < n; k++) s += hq[(size_t)k * n + i] * hq[(size_t)k * n + j];
+          eo = std::max(eo, fabs(s - (i == j ? 1.0 : 0.0)));
+        }
+      double hn = 0.0;
+      for (double v : H) hn = std::max(hn, fabs(v));
+      for (int j = 0; j < std::min(n, 64); j++)
+        for (int i = j + 1; i < n; i++) {  // (Q^T H)[i, j] for i > j must vanish
+          double s = 0.0;
+          for (int k = 0; k < n; k++) s += hq[(size_t)k * n + i] * H[(size_t)k * n + j];
+          et = std::max(et, fabs(s) / hn);
+        }
+      printf("   max |Q^T Q - I| = %.2e   max |(Q^T H)_{i>j}| / max|H| = %.2e\n", eo, et);
+    }
     if (rep == 2) {
       static char buf[1 << 22];
       tk_ctx_profile_dump(ctx, buf, sizeof(buf));
