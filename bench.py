@@ -111,6 +111,13 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# DRAM traffic of the largest dgemm launch from one `ncu --set full` capture (the per-launch
+# average over all dgemm launches is not captured, so `traffic` stays null and the capture is
+# quoted beside it): profiles/r01/ncu_dgemm_formW.txt
+DGEMM_TRAFFIC = {"launch": "bond1.form_W (786432 x 640 x 896)", "dram_bytes": 9.65e9,
+                 "algorithmic_bytes": 9.67e9, "source": "profiles/r01/ncu_dgemm_formW.txt"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -316,6 +323,7 @@ def run_ours(args, cfg, op, x):
             ach = fl / cnt / (avg_ms * 1e-3) / 1e12
             roofline = {"kernel": cat, "bound": "tensor", "achieved": ach, "peak": fp64_peak,
                         "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                        "traffic_capture": DGEMM_TRAFFIC,
                         "peak_source": f"bf16 {peak_kind} {peaks['bf16_tflops']} x 45/2250 (fp64 DMMA nominal ratio)",
                         "launches": cnt, "avg_ms": avg_ms, "share_of_step": ms / total_ms}
         elif by > 0:
