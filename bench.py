@@ -257,9 +257,8 @@ def run_ours(args, cfg, op, x):
         flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
     def step():
-        y = ttk.tt_apply_op(gop, xg, out=ycap)
-        ttk.tt_round(y, cfg.tol, cfg.rmax, ctx)
-        return y
+        # the fused entry point: apply + round in one call (tk_apply_round)
+        return ttk.tt_apply_round(gop, xg, cfg.tol, cfg.rmax, out=ycap)
 
     for _ in range(args.warmup):
         step()
@@ -356,8 +355,7 @@ def run_ours(args, cfg, op, x):
             e0.record(stream)
             for buf_, src in zip((xe.b1, xe.b2, xe.b3), pinned):
                 buf_[: src.numel()].copy_(src.reshape(-1), non_blocking=True)
-            ye = ttk.tt_apply_op(gop, xe, out=ycap)
-            ttk.tt_round(ye, cfg.tol, cfg.rmax, ctx)
+            ye = ttk.tt_apply_round(gop, xe, cfg.tol, cfg.rmax, out=ycap)
             d2h = 0
             for o, c in zip(outs, (ye.U1, ye.U2, ye.U3)):
                 o[: c.numel()].copy_(c.reshape(-1), non_blocking=True)

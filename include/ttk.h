@@ -112,6 +112,15 @@ int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y);
 int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
              double* sigma2_out, double* discarded_out, double* norm_out);
 
+/* y = T_eps(A x): tk_apply_op followed by tk_round on y, fused: the block
+ * diagonal middle core of A x is never written densely — its T diagonal blocks G_k x_2 U2 stay
+ * in scratch and the right-to-left step U2 x_3 L3 runs block by block (T-fold fewer flops).
+ * Same contract, outputs and results as the two calls in sequence; y needs cap1 >= T*x.r1,
+ * cap2 >= T*x.r2 and holds the rounded TT on return.  BLOCKS the host. */
+int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
+                   int64_t rmax, double* sigma1_out, double* sigma2_out, double* discarded_out,
+                   double* norm_out);
+
 /* <x, y>_F contracted core by core (Alg. 3 line 7):
  * W1 = X1^T Y1, W2 = sum_i X2(:,i,:)^T W1 Y2(:,i,:), <x,y> = sum(W2 .* (X3 Y3^T)).
  * out_dev: DEVICE pointer to one double.  Asynchronous. */

@@ -5,4 +5,4 @@ cycle — all in libttk.so (hand-written CUDA, C ABI in include/ttk.h).  This pa
 thin Python binding; it never imports the CPU oracle and has no CPU fallback.
 """
 from .ttk import (TT, Context, Operator, RoundInfo, TkError, default_context, gmres_cycle,  # noqa: F401
-                  lib, tt_apply_op, tt_axpby, tt_dot, tt_norm, tt_round)
+                  lib, tt_apply_op, tt_apply_round, tt_axpby, tt_dot, tt_norm, tt_round)

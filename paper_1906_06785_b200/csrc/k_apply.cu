@@ -154,14 +154,17 @@ __global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm
 //   Y2[k r1 + a, i, k r2 + b] = sum_j G_k[i, j] U2[a, j, b]
 // blockIdx.y = row k r1 + a; threads over (i, b), b fastest (coalesced U2 reads and Y2 writes,
 // G_k[i, :] broadcast within a warp when r2 >= 32).
+// compact != 0: write the blocks densely packed, B[k r1 + a, i, b] (T r1 x n_xi x r2), for the
+// fused apply+round (the zero off-diagonal blocks are never materialised).
 __global__ void stoch_apply_k(int T, int r1, int n_xi, int r2, const double* __restrict__ G,
-                              const double* __restrict__ U2, double* __restrict__ Y2) {
+                              const double* __restrict__ U2, double* __restrict__ Y2,
+                              int compact) {
   const int row = blockIdx.y;
   const int k = row / r1, a = row % r1;
-  const int64_t R2 = (int64_t)T * r2;
+  const int64_t R2 = compact ? r2 : (int64_t)T * r2;
   const double* g = G + (int64_t)k * n_xi * n_xi;
   const double* u = U2 + (int64_t)a * n_xi * r2;
-  double* y = Y2 + (int64_t)row * n_xi * R2 + (int64_t)k * r2;
+  double* y = Y2 + (int64_t)row * n_xi * R2 + (compact ? 0 : (int64_t)k * r2);
   const int n = n_xi * r2;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int i = e / r2, b = e - i * r2;
@@ -229,10 +232,10 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
 }
 
 int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
-                          double* Y2) {
+                          double* Y2, bool compact) {
   const int64_t rows = (int64_t)op->T * r1;
   const int64_t total = rows * op->n_xi * op->T * r2;
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(Y2, 0, sizeof(double) * total, ctx->stream));
+  if (!compact) TK_CUDA_TRY(ctx, cudaMemsetAsync(Y2, 0, sizeof(double) * total, ctx->stream));
   const int n = (int)(op->n_xi * r2);
   const int bx = std::max(1, std::min((n + 255) / 256, 8));
   if (rows > 65535) {
@@ -240,7 +243,7 @@ int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const do
     return TK_EARG;
   }
   stoch_apply_k<<<dim3(bx, (unsigned)rows), 256, 0, ctx->stream>>>(op->T, r1, (int)op->n_xi, r2,
-                                                                    op->G, U2, Y2);
+                                                                    op->G, U2, Y2, compact ? 1 : 0);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }

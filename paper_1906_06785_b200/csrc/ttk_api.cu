@@ -291,6 +291,27 @@ static int check_tt(tk_ctx* ctx, const tk_tt* x, const char* who) {
 }
 
 // ============================================================================ apply
+// The space and time cores of y = A x: Y1 = [K_k U1]_k (SpMM), Y3 = [U3 T_k^T]_k (band).
+static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y) {
+  const int64_t R1 = op->T * x->r1, R2 = op->T * x->r2;
+  {
+    // algorithmic bytes: read U1 once, write Y1 once, read the CSR (12 B/nnz + rowptr)
+    double nnz = 0;
+    for (auto v : op->h_nnz) nnz += (double)v;
+    double bytes = 8.0 * x->n_x * x->r1 + 8.0 * x->n_x * R1 + 12.0 * nnz +
+                   4.0 * op->T * (x->n_x + 1);
+    int id = tk_prof_begin(ctx, "spmm_multi", 2.0 * nnz * x->r1, bytes);
+    TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
+    tk_prof_end(ctx, id);
+  }
+  {
+    int id = tk_prof_begin(ctx, "time_apply", 0.0, 8.0 * (R2 + x->r2) * x->n_t);
+    TK_TRY(tk_launch_time_apply(ctx, op, (int)x->r2, x->U3, y->U3));
+    tk_prof_end(ctx, id);
+  }
+  return TK_OK;
+}
+
 extern "C" int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y) {
   if (!ctx || !op) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_apply_op(x)"));
@@ -308,26 +329,12 @@ extern "C" int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* 
     ctx->err = "tk_apply_op: output capacity < (T r1, T r2)";
     return TK_ECAP;
   }
-  {
-    // algorithmic bytes: read U1 once, write Y1 once, read the CSR (12 B/nnz + rowptr)
-    double nnz = 0;
-    for (auto v : op->h_nnz) nnz += (double)v;
-    double bytes = 8.0 * x->n_x * x->r1 + 8.0 * x->n_x * R1 + 12.0 * nnz +
-                   4.0 * op->T * (x->n_x + 1);
-    int id = tk_prof_begin(ctx, "spmm_multi", 2.0 * nnz * x->r1, bytes);
-    TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
-    tk_prof_end(ctx, id);
-  }
+  TK_TRY(apply_space_time(ctx, op, x, y));
   {
     double bytes = 8.0 * (R1 * x->n_xi * R2 + x->r1 * x->n_xi * x->r2);
     int id = tk_prof_begin(ctx, "stoch_apply", 2.0 * op->T * x->r1 * x->n_xi * x->n_xi * x->r2,
                            bytes);
     TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, y->U2));
-    tk_prof_end(ctx, id);
-  }
-  {
-    int id = tk_prof_begin(ctx, "time_apply", 0.0, 8.0 * (R2 + x->r2) * x->n_t);
-    TK_TRY(tk_launch_time_apply(ctx, op, (int)x->r2, x->U3, y->U3));
     tk_prof_end(ctx, id);
   }
   y->r1 = R1;
@@ -703,8 +710,11 @@ int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
 
 }  // namespace
 
+// y2blk (nullable): the middle core is block diagonal with nb = R1 / rb1 diagonal blocks of
+// size rb1 x n_xi x rb2, packed in y2blk (the fused apply+round); x->U2 is then output only.
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
-                      double* sigma2_out, double* discarded_out, double* norm_out);
+                      double* sigma2_out, double* discarded_out, double* norm_out,
+                      const double* y2blk = nullptr, int64_t rb1 = 0, int64_t rb2 = 0);
 
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
@@ -714,8 +724,47 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
   return st;
 }
 
+extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
+                              int64_t rmax, double* sigma1_out, double* sigma2_out,
+                              double* discarded_out, double* norm_out) {
+  if (!ctx || !op) return TK_EARG;
+  TK_TRY(check_tt(ctx, x, "tk_apply_round(x)"));
+  if (!y || !y->U1 || !y->U2 || !y->U3) {
+    ctx->err = "tk_apply_round: null output TT";
+    return TK_EARG;
+  }
+  if (x->n_x != op->n_x || x->n_xi != op->n_xi || x->n_t != op->n_t || y->n_x != op->n_x ||
+      y->n_xi != op->n_xi || y->n_t != op->n_t) {
+    ctx->err = "tk_apply_round: mode sizes differ from the operator's";
+    return TK_ESHAPE;
+  }
+  const int64_t R1 = op->T * x->r1, R2 = op->T * x->r2;
+  if (R1 > y->cap1 || R2 > y->cap2) {
+    ctx->err = "tk_apply_round: output capacity < (T r1, T r2)";
+    return TK_ECAP;
+  }
+  TK_TRY(apply_space_time(ctx, op, x, y));
+  DevBuf blk;
+  TK_TRY(blk.get(ctx, R1 * x->n_xi * x->r2));
+  {
+    double bytes = 8.0 * (R1 * x->n_xi * x->r2 + x->r1 * x->n_xi * x->r2);
+    int id = tk_prof_begin(ctx, "stoch_apply", 2.0 * op->T * x->r1 * x->n_xi * x->n_xi * x->r2,
+                           bytes);
+    TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, blk.p, true));
+    tk_prof_end(ctx, id);
+  }
+  y->r1 = R1;
+  y->r2 = R2;
+  const int st = round_impl(ctx, y, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out,
+                            blk.p, x->r1, x->r2);
+  blk.release();
+  pool_settle(ctx);
+  return st;
+}
+
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
-                      double* sigma2_out, double* discarded_out, double* norm_out) {
+                      double* sigma2_out, double* discarded_out, double* norm_out,
+                      const double* y2blk, int64_t rb1, int64_t rb2) {
   TK_TRY(check_tt(ctx, x, "tk_round"));
   if (!(tol >= 0.0) || !std::isfinite(tol)) {
     ctx->err = "tk_round: tol must be finite and >= 0";
@@ -736,7 +785,15 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   DevBuf Y2p;
   TagScope tagr(ctx, "round.small");
   TK_TRY(Y2p.get(ctx, R1 * n_xi * k3));
-  TK_TRY(tk_dgemm(ctx, false, false, R1 * n_xi, k3, R2, 1.0, x->U2, R2, L3, k3, 0.0, Y2p.p, k3));
+  if (y2blk) {
+    // block diagonal middle core: row block b of Y2p = B_b (rb1 n_xi x rb2) L3[b rb2 : (b+1) rb2, :]
+    // (T-fold fewer flops than the dense product with its zero blocks)
+    for (int64_t b = 0; b < R1 / rb1; b++)
+      TK_TRY(tk_dgemm(ctx, false, false, rb1 * n_xi, k3, rb2, 1.0, y2blk + b * rb1 * n_xi * rb2,
+                      rb2, L3 + b * rb2 * k3, k3, 0.0, Y2p.p + b * rb1 * n_xi * k3, k3));
+  } else {
+    TK_TRY(tk_dgemm(ctx, false, false, R1 * n_xi, k3, R2, 1.0, x->U2, R2, L3, k3, 0.0, Y2p.p, k3));
+  }
   // ---- step C: Y2p as R1 x (n_xi k3) = L2 Q2
   const int64_t N2 = n_xi * k3;
   DevBuf L2b, Q2c;
@@ -997,8 +1054,7 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     const tk_tt& vk = V[k]->t;
     auto x = std::make_unique<OwnedTT>();
     TK_TRY(x->make(ctx, n_x, n_xi, n_t, T * vk.r1, T * vk.r2));
-    TK_TRY(tk_apply_op(ctx, op, &vk, &x->t));
-    TK_TRY(tk_round(ctx, &x->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_apply_round(ctx, op, &vk, &x->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
     TK_TRY(tk_norm(ctx, &x->t, d_nav));
     for (int i = 0; i <= k; i++) {
       TK_TRY(tk_dot(ctx, &x->t, &V[i]->t, d_h + i));

@@ -183,7 +183,7 @@ int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X
 // Apply kernels
 int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1);
 int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
-                          double* Y2);
+                          double* Y2, bool compact = false);
 int tk_launch_time_apply(tk_ctx* ctx, const tk_op* op, int r2, const double* U3, double* Y3);
 
 // small helpers (k_small.cu)

@@ -20,7 +20,8 @@ _CODES = {TK_ESHAPE: "TK_ESHAPE", TK_ECAP: "TK_ECAP", TK_EARG: "TK_EARG",
 
 EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "tk_ctx_launch_count",
             "tk_ctx_profile", "tk_ctx_profile_dump",
-            "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round", "tk_dot",
+            "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round",
+            "tk_apply_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle"]
 
 
@@ -65,6 +66,7 @@ def lib():
     DP = ctypes.POINTER(D)
     L.tk_apply_op.argtypes = [P, P, TTP, TTP]
     L.tk_round.argtypes = [P, TTP, D, I64, DP, DP, DP, DP]
+    L.tk_apply_round.argtypes = [P, P, TTP, TTP, D, I64, DP, DP, DP, DP]
     L.tk_dot.argtypes = [P, TTP, TTP, P]
     L.tk_norm.argtypes = [P, TTP, P]
     L.tk_axpby.argtypes = [P, P, TTP, P, TTP, TTP]
@@ -258,6 +260,32 @@ def tt_round(x: TT, tol: float, rmax: int = 0, ctx: Context | None = None,
         return x, RoundInfo((x.r1, x.r2), np.array(s1[:]), np.array(s2[:]), (disc[0], disc[1]),
                             nrm.value)
     return x
+
+
+def tt_apply_round(op: "Operator", x: TT, tol: float, rmax: int = 0, out: TT | None = None,
+                   want_info: bool = False):
+    """y = T_tol(A x) fused (tk_apply_round): the block-diagonal middle core of A x is never
+    written densely.  Same results as tt_round(tt_apply_op(op, x), tol, rmax)."""
+    ctx = op.ctx
+    T = op.T
+    y = out if out is not None else TT(x.n_x, x.n_xi, x.n_t, T * x.r1, T * x.r2)
+    xs, ys = x.struct(), y.struct()
+    D = ctypes.c_double
+    if want_info:
+        s1 = (D * max(T * x.r1, 1))()
+        s2 = (D * max(T * x.r2, 1))()
+        disc = (D * 2)()
+        nrm = D()
+        ctx.check(lib().tk_apply_round(ctx._h, op._h, ctypes.byref(xs), ctypes.byref(ys),
+                                       float(tol), int(rmax), s1, s2, disc, ctypes.byref(nrm)))
+    else:
+        ctx.check(lib().tk_apply_round(ctx._h, op._h, ctypes.byref(xs), ctypes.byref(ys),
+                                       float(tol), int(rmax), None, None, None, None))
+    y._update(ys)
+    if want_info:
+        return y, RoundInfo((y.r1, y.r2), np.array(s1[:]), np.array(s2[:]), (disc[0], disc[1]),
+                            nrm.value)
+    return y
 
 
 def tt_dot(x: TT, y: TT, ctx: Context | None = None, out: torch.Tensor | None = None):

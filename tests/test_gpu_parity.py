@@ -112,10 +112,15 @@ def test_apply_capacity_and_shape_errors(ctx):
 
 
 # ----------------------------------------------------------------------------- round
-def check_round(y_cores, tol, rmax, ctx, dense=True):
+def check_round(y_cores, tol, rmax, ctx, dense=True, gpu=None):
+    """Oracle round of y_cores vs the GPU: tk_round on the same cores, or gpu() -> (TT, info)
+    (the fused tk_apply_round on the operator and input that produced y_cores)."""
     o, info = otT.round_tt(y_cores, tol, rmax, return_info=True)
-    g = ttk.TT.from_cores(*y_cores)
-    g, ginfo = ttk.tt_round(g, tol, rmax, ctx, want_info=True)
+    if gpu is None:
+        g = ttk.TT.from_cores(*y_cores)
+        g, ginfo = ttk.tt_round(g, tol, rmax, ctx, want_info=True)
+    else:
+        g, ginfo = gpu()
     gc = g.cores_numpy()
     assert ranks_excused(info["sigma1"], info["delta"], ginfo.ranks[0], info["ranks"][0], rmax)
     # kept singular values to 1e-10 s_1 and the discarded tail norms to 1e-10 ||x|| (DESIGN.md
@@ -211,6 +216,49 @@ def test_round_parity_c3(ctx):
     for a, b in zip(yg.cores_numpy(), y):
         assert rel(a, b) <= 1e-13
     check_round(y, cfg.tol, cfg.rmax, ctx, dense=False)
+
+
+# ----------------------------------------------------------------------------- fused apply+round
+@pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c1", 1e-3), ("c2", None)])
+def test_apply_round_parity(name, tol, ctx):
+    """tk_apply_round (block-diagonal middle core never materialised) vs oracle apply + round."""
+    cfg = CONFIGS[name]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    tol = cfg.tol if tol is None else tol
+    y = otT.apply_op(op, x)
+    g = gpu_op(op, ctx)
+    check_round(y, tol, cfg.rmax, ctx, dense=(name == "c1"),
+                gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), tol, cfg.rmax,
+                                               want_info=True))
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_apply_round_parity_random(seed, ctx):
+    """Random operators (T terms, ragged CSR, banded T_k) and odd ranks through the fused path."""
+    rng = np.random.default_rng(seed)
+    T = int(rng.integers(1, 5))
+    n_x, n_xi, n_t = int(rng.integers(20, 90)), int(rng.integers(2, 9)), int(rng.integers(3, 17))
+    r1, r2 = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+    op = random_operator(rng, n_x, n_xi, n_t, T)
+    x = random_tt(rng, n_x, n_xi, n_t, r1, r2)
+    y = otT.apply_op(op, x)
+    g = gpu_op(op, ctx)
+    tol = float(10.0 ** rng.uniform(-10, -2))
+    check_round(y, tol, 0, ctx, dense=True,
+                gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), tol, 0, want_info=True))
+
+
+@pytest.mark.slow
+def test_apply_round_parity_c3(ctx):
+    cfg = CONFIGS["c3"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    y = otT.apply_op(op, x)
+    g = gpu_op(op, ctx)
+    check_round(y, cfg.tol, cfg.rmax, ctx, dense=False,
+                gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), cfg.tol, cfg.rmax,
+                                               want_info=True))
 
 
 # ----------------------------------------------------------------------------- GMRES c5
