@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -192,6 +193,146 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
   }
 }
 
+// Register variant for n <= PT: each thread keeps its own column's panel values in
+// registers (Rp), so a step reads only the pivot column's values from shared memory (broadcast)
+// — the shared-memory variant above streams both operands of every row dot product through
+// shared memory.  The step loop is unrolled (NB compile-time) so Rp is statically indexed.
+template <int MAXC, int NB>
+__global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot,
+                                                        const double* __restrict__ Hw,
+                                                        double* __restrict__ Ro,
+                                                        int* __restrict__ piv,
+                                                        int* __restrict__ state,
+                                                        const double* __restrict__ tol_dev,
+                                                        double* __restrict__ rem_out) {
+  extern __shared__ double sR[];  // NB x n
+  __shared__ double s_val[PT / 32];
+  __shared__ int s_idx[PT / 32];
+  __shared__ int s_p;
+  __shared__ double s_dmax;
+  if (state[1]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = tol_dev[0];
+  int* retired = state + 2;
+  double d[MAXC], Rp[MAXC][NB];
+  bool live[MAXC];
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int m = 0; m < MAXC; m++) {
+    const int c = tid + m * PT;
+    live[m] = c < n && !retired[c];
+    d[m] = live[m] ? Hw[(int64_t)c * n + c] : -INFINITY;
+    if (d[m] > bv) {
+      bv = d[m];
+      bi = c;
+    }
+#pragma unroll
+    for (int t = 0; t < NB; t++) Rp[m][t] = 0.0;
+  }
+  if (pivot) {
+    block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);
+  } else {
+#pragma unroll
+    for (int m = 0; m < MAXC; m++)
+      if (tid + m * PT == j0) {
+        s_p = j0;
+        s_dmax = d[m];
+      }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < NB; s++) {
+    const int j = j0 + s;
+    if (j >= n) break;
+    const int p = s_p;
+    const double dmax = s_dmax;
+    if (!(dmax > tol) || p >= n) {  // uniform: rank reached (or nothing left / non-finite)
+      if (tid == 0) {
+        state[0] = j;
+        state[1] = 1;
+      }
+      if (rem_out) {
+        double t = 0.0;
+#pragma unroll
+        for (int m = 0; m < MAXC; m++)
+          if (live[m]) t += fmax(d[m], 0.0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        __syncthreads();
+        if (lane == 0) s_val[warp] = t;
+        __syncthreads();
+        if (tid == 0) {
+          double tt = 0.0;
+          for (int w = 0; w < (int)(blockDim.x >> 5); w++) tt += s_val[w];
+          rem_out[0] = tt;
+        }
+      }
+      return;
+    }
+    const double r = sqrt(dmax), rinv = 1.0 / r;
+    double pc[NB];
+#pragma unroll
+    for (int t = 0; t < NB; t++) pc[t] = t < s ? sR[t * n + p] : 0.0;
+    const double* hrow = Hw + (int64_t)p * n;
+    double* orow = Ro + (int64_t)j * n;
+    bv = -INFINITY;
+    bi = 0x7fffffff;
+#pragma unroll
+    for (int m = 0; m < MAXC; m++) {
+      const int c = tid + m * PT;
+      if (c >= n) continue;
+      double out = 0.0;
+      if (c == p) {
+        out = r;
+        live[m] = false;
+        d[m] = -INFINITY;
+        retired[c] = 1;
+      } else if (live[m]) {
+        double v0 = hrow[c], v1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < NB; t++) {
+          if (t < s) {
+            if (t & 1)
+              v1 = fma(-pc[t], Rp[m][t], v1);
+            else
+              v0 = fma(-pc[t], Rp[m][t], v0);
+          }
+        }
+        out = (v0 + v1) * rinv;
+        d[m] = fma(-out, out, d[m]);
+        if (d[m] > bv) {
+          bv = d[m];
+          bi = c;
+        }
+      }
+      Rp[m][s] = out;
+      orow[c] = out;
+      sR[s * n + c] = out;
+    }
+    if (tid == 0) {
+      piv[j] = p;
+      state[0] = j + 1;
+    }
+    if (pivot) {
+      block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);  // also orders this step's writes
+    } else {
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < MAXC; m++)
+        if (tid + m * PT == j + 1) {
+          s_p = j + 1;
+          s_dmax = d[m];
+        }
+      if (j + 1 >= n && tid == 0) {
+        s_p = n;
+        s_dmax = -INFINITY;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void max_diag_tol_k(int n, const double* __restrict__ H, double rel,
                                const double* __restrict__ abs_dev, double* __restrict__ tol) {
   __shared__ double red[256];
@@ -296,6 +437,33 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   if (rem_out) TK_CUDA_TRY(ctx, cudaMemsetAsync(rem_out, 0, sizeof(double), ctx->stream));
   max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
   TK_LAUNCH_CHECK(ctx);
+  // register variant (n <= 2 PT): nb = 16 panel rows in registers, broadcast reads of the pivot
+  // column from shared memory
+  static const bool no_reg = getenv("TTK_PCHOL_SMEM") != nullptr;
+  if (!no_reg && n <= PT) {
+    // one column per thread: 32 panel rows fit in registers (for two columns per thread only
+    // 16 do, and the doubled number of rank-nb updates then costs more than it saves)
+    constexpr int NBR = 32;
+    const size_t rsmem = (size_t)NBR * n * sizeof(double);
+    static size_t rattr = 0;
+    if (rsmem > 48 * 1024 && rattr < rsmem) {
+      cudaFuncSetAttribute(pchol_panel_reg_k<1, NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)rsmem);
+      rattr = rsmem;
+    }
+    for (int j0 = 0; j0 < n; j0 += NBR) {
+      const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
+      pchol_panel_reg_k<1, NBR><<<1, PT, rsmem, ctx->stream>>>(n, j0, pivot ? 1 : 0, Hw.p, Ro, piv,
+                                                              state, tol.p, rem_out);
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
+      const int jb = std::min(NBR, n - j0);
+      if (j0 + jb < n)
+        TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
+                        Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true));
+    }
+    return TK_OK;
+  }
   // panel width: the panel rows of Ro (nb x n) and the diagonal stay in shared memory
   const int nb = (int)std::max<int64_t>(4, std::min<int64_t>(32, (200 * 1024 / 8) / n - 1));
   const size_t smem = ((size_t)nb + 1) * n * sizeof(double);

@@ -29,6 +29,38 @@ static void spd(int n, std::vector<double>& H, double span) {
 int main(int argc, char** argv) {
   int n = argc > 1 ? atoi(argv[1]) : 896;
   const char* what = argc > 2 ? argv[2] : "qr";
+  if (!strcmp(what, "gemm") || !strcmp(what, "gram")) {
+    // c4 bond-1 shapes: W = Y P (786432 x 640 x 896) and G_W = W^T W (sym)
+    const int64_t M = 786432, K = 896, N = 640;
+    tk_ctx* c2;
+    cudaStream_t st2;
+    cudaStreamCreate(&st2);
+    tk_ctx_create(&c2, st2);
+    double *Y, *P, *W, *G;
+    cudaMalloc(&Y, sizeof(double) * M * K);
+    cudaMalloc(&P, sizeof(double) * K * N);
+    cudaMalloc(&W, sizeof(double) * M * N);
+    cudaMalloc(&G, sizeof(double) * N * N);
+    cudaMemset(Y, 0, sizeof(double) * M * K);
+    cudaMemset(P, 0, sizeof(double) * K * N);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int rep = 0; rep < 3; rep++) {
+      cudaEventRecord(e0, st2);
+      if (!strcmp(what, "gemm"))
+        tk_dgemm(c2, false, false, M, N, K, 1.0, Y, K, P, N, 0.0, W, N);
+      else
+        tk_dgemm(c2, true, false, N, N, M, 1.0, W, N, W, N, 0.0, G, N, true);
+      cudaEventRecord(e1, st2);
+      cudaStreamSynchronize(st2);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double fl = !strcmp(what, "gemm") ? 2.0 * M * N * K : (double)N * (N + 1) * M;
+      printf("%s %.3f ms  %.2f TF/s\n", what, ms, fl / ms / 1e9);
+    }
+    return 0;
+  }
   tk_ctx* ctx;
   cudaStream_t st;
   cudaStreamCreate(&st);
@@ -69,6 +101,23 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     printf("%s n=%d rc=%d total %.3f ms\n", what, n, rc, ms);
+    if (rep == 2 && !strcmp(what, "pchol")) {
+      // reconstruction H ~ Ro^T Ro over the first k rows, on the host
+      std::vector<double> ro((size_t)n * n);
+      int st[2];
+      cudaMemcpy(ro.data(), dR, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(st, state, sizeof(st), cudaMemcpyDeviceToHost);
+      const int k = st[0];
+      double hn = 0.0, e = 0.0;
+      for (double v : H) hn = std::max(hn, fabs(v));
+      for (int i = 0; i < n; i++)
+        for (int j = 0; j <= i; j++) {
+          double s2 = 0.0;
+          for (int t = 0; t < k; t++) s2 += ro[(size_t)t * n + i] * ro[(size_t)t * n + j];
+          e = std::max(e, fabs(s2 - H[(size_t)i * n + j]));
+        }
+      printf("   rank %d  max |H - Ro^T Ro| / max|H| = %.2e\n", k, e / hn);
+    }
     if (rep == 2 && !strcmp(what, "qr")) {
       // orthogonality of Q and the triangularity of Q^T H (first 64 columns), on the host
       std::vector<double> hq((size_t)n * n);
