@@ -497,8 +497,8 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
 int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx) {
   if (k <= 0) return TK_OK;
   TagScope tag(ctx, "tri_inv");
-  for (int64_t i = 0; i < k; i++)
-    TK_CUDA_TRY(ctx, cudaMemsetAsync(X + i * ldx, 0, sizeof(double) * k, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemset2DAsync(X, sizeof(double) * ldx, 0, sizeof(double) * k, k,
+                                     ctx->stream));
   const int nbk = (k + TS_H - 1) / TS_H;
   for (int b = nbk - 1; b >= 0; b--) {
     const int i0 = b * TS_H, i1 = std::min(k, i0 + TS_H), h = i1 - i0;

@@ -273,8 +273,8 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
       ctx->err = "tk_dgemm: K == 0 with beta != 0 is not supported";
       return TK_EARG;
     }
-    for (int64_t m = 0; m < M; m++)
-      TK_CUDA_TRY(ctx, cudaMemsetAsync(C + m * ldc, 0, N * sizeof(double), ctx->stream));
+    TK_CUDA_TRY(ctx, cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * N, M,
+                                       ctx->stream));
     return TK_OK;
   }
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;

@@ -853,10 +853,12 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     }
   }
   // join: everything on s1 / s2 before s0 continues (and before the scratch buffers are freed)
+  const int jid = tk_prof_begin(ctx, "qr_join", 0.0, 0.0);  // s0 idle time waiting for s1 / s2
   TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s1));
   TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
   TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s2));
   TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
+  tk_prof_end(ctx, jid);
   if (dbg) {
     std::vector<unsigned long long> h(12 * (size_t)np);
     TK_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), dbgb.p, 8 * h.size(), cudaMemcpyDeviceToHost, s0));
