@@ -359,3 +359,30 @@ int tk_col_norms(tk_ctx* ctx, int64_t rows, int64_t cols, const double* A, int64
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
+
+namespace {
+// out[b][q][p][w] = in[b][p][q][w]  (w contiguous)
+__global__ void swap_mid_k(int64_t nb, int64_t np, int64_t nq, int64_t nw,
+                           const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t total = nb * np * nq * nw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = e % nw;
+    int64_t t = e / nw;
+    const int64_t q = t % nq;
+    t /= nq;
+    const int64_t p = t % np;
+    const int64_t b = t / np;
+    out[((b * nq + q) * np + p) * nw + w] = in[e];
+  }
+}
+}  // namespace
+
+int tk_swap_mid(tk_ctx* ctx, int64_t nb, int64_t np, int64_t nq, int64_t nw, const double* in,
+                double* out) {
+  const int64_t total = nb * np * nq * nw;
+  if (total <= 0) return TK_OK;
+  swap_mid_k<<<grid_for(ctx, total), 256, 0, ctx->stream>>>(nb, np, nq, nw, in, out);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

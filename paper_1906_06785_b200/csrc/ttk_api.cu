@@ -747,11 +747,17 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   DevBuf blk;
   TK_TRY(blk.get(ctx, R1 * x->n_xi * x->r2));
   {
-    double bytes = 8.0 * (R1 * x->n_xi * x->r2 + x->r1 * x->n_xi * x->r2);
-    int id = tk_prof_begin(ctx, "stoch_apply", 2.0 * op->T * x->r1 * x->n_xi * x->n_xi * x->r2,
-                           bytes);
-    TK_TRY(tk_launch_stoch_apply(ctx, op, (int)x->r1, (int)x->r2, x->U2, blk.p, true));
-    tk_prof_end(ctx, id);
+    // the T diagonal blocks G_k x_2 U2 as ONE DMMA GEMM: [G_0; ...; G_{T-1}] (T n_xi x n_xi)
+    // times U2 permuted to (n_xi) x (r1 r2), then (k, i, a, b) -> (k, a, i, b)
+    TagScope t(ctx, "stoch_apply");
+    const int64_t nxi = x->n_xi, r1 = x->r1, r2 = x->r2;
+    DevBuf U2p, C;
+    TK_TRY(U2p.get(ctx, nxi * r1 * r2));
+    TK_TRY(tk_swap_mid(ctx, 1, r1, nxi, r2, x->U2, U2p.p));
+    TK_TRY(C.get(ctx, op->T * nxi * r1 * r2));
+    TK_TRY(tk_dgemm(ctx, false, false, op->T * nxi, r1 * r2, nxi, 1.0, op->G, nxi, U2p.p, r1 * r2,
+                    0.0, C.p, r1 * r2));
+    TK_TRY(tk_swap_mid(ctx, op->T, nxi, r1, r2, C.p, blk.p));
   }
   y->r1 = R1;
   y->r2 = R2;

@@ -213,6 +213,9 @@ int tk_neg_scalar(tk_ctx* ctx, const double* src, double* dst);
 int tk_transpose(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
                  double* dst, int64_t ldd);
 int tk_symmetrize(tk_ctx* ctx, int64_t n, double* A);
+// out[b][q][p][w] = in[b][p][q][w] (swap of the two middle indices, w contiguous).
+int tk_swap_mid(tk_ctx* ctx, int64_t nb, int64_t np, int64_t nq, int64_t nw, const double* in,
+                double* out);
 // Euclidean norms of the columns of the rows x cols matrix A (ld lda) into out (device).
 int tk_col_norms(tk_ctx* ctx, int64_t rows, int64_t cols, const double* A, int64_t lda,
                  double* out);
