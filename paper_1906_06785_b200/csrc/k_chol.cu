@@ -352,38 +352,39 @@ __global__ void max_diag_tol_k(int n, const double* __restrict__ H, double rel,
   }
 }
 
-// X[i0:i0+h, c0:c0+w] <- Rd^{-1} X[i0:i0+h, c0:c0+w] for the h x h (h <= 64) upper triangular
-// diagonal block Rd = R[i0:i0+h, i0:i0+h]: back substitution, one thread per column (the block
-// of R and the columns in shared memory).
-constexpr int TS_H = 64, TS_W = 128;
-__global__ void __launch_bounds__(TS_W) trsm_diag_k(int h, int i0, int ncols, int c0,
-                                                    const double* __restrict__ R, int64_t ldr,
-                                                    double* __restrict__ X, int64_t ldx) {
-  extern __shared__ double tsm[];
-  double(*Rs)[TS_H] = reinterpret_cast<double(*)[TS_H]>(tsm);            // broadcast reads
-  double(*xs)[TS_W] = reinterpret_cast<double(*)[TS_W]>(tsm + TS_H * TS_H);
-  const int tid = threadIdx.x;
-  for (int e = tid; e < h * h; e += blockDim.x) {
-    const int i = e / h, l = e % h;
-    Rs[i][l] = R[(int64_t)(i0 + i) * ldr + i0 + l];
-  }
-  const int c = c0 + blockIdx.x * TS_W + tid;
-  const bool live = c < c0 + ncols;
-  for (int i = 0; i < h; i++) xs[i][tid] = live ? X[(int64_t)(i0 + i) * ldx + c] : 0.0;
-  __syncthreads();
-  for (int i = h - 1; i >= 0; i--) {
-    double s = xs[i][tid];
-    for (int l = i + 1; l < h; l++) s = fma(-Rs[i][l], xs[l][tid], s);
-    xs[i][tid] = s / Rs[i][i];
-  }
-  if (live)
-    for (int i = 0; i < h; i++) X[(int64_t)(i0 + i) * ldx + c] = xs[i][tid];
-}
+constexpr int TS_H = 64;
 
-__global__ void eye_block_k(int h, int i0, double* __restrict__ X, int64_t ldx) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < h * h; e += gridDim.x * blockDim.x) {
+// Inverse of every 64 x 64 (or smaller, last) diagonal block of the upper triangular R,
+// written into the matching diagonal blocks of X: one CTA per block, thread c computes column
+// c of the block inverse by back substitution (block of R and the columns in shared memory).
+__global__ void __launch_bounds__(TS_H) diag_inv_k(int k, const double* __restrict__ R,
+                                                   int64_t ldr, double* __restrict__ X,
+                                                   int64_t ldx) {
+  extern __shared__ double dsm[];
+  double(*Rs)[TS_H + 1] = reinterpret_cast<double(*)[TS_H + 1]>(dsm);
+  double(*xs)[TS_H + 1] = reinterpret_cast<double(*)[TS_H + 1]>(dsm + TS_H * (TS_H + 1));
+  const int i0 = blockIdx.x * TS_H, h = min(TS_H, k - i0), c = threadIdx.x;
+  for (int e = c; e < h * h; e += blockDim.x) {
     const int i = e / h, l = e % h;
-    X[(int64_t)(i0 + i) * ldx + i0 + l] = (i == l) ? 1.0 : 0.0;
+    Rs[i][l] = (l >= i) ? R[(int64_t)(i0 + i) * ldr + i0 + l] : 0.0;
+  }
+  __syncthreads();
+  if (c < h) {
+    for (int i = h - 1; i >= 0; i--) {
+      double s = (i == c) ? 1.0 : 0.0;
+      if (i < c) {
+        double s0 = 0.0, s1 = 0.0;
+        int l = i + 1;
+        for (; l + 1 <= c; l += 2) {
+          s0 = fma(Rs[i][l], xs[l][c], s0);
+          s1 = fma(Rs[i][l + 1], xs[l + 1][c], s1);
+        }
+        if (l <= c) s0 = fma(Rs[i][l], xs[l][c], s0);
+        s -= s0 + s1;
+      }
+      xs[i][c] = (i <= c) ? s / Rs[i][i] : 0.0;
+    }
+    for (int i = 0; i < h; i++) X[(int64_t)(i0 + i) * ldx + i0 + c] = xs[i][c];
   }
 }
 
@@ -494,31 +495,37 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
 // X = R^{-1} (k x k upper triangular), blocked back substitution from the bottom block row:
 //   X[I, J>I] = -R[I, I]^{-1} R[I, >I] X[>I, J],   X[I, I] = R[I, I]^{-1}
 // (one DMMA GEMM and one diagonal-block solve per 64-row block).
+// X = R^{-1} (k x k upper triangular), blocked from the bottom block row:
+//   X[I, I] = D_I = R[I, I]^{-1}  (all 64 x 64 diagonal blocks at once, diag_inv_k)
+//   X[I, >I] = -D_I (R[I, >I] X[>I, >I])   (two DMMA GEMMs per block row)
 int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx) {
   if (k <= 0) return TK_OK;
   TagScope tag(ctx, "tri_inv");
   TK_CUDA_TRY(ctx, cudaMemset2DAsync(X, sizeof(double) * ldx, 0, sizeof(double) * k, k,
                                      ctx->stream));
   const int nbk = (k + TS_H - 1) / TS_H;
-  for (int b = nbk - 1; b >= 0; b--) {
-    const int i0 = b * TS_H, i1 = std::min(k, i0 + TS_H), h = i1 - i0;
-    eye_block_k<<<(h * h + 255) / 256, 256, 0, ctx->stream>>>(h, i0, X, ldx);
-    TK_LAUNCH_CHECK(ctx);
-    if (i1 < k) {
-      // X[i0:i1, i1:k] = -R[i0:i1, i1:k] X[i1:k, i1:k]
-      TK_TRY(tk_dgemm(ctx, false, false, h, k - i1, k - i1, -1.0, R + (int64_t)i0 * ldr + i1, ldr,
-                      X + (int64_t)i1 * ldx + i1, ldx, 0.0, X + (int64_t)i0 * ldx + i1, ldx));
-    }
-    const int ncols = k - i0;
-    const size_t smem = sizeof(double) * (TS_H * TS_H + TS_H * TS_W);
+  {
+    const int pid = tk_prof_begin(ctx, "tri_inv_diag", 0.0, 0.0);
+    const size_t dsm = sizeof(double) * 2 * TS_H * (TS_H + 1);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(trsm_diag_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(diag_inv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
       attr = true;
     }
-    trsm_diag_k<<<(ncols + TS_W - 1) / TS_W, TS_W, smem, ctx->stream>>>(h, i0, ncols, i0, R, ldr,
-                                                                         X, ldx);
+    diag_inv_k<<<nbk, TS_H, dsm, ctx->stream>>>(k, R, ldr, X, ldx);
     TK_LAUNCH_CHECK(ctx);
+    tk_prof_end(ctx, pid);
+  }
+  DevBuf T;
+  if (nbk > 1) TK_TRY(T.get(ctx, (size_t)TS_H * k));
+  for (int b = nbk - 2; b >= 0; b--) {
+    const int i0 = b * TS_H, i1 = i0 + TS_H, h = TS_H, w = k - i1;
+    // T = R[i0:i1, i1:k] X[i1:k, i1:k]   (X block upper triangular)
+    TK_TRY(tk_dgemm(ctx, false, false, h, w, w, 1.0, R + (int64_t)i0 * ldr + i1, ldr,
+                    X + (int64_t)i1 * ldx + i1, ldx, 0.0, T.p, w, false, true));
+    // X[i0:i1, i1:k] = -D_b T
+    TK_TRY(tk_dgemm(ctx, false, false, h, w, h, -1.0, X + (int64_t)i0 * ldx + i0, ldx, T.p, w,
+                    0.0, X + (int64_t)i0 * ldx + i1, ldx));
   }
   return TK_OK;
 }

@@ -101,6 +101,20 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     printf("%s n=%d rc=%d total %.3f ms\n", what, n, rc, ms);
+    if (rep == 2 && !strcmp(what, "triinv")) {
+      // X R = I for the upper triangular R (unpivoted Cholesky factor of H), on the host
+      std::vector<double> ro((size_t)n * n), xi((size_t)n * n);
+      cudaMemcpy(ro.data(), dR, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(xi.data(), dQ, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      double e = 0.0;
+      for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) {
+          double s2 = 0.0;
+          for (int t = 0; t < n; t++) s2 += xi[(size_t)i * n + t] * ro[(size_t)t * n + j];
+          e = std::max(e, fabs(s2 - (i == j ? 1.0 : 0.0)));
+        }
+      printf("   max |X R - I| = %.2e\n", e);
+    }
     if (rep == 2 && !strcmp(what, "pchol")) {
       // reconstruction H ~ Ro^T Ro over the first k rows, on the host
       std::vector<double> ro((size_t)n * n);
