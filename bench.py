@@ -118,6 +118,12 @@ DGEMM_TRAFFIC = {"launch": "bond1.form_W (786432 x 640 x 896)", "dram_bytes": 9.
                  "algorithmic_bytes": 9.67e9, "source": "profiles/r01/ncu_dgemm_formW.txt"}
 
 
+# FP64 tensor-pipe ceiling measured on this pool's B200 (register-only DMMA m8n8k4 chains,
+# >= 8 warps/SM, 1965 MHz): tools/ubench/dmma_peak.cu.  Stricter than the rule-derived peak
+# (bf16 measured x 45/2250 = 32.5), so both fractions are reported.
+DMMA_PEAK_MEASURED = 37.1
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -323,6 +329,8 @@ def run_ours(args, cfg, op, x):
             roofline = {"kernel": cat, "bound": "tensor", "achieved": ach, "peak": fp64_peak,
                         "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
                         "traffic_capture": DGEMM_TRAFFIC,
+                        "peak_dmma_measured": DMMA_PEAK_MEASURED,
+                        "frac_vs_measured_dmma": ach / DMMA_PEAK_MEASURED,
                         "peak_source": f"bf16 {peak_kind} {peaks['bf16_tflops']} x 45/2250 (fp64 DMMA nominal ratio)",
                         "launches": cnt, "avg_ms": avg_ms, "share_of_step": ms / total_ms}
         elif by > 0:
