@@ -249,6 +249,40 @@ def test_apply_round_parity_random(seed, ctx):
                 gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), tol, 0, want_info=True))
 
 
+@pytest.mark.parametrize("shape", [
+    # (n_x, n_xi, n_t, T, r1, r2): n_t > T r2 (time core orthogonalised, L3 != identity)
+    (40, 3, 24, 2, 3, 2),
+    # n_xi k3 <= T r1 (Q2 = identity) and T = 1
+    (35, 2, 3, 1, 5, 4),
+    # rank one everywhere, several terms
+    (50, 4, 6, 3, 1, 1),
+])
+def test_apply_round_parity_shapes(shape, ctx):
+    """Both branches of the identity shortcuts (Q3, Q2) through the fused path."""
+    n_x, n_xi, n_t, T, r1, r2 = shape
+    rng = np.random.default_rng(sum(shape))
+    op = random_operator(rng, n_x, n_xi, n_t, T)
+    x = random_tt(rng, n_x, n_xi, n_t, r1, r2)
+    y = otT.apply_op(op, x)
+    g = gpu_op(op, ctx)
+    for tol, rmax in ((1e-12, 0), (1e-4, 0), (1e-6, 2)):
+        check_round(y, tol, rmax, ctx, dense=True,
+                    gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), tol, rmax,
+                                                   want_info=True))
+
+
+def test_apply_round_zero_input(ctx):
+    """The zero tensor through the fused path canonicalises to ranks (1, 1), zero cores."""
+    rng = np.random.default_rng(21)
+    op = random_operator(rng, 30, 3, 5, 2)
+    x = [np.zeros((30, 2)), np.zeros((2, 3, 2)), np.zeros((2, 5))]
+    g = gpu_op(op, ctx)
+    y, info = ttk.tt_apply_round(g, ttk.TT.from_cores(*x), 1e-8, 0, want_info=True)
+    assert y.ranks == (1, 1)
+    assert info.norm == 0.0
+    assert all(np.all(c == 0) for c in y.cores_numpy())
+
+
 @pytest.mark.slow
 def test_apply_round_parity_c3(ctx):
     cfg = CONFIGS["c3"]
