@@ -384,7 +384,25 @@ __global__ void __launch_bounds__(32 * QB)
                    double* __restrict__ Vout, double* __restrict__ Tout,
                    double* __restrict__ VTout, double* __restrict__ VTtout,
                    const double* __restrict__ Vprev, const double* __restrict__ VTtprev,
-                   unsigned long long* __restrict__ dbg) {
+                   unsigned long long* __restrict__ dbg, int panel, int* __restrict__ stop_at,
+                   const double* __restrict__ sqprev, int nsq, const double* __restrict__ thr2) {
+  // early stop (rank revealed): the trailing block beyond this panel, as measured two panels
+  // ago (H_prev is orthogonal: its norm can only be smaller now), is at the noise level
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
+    int stop = *(volatile int*)stop_at <= panel;
+    if (!stop && sqprev) {
+      double t = 0.0;
+      for (int i = 0; i < nsq; i++) t += sqprev[i];
+      if (t <= thr2[0]) {
+        atomicMin(stop_at, panel);
+        stop = 1;
+      }
+    }
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) return;
   auto stamp = [&](int k) {
     if (dbg && threadIdx.x == 0) {
       unsigned long long t;
@@ -614,9 +632,17 @@ __global__ void __launch_bounds__(32 * QB)
 // warps and reduced in shared memory, phase 2 updates the strip row by row.  Rows of V and X
 // are warp-uniform (broadcast loads), C accesses are coalesced along the strip.
 constexpr int AR_W = 4, AR_T = 256, AR_G = AR_T / AR_W, AR_U = 4;
+// Optional early-stop bookkeeping (trailing updates of pass 1): the kernel is skipped when
+// panel >= *stop_at, and writes to sqpart[blockIdx.x] the sum of squares of its updated values in
+// rows >= rowskip (deterministic per-CTA partial; the panel two steps later sums them).
 __global__ void __launch_bounds__(AR_T) apply_reflector_k(int m, int nc, const double* __restrict__ V,
                                                           const double* __restrict__ X,
-                                                          double* __restrict__ C, int64_t ldc) {
+                                                          double* __restrict__ C, int64_t ldc,
+                                                          int panel = 0,
+                                                          const int* __restrict__ stop_at = nullptr,
+                                                          double* __restrict__ sqpart = nullptr,
+                                                          int rowskip = 0) {
+  if (stop_at && panel >= *(volatile const int*)stop_at) return;
   __shared__ double red[AR_G][QB][AR_W];
   __shared__ double Ws[QB][AR_W];
   const int col = threadIdx.x % AR_W, rg = threadIdx.x / AR_W;
@@ -659,8 +685,8 @@ __global__ void __launch_bounds__(AR_T) apply_reflector_k(int m, int nc, const d
   double w[QB];
 #pragma unroll
   for (int q = 0; q < QB; q++) w[q] = Ws[q][col];
-  if (!live) return;
-  for (int i0 = rg; i0 < m; i0 += AR_G * AR_U) {
+  double sq = 0.0;
+  for (int i0 = rg; live && i0 < m; i0 += AR_G * AR_U) {
     double d[AR_U];
 #pragma unroll
     for (int u = 0; u < AR_U; u++) {
@@ -677,8 +703,23 @@ __global__ void __launch_bounds__(AR_T) apply_reflector_k(int m, int nc, const d
 #pragma unroll
     for (int u = 0; u < AR_U; u++) {
       const int i = i0 + u * AR_G;
-      if (i < m) C[(int64_t)i * ldc + gc] -= d[u];
+      if (i < m) {
+        const double v = C[(int64_t)i * ldc + gc] - d[u];
+        C[(int64_t)i * ldc + gc] = v;
+        if (i >= rowskip) sq = fma(v, v, sq);
+      }
     }
+  }
+  if (sqpart) {
+    __syncthreads();  // red is reused for the partial sums
+    double* r = &red[0][0][0];
+    r[threadIdx.x] = sq;
+    __syncthreads();
+    for (int st = AR_T / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) r[threadIdx.x] += r[threadIdx.x + st];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) sqpart[blockIdx.x] = r[0];
   }
 }
 
@@ -689,7 +730,9 @@ __global__ void __launch_bounds__(256) apply_reflector_right_k(int n, int m,
                                                                const double* __restrict__ V,
                                                                const double* __restrict__ VTt,
                                                                double* __restrict__ C,
-                                                               int64_t ldc) {
+                                                               int64_t ldc, int panel,
+                                                               const int* __restrict__ stop_at) {
+  if (panel >= *(volatile const int*)stop_at) return;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= n) return;
@@ -722,6 +765,26 @@ __global__ void __launch_bounds__(256) apply_reflector_right_k(int n, int m,
   }
 }
 
+// thr2[0] = (64 eps ||A||_F)^2 and stop_at[0] = INT_MAX (one CTA, fixed-order reduction)
+__global__ void __launch_bounds__(1024) qr_stop_init_k(int64_t nn, const double* __restrict__ A,
+                                                       double* __restrict__ thr2,
+                                                       int* __restrict__ stop_at) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < nn; e += blockDim.x) s = fma(A[e], A[e], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double e64 = 64.0 * 2.220446049250313e-16;
+    thr2[0] = e64 * e64 * red[0];
+    stop_at[0] = 0x7fffffff;
+  }
+}
+
 }  // namespace
 
 // Q (n x n, row-major) from the Householder QR of A (n x n, row-major; A is not modified).
@@ -738,6 +801,18 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   TK_TRY(VTtb.get(ctx, (size_t)np * n * QB));
   TK_TRY(Tb.get(ctx, (size_t)np * QB * QB));
   TK_TRY(tk_eye(ctx, Q, n));
+  // early stop once the trailing block is at the rounding-noise level (numerical rank reached):
+  // the remaining reflectors would act on noise and the identity completion is as good a pass-1
+  // basis; sqpart[p]: per-CTA squared norms written by the trailing update of panel p
+  const int sq_stride = (n + AR_W - 1) / AR_W + 1;
+  DevBuf qst, sqpart;
+  TK_TRY(qst.get(ctx, 2));
+  TK_TRY(sqpart.get(ctx, (size_t)np * sq_stride));
+  double* thr2 = qst.p;
+  int* stop_at = (int*)(qst.p + 1);
+  static const bool no_stop = getenv("TTK_QR_NO_EARLY_STOP") != nullptr;
+  qr_stop_init_k<<<1, 1024, 0, ctx->stream>>>((int64_t)n * n, A, thr2, stop_at);
+  TK_LAUNCH_CHECK(ctx);
   static const bool dbg = getenv("TTK_DEBUG_QR") != nullptr;
   DevBuf dbgb;
   if (dbg) TK_TRY(dbgb.get(ctx, 12 * (size_t)np));
@@ -776,6 +851,16 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
       // register-resident columns
       const size_t rsmem = sizeof(double) * (size_t)mt * (QB + 1);
       const double* Pp = Aw.p + (int64_t)(j0 - off) * n + j0;
+      // the trailing update of panel p-2 measured the block this panel would work on
+      const double* sqp = nullptr;
+      int nsq = 0;
+      if (!no_stop && p >= 2) {
+        const int c2q = (p - 2) * QB + 2 * QB;
+        if (n - c2q > 0) {
+          sqp = sqpart.p + (size_t)(p - 2) * sq_stride;
+          nsq = (n - c2q + AR_W - 1) / AR_W;
+        }
+      }
 #define TK_QR_REG(MR)                                                                        \
   {                                                                                          \
     static bool at = false;                                                                  \
@@ -785,7 +870,8 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
       at = true;                                                                             \
     }                                                                                        \
     qr_panel_reg_k<MR><<<1, 32 * QB, rsmem, s0>>>(m, jb, Pp, n, Vp, Tp, VTp, VTtp, Vq0, VTtq0, \
-        dbgb.p ? (unsigned long long*)dbgb.p + 12 * p : nullptr);                             \
+        dbgb.p ? (unsigned long long*)dbgb.p + 12 * p : nullptr, p, stop_at,                   \
+        sqp, nsq, thr2);                                                                       \
   }
       if (mt <= 32 * 8)
         TK_QR_REG(8)
@@ -838,13 +924,14 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s1, evF[p], 0));
     if (n - c2 > 0) {
       apply_reflector_k<<<(n - c2 + AR_W - 1) / AR_W, AR_T, 0, s1>>>(
-          m, n - c2, Vp, VTtp, Aw.p + (int64_t)j0 * n + c2, n);
+          m, n - c2, Vp, VTtp, Aw.p + (int64_t)j0 * n + c2, n, p, stop_at,
+          sqpart.p + (size_t)p * sq_stride, jb);
       TK_LAUNCH_CHECK(ctx);
     }
     TK_CUDA_TRY(ctx, cudaEventRecord(evR[p], s1));
     // s2: Q <- Q H_p (all n rows, columns j0..n)
     TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s2, evF[p], 0));
-    apply_reflector_right_k<<<(n + 7) / 8, 256, 0, s2>>>(n, m, Vp, VTtp, Q + j0, n);
+    apply_reflector_right_k<<<(n + 7) / 8, 256, 0, s2>>>(n, m, Vp, VTtp, Q + j0, n, p, stop_at);
     TK_LAUNCH_CHECK(ctx);
     // s0: panel p+1 (its columns got H_{p-1} from s1; it applies H_p itself), then factor it
     if (nnext > 0) {

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include "../../paper_1906_06785_b200/csrc/ttk_internal.h"
 
+static int g_rank = -1;  // < n: exact rank of the synthetic H (eigenvalues beyond it are 0)
 static void spd(int n, std::vector<double>& H, double span) {
   // H = B diag(d) B^T with B random, d graded over `span` decades
   std::vector<double> B((size_t)n * n);
@@ -17,7 +18,7 @@ static void spd(int n, std::vector<double>& H, double span) {
   for (auto& v : B) v = (rand() / (double)RAND_MAX) - 0.5;
   H.assign((size_t)n * n, 0.0);
   std::vector<double> d(n);
-  for (int i = 0; i < n; i++) d[i] = pow(10.0, -span * i / n);
+  for (int i = 0; i < n; i++) d[i] = (g_rank >= 0 && i >= g_rank) ? 0.0 : pow(10.0, -span * i / n);
   for (int i = 0; i < n; i++)
     for (int j = 0; j <= i; j++) {
       double s = 0;
@@ -29,6 +30,7 @@ static void spd(int n, std::vector<double>& H, double span) {
 int main(int argc, char** argv) {
   int n = argc > 1 ? atoi(argv[1]) : 896;
   const char* what = argc > 2 ? argv[2] : "qr";
+  if (argc > 3) g_rank = atoi(argv[3]);
   if (!strcmp(what, "gemm") || !strcmp(what, "gram")) {
     // c4 bond-1 shapes: W = Y P (786432 x 640 x 896) and G_W = W^T W (sym)
     const int64_t M = 786432, K = 896, N = 640;
@@ -152,6 +154,17 @@ int main(int argc, char** argv) {
           et = std::max(et, fabs(s) / hn);
         }
       printf("   max |Q^T Q - I| = %.2e   max |(Q^T H)_{i>j}| / max|H| = %.2e\n", eo, et);
+      if (g_rank >= 0) {
+        // range(H) inside span(Q[:, :rank]): rows >= rank of Q^T H vanish
+        double el = 0.0;
+        for (int i = g_rank; i < n; i++)
+          for (int j = 0; j < n; j++) {
+            double s2 = 0.0;
+            for (int k = 0; k < n; k++) s2 += hq[(size_t)k * n + i] * H[(size_t)k * n + j];
+            el = std::max(el, fabs(s2) / hn);
+          }
+        printf("   rank %d: max |(Q^T H)_{i>=rank}| / max|H| = %.2e\n", g_rank, el);
+      }
     }
     if (rep == 2) {
       static char buf[1 << 22];
