@@ -311,7 +311,7 @@ def run_ours(args, cfg, op, x):
     # named kernels below is a launch of the DMMA GEMM (dgemm_kernel + its split-K reduce)
     named = {"jacobi": "jacobi_persistent_k", "qr_panel": "qr_panel_warp_k",
              "qr_reflector": "apply_reflector_k", "pchol_panel": "pchol_panel_k",
-             "spmm_multi": "spmm_multi_k", "stoch_apply": "stoch_apply_k",
+             "spmm_multi": "spmm_merged_k", "stoch_apply": "stoch_apply_k",
              "time_apply": "time_apply_k"}
     kernels = {}
     for cat, v in phases.items():
@@ -345,6 +345,29 @@ def run_ours(args, cfg, op, x):
                         "avg_ms": avg_ms, "share_of_step": ms / total_ms}
     spmm = phases.get("spmm_multi")
     spmm_gbs = spmm[3] / (spmm[1] * 1e-3) / 1e9 if spmm else None
+
+    # the TT axpby of GMRES (a9/a10 rows) on the rounded result: z = a y + b y, a copy stream
+    # (16 bytes per U1 entry of z), timed by the library's own per-kernel events
+    axpby_gbs = None
+    # x and y are distinct TTs of equal ranks (y and a copy of it: no L2 reuse between them)
+    y2 = ttk.TT.from_cores(*y.cores_numpy())
+    zcap = ttk.TT(op.n_x, op.n_xi, op.n_t, 2 * y.r1, 2 * y.r2)
+    ttk.tt_axpby(0.5, y, -0.25, y2, ctx, out=zcap)
+    torch.cuda.synchronize()
+    L.tk_ctx_profile(ctx._h, 1)
+    for _ in range(5):
+        ttk.tt_axpby(0.5, y, -0.25, y2, ctx, out=zcap)
+    torch.cuda.synchronize()
+    buf2 = __import__("ctypes").create_string_buffer(1 << 16)
+    L.tk_ctx_profile_dump(ctx._h, buf2, len(buf2))
+    L.tk_ctx_profile(ctx._h, 0)
+    ax = [ln.split() for ln in buf2.value.decode().splitlines() if ln.startswith("axpby")]
+    if ax:
+        axpby_gbs = {"value": sum(float(a[3]) for a in ax) / (sum(float(a[1]) for a in ax) * 1e-3) / 1e9,
+                     "unit": "GB/s", "peak": peaks["hbm_gbs"], "ranks": [2 * y.r1, 2 * y.r2],
+                     "bytes_per_call": float(ax[0][3]), "calls": len(ax)}
+        axpby_gbs["frac"] = axpby_gbs["value"] / peaks["hbm_gbs"]
+    del zcap, y2
 
     # e2e through the public API with host buffers
     e2e = None
@@ -394,6 +417,7 @@ def run_ours(args, cfg, op, x):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(cfg, op), "ranks_out": list(ranks_out),
             "roofline": roofline, "spmm_gbs": spmm_gbs,
+            "spmm_frac": spmm_gbs / peaks["hbm_gbs"] if spmm_gbs else None, "axpby_gbs": axpby_gbs,
             "phases_ms_per_step": {k: round(v[1] / args.steps, 4) for k, v in phases.items()},
             "kernels_ms_per_step": {k: round(v[1] / args.steps, 4) for k, v in kernels.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),

@@ -11,6 +11,7 @@
 //  time_apply : Y3[k r2 + b, :] = U3[b, :] T_k^T with T_k in LAPACK band storage.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -150,6 +151,165 @@ __global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm
   }
 }
 
+// Column-merged variant (T <= TM terms).  All T terms of a spatial row are merged by column
+// (host side, tk_op_create): for each DISTINCT column c of the row, one word col | mask << 32
+// (bit k of mask = term k has an entry at (i, c)) and, in (c, k) order, the values.  A warp
+// loads each U1 row ONCE for all the terms that touch it (the per-term kernel above loads it
+// once per term: at c4 44 U1-row gathers per spatial row become ~7).  Lane j expands distinct
+// column j's values into a dense, zero-padded TM-vector in shared memory, so the inner loop is
+// branch-free: per distinct column one U1 row load, TM/2 16-byte broadcast loads of values and
+// 2 TM FMAs into the T x RPL register accumulators (k a compile-time index).  Per term the
+// entries are still summed in ascending column order, as in each term's sorted CSR row (the
+// zero padding adds exact zeros).  The row's T r outputs are streamed once at the end.
+//
+// Each row is ONE contiguous record in `rec` (int64 words): [gn][gn words col | mask << 32]
+// [values as doubles], at rec + recptr[i].  The row loop is software-pipelined: while row i is
+// computed, the record of the warp's next row (RW words per lane, one coalesced load) and the
+// record pointer of the row after it are already in flight, so the dependent global loads
+// (pointer -> record) leave the critical path; only the U1 row gathers (L2) remain on it.
+template <int TM, bool V2>
+__global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int r,
+                                                       const int64_t* __restrict__ recptr,
+                                                       const long long* __restrict__ rec,
+                                                       const double* __restrict__ U1,
+                                                       double* __restrict__ Y1) {
+  static_assert(TM % 2 == 0, "TM even (16-byte value loads)");
+  constexpr int RPL = V2 ? 2 : 1;
+  constexpr int CW = 32 * RPL;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int UNR = V2 ? 2 : 8;  // U1 rows loaded together
+  constexpr int RW = 3;   // record words per lane held in registers (96 per warp)
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t R = (int64_t)T * r;
+  // per warp: the staged record, dense values [distinct column][term pair] and the distinct
+  // columns (<= 32 per row: the host routes longer merged rows to the per-term kernel)
+  __shared__ long long rec_all[256 / 32][32 * RW];
+  __shared__ double2 vd_all[256 / 32][32][TM / 2];
+  __shared__ int col_all[256 / 32][32];
+  long long* rs = rec_all[threadIdx.x >> 5];
+  double2 (*vd)[TM / 2] = vd_all[threadIdx.x >> 5];
+  int* cols = col_all[threadIdx.x >> 5];
+
+  auto load_rec = [&](int64_t row, int64_t p0, int64_t p1, long long* w) {
+#pragma unroll
+    for (int m = 0; m < RW; m++) {
+      const int64_t e = lane + 32 * m;
+      w[m] = (row < n_x && e < p1 - p0) ? __ldg(rec + p0 + e) : 0LL;
+    }
+  };
+  int64_t i = warp;
+  int64_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;
+  if (i < n_x) {
+    p0 = __ldg(recptr + i);
+    p1 = __ldg(recptr + i + 1);
+  }
+  if (i + nwarps < n_x) {
+    q0 = __ldg(recptr + i + nwarps);
+    q1 = __ldg(recptr + i + nwarps + 1);
+  }
+  long long cur[RW];
+  load_rec(i, p0, p1, cur);
+  for (; i < n_x; i += nwarps) {
+    // pipeline: next row's record and the pointer of the row after it
+    long long nxt[RW];
+    load_rec(i + nwarps, q0, q1, nxt);
+    int64_t s0 = 0, s1 = 0;
+    if (i + 2 * nwarps < n_x) {
+      s0 = __ldg(recptr + i + 2 * nwarps);
+      s1 = __ldg(recptr + i + 2 * nwarps + 1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < RW; m++) rs[lane + 32 * m] = cur[m];
+    __syncwarp();
+    const int gn = (int)rs[0];
+    const long long w = lane < gn ? rs[1 + lane] : 0LL;
+    const unsigned mask = (unsigned)(w >> 32);
+    const int cnt = __popc(mask);
+    int off = cnt;  // inclusive scan of the value counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, off, o);
+      if (lane >= o) off += t;
+    }
+    off -= cnt;
+    const int gp = (gn + UNR - 1) / UNR * UNR;  // padded to the unroll: pad slots hold zeros
+    if (lane < gp) {  // lane j: dense, zero-padded values of distinct column j
+      const int64_t v0 = 1 + gn + off;
+      // staged record, or (rows longer than 32 RW words) straight from global
+      const long long* src = (p1 - p0 <= 32 * RW) ? rs + v0 : rec + p0 + v0;
+      int q = 0;
+#pragma unroll
+      for (int k = 0; k < TM; k += 2) {
+        double a = 0.0, b = 0.0;
+        if (mask & (1u << k)) a = __longlong_as_double(src[q++]);
+        if (mask & (2u << k)) b = __longlong_as_double(src[q++]);
+        vd[lane][k / 2] = make_double2(a, b);
+      }
+      cols[lane] = lane < gn ? (int)(w & 0xffffffffLL) : 0;
+    }
+    __syncwarp();
+    double* yrow = Y1 + i * R;
+    for (int c0 = 0; c0 < r; c0 += CW) {
+      const int cc = c0 + (V2 ? 2 * lane : lane);
+      const bool okc = cc < r;
+      const double* ub = U1 + (okc ? cc : 0);
+      double acc[TM][RPL];
+#pragma unroll
+      for (int k = 0; k < TM; k++)
+#pragma unroll
+        for (int q = 0; q < RPL; q++) acc[k][q] = 0.0;
+      for (int j0 = 0; j0 < gp; j0 += UNR) {
+        double u[UNR][RPL];
+#pragma unroll
+        for (int s = 0; s < UNR; s++) {
+          const double* urow = ub + (int64_t)cols[j0 + s] * r;
+          if (V2) {
+            const double2 t = __ldg((const double2*)urow);
+            u[s][0] = t.x;
+            u[s][RPL - 1] = t.y;
+          } else {
+            u[s][0] = __ldg(urow);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < UNR; s++) {
+#pragma unroll
+          for (int k = 0; k < TM; k += 2) {
+            const double2 v = vd[j0 + s][k / 2];
+#pragma unroll
+            for (int q = 0; q < RPL; q++) {
+              acc[k][q] = fma(v.x, u[s][q], acc[k][q]);
+              acc[k + 1][q] = fma(v.y, u[s][q], acc[k + 1][q]);
+            }
+          }
+        }
+      }
+      if (okc) {
+        double* dst = yrow + cc;
+#pragma unroll
+        for (int k = 0; k < TM; k++) {
+          if (k < T) {
+            if (V2)
+              __stcs((double2*)dst, make_double2(acc[k][0], acc[k][RPL - 1]));
+            else
+              __stcs(dst, acc[k][0]);
+          }
+          dst += r;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < RW; m++) cur[m] = nxt[m];
+    p0 = q0;
+    p1 = q1;
+    q0 = s0;
+    q1 = s1;
+  }
+}
+
 // The diagonal blocks only (the rest of Y2 is zeroed by a memset first):
 //   Y2[k r1 + a, i, k r2 + b] = sum_j G_k[i, j] U2[a, j, b]
 // blockIdx.y = row k r1 + a; threads over (i, b), b fastest (coalesced U2 reads and Y2 writes,
@@ -203,6 +363,36 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
 
+  if (op->rec && !op->spmm_perterm) {
+    blocks = std::min<int64_t>((n_x * 32 + threads - 1) / threads, 16LL * ctx->num_sms);
+    // scalar lanes (two 32-column chunks at r = 64) measured faster than 16-byte lanes: the
+    // 2x accumulators of the 16-byte variant halve the resident warps (TTK_SPMM_V2=1 for it)
+    static const bool no_v2 = getenv("TTK_SPMM_V2") == nullptr;
+    const bool v2m = !no_v2 && (r % 2 == 0) && (((uintptr_t)U1 & 15) == 0) && (((uintptr_t)Y1 & 15) == 0);
+#define TK_SPMM_M(TM, V)                                                                    \
+  spmm_merged_k<TM, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                      \
+      n_x, op->T, r, op->recptr, (const long long*)op->rec, U1, Y1)
+    if (op->T <= 2) {
+      if (v2m) TK_SPMM_M(2, true); else TK_SPMM_M(2, false);
+    } else if (op->T <= 4) {
+      if (v2m) TK_SPMM_M(4, true); else TK_SPMM_M(4, false);
+    } else if (op->T <= 6) {
+      if (v2m) TK_SPMM_M(6, true); else TK_SPMM_M(6, false);
+    } else if (op->T <= 8) {
+      if (v2m) TK_SPMM_M(8, true); else TK_SPMM_M(8, false);
+    } else if (op->T <= 10) {
+      if (v2m) TK_SPMM_M(10, true); else TK_SPMM_M(10, false);
+    } else if (op->T <= 12) {
+      if (v2m) TK_SPMM_M(12, true); else TK_SPMM_M(12, false);
+    } else if (op->T <= 14) {
+      if (v2m) TK_SPMM_M(14, true); else TK_SPMM_M(14, false);
+    } else {
+      if (v2m) TK_SPMM_M(16, true); else TK_SPMM_M(16, false);
+    }
+#undef TK_SPMM_M
+    TK_LAUNCH_CHECK(ctx);
+    return TK_OK;
+  }
   const int rpl = (r + 31) / 32;
 #define TK_SPMM(R, V)                                                                       \
   spmm_multi_k<R, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                        \

@@ -113,13 +113,23 @@ __global__ void rank_select_k(int n, const double* __restrict__ lam, double* __r
 }
 
 // z = a x + b y cores (concatenation)
-__global__ void axpby_u1_k(int64_t n_x, int64_t rx, int64_t ry, const double* __restrict__ x1,
+// z1 = [x1 | y1] (n_x x (rx + ry)): a pure copy stream.  One thread per element (or per
+// 16-byte pair when rx, ry are even and the bases aligned); 32-bit index arithmetic when the
+// element count fits (the 64-bit division per element made the copy ALU-bound).
+template <typename I, bool V2>
+__global__ void axpby_u1_k(I n_x, I rx, I ry, const double* __restrict__ x1,
                            const double* __restrict__ y1, double* __restrict__ z1) {
-  int64_t R = rx + ry, n = n_x * R;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = e / R, c = e % R;
-    z1[e] = c < rx ? x1[i * rx + c] : y1[i * ry + (c - rx)];
+  constexpr int W = V2 ? 2 : 1;
+  const I ux = rx / W, uy = ry / W, U = ux + uy, n = n_x * U;
+  for (I e = blockIdx.x * (I)blockDim.x + threadIdx.x; e < n; e += (I)gridDim.x * blockDim.x) {
+    const I i = e / U, c = e - i * U;
+    if (V2) {
+      const double2 v = c < ux ? __ldcs((const double2*)x1 + i * ux + c)
+                               : __ldcs((const double2*)y1 + i * uy + (c - ux));
+      __stcs((double2*)z1 + e, v);
+    } else {
+      z1[e] = c < ux ? __ldcs(x1 + i * ux + c) : __ldcs(y1 + i * uy + (c - ux));
+    }
   }
 }
 __global__ void axpby_u2_k(int64_t rx1, int64_t ry1, int64_t n_xi, int64_t rx2, int64_t ry2,
@@ -306,8 +316,26 @@ int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double to
 int tk_axpby_cores(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
                    const tk_tt* y, tk_tt* z) {
   int64_t R1 = x->r1 + y->r1, R2 = x->r2 + y->r2;
-  axpby_u1_k<<<grid_for(ctx, x->n_x * R1), 256, 0, ctx->stream>>>(x->n_x, x->r1, y->r1, x->U1,
-                                                                  y->U1, z->U1);
+  {
+    const bool v2 = x->r1 % 2 == 0 && y->r1 % 2 == 0 && ((uintptr_t)x->U1 & 15) == 0 &&
+                    ((uintptr_t)y->U1 & 15) == 0 && ((uintptr_t)z->U1 & 15) == 0;
+    const int64_t n = x->n_x * R1 / (v2 ? 2 : 1);
+    const int g = grid_for(ctx, n);
+    if (n < (int64_t)INT32_MAX - 256LL * g) {
+      if (v2)
+        axpby_u1_k<uint32_t, true><<<g, 256, 0, ctx->stream>>>(
+            (uint32_t)x->n_x, (uint32_t)x->r1, (uint32_t)y->r1, x->U1, y->U1, z->U1);
+      else
+        axpby_u1_k<uint32_t, false><<<g, 256, 0, ctx->stream>>>(
+            (uint32_t)x->n_x, (uint32_t)x->r1, (uint32_t)y->r1, x->U1, y->U1, z->U1);
+    } else if (v2) {
+      axpby_u1_k<int64_t, true><<<g, 256, 0, ctx->stream>>>(x->n_x, x->r1, y->r1, x->U1, y->U1,
+                                                             z->U1);
+    } else {
+      axpby_u1_k<int64_t, false><<<g, 256, 0, ctx->stream>>>(x->n_x, x->r1, y->r1, x->U1, y->U1,
+                                                              z->U1);
+    }
+  }
   TK_LAUNCH_CHECK(ctx);
   axpby_u2_k<<<grid_for(ctx, R1 * x->n_xi * R2), 256, 0, ctx->stream>>>(
       x->r1, y->r1, x->n_xi, x->r2, y->r2, x->U2, y->U2, z->U2);

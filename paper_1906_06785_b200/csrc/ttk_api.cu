@@ -171,6 +171,69 @@ static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
 }
 
 // ============================================================================ operator
+// Column-merged copy of the T spatial factors for spmm_merged_k (k_apply.cu): per row, the
+// distinct columns over all terms in ascending order, each as col | (term mask << 32), and the
+// values in (column, term) order.  Duplicate (column, term) entries are summed.  Not built (the
+// per-term kernel runs) when a row has more than 32 distinct columns.
+static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
+                        const int32_t* const* K_col, const double* const* K_val) {
+  const int T = op->T;
+  const int64_t n_x = op->n_x;
+  std::vector<int64_t> recptr(n_x + 1, 0), rec, words;
+  std::vector<double> vals;
+  int64_t tot = 0;
+  for (int k = 0; k < T; k++) tot += K_rowptr[k][n_x];
+  rec.reserve(tot + tot / 4 + 2 * n_x + 16);
+  struct E {
+    int32_t c;
+    int32_t k;
+    double v;
+  };
+  std::vector<E> ents;
+  for (int64_t i = 0; i < n_x; i++) {
+    ents.clear();
+    words.clear();
+    vals.clear();
+    for (int k = 0; k < T; k++)
+      for (int32_t p = K_rowptr[k][i]; p < K_rowptr[k][i + 1]; p++)
+        ents.push_back({K_col[k][p], k, K_val[k][p]});
+    std::stable_sort(ents.begin(), ents.end(), [](const E& a, const E& b) {
+      return a.c != b.c ? a.c < b.c : a.k < b.k;
+    });
+    size_t q = 0;
+    while (q < ents.size()) {
+      const int32_t c = ents[q].c;
+      uint32_t mask = 0;
+      while (q < ents.size() && ents[q].c == c) {
+        const int k = ents[q].k;
+        double v = 0.0;
+        while (q < ents.size() && ents[q].c == c && ents[q].k == k) v += ents[q++].v;
+        mask |= 1u << k;
+        vals.push_back(v);
+      }
+      words.push_back((int64_t)(uint32_t)c | ((int64_t)mask << 32));
+    }
+    // the merged kernel keeps one row's distinct columns in one warp's lanes
+    if (words.size() > 32) return TK_OK;  // per-term kernel for this operator
+    rec.push_back((int64_t)words.size());
+    rec.insert(rec.end(), words.begin(), words.end());
+    for (double v : vals) {
+      int64_t b;
+      memcpy(&b, &v, sizeof(b));
+      rec.push_back(b);
+    }
+    recptr[i + 1] = (int64_t)rec.size();
+  }
+  auto up = [&](void** d, const void* h, size_t b) -> int {
+    TK_CUDA_TRY(ctx, cudaMalloc(d, b ? b : 8));
+    if (b) TK_CUDA_TRY(ctx, cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice));
+    return TK_OK;
+  };
+  TK_TRY(up((void**)&op->recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
+  TK_TRY(up((void**)&op->rec, rec.data(), sizeof(int64_t) * rec.size()));
+  return TK_OK;
+}
+
 extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_t n_xi,
                             int64_t n_t, const int32_t* const* K_rowptr,
                             const int32_t* const* K_col, const double* const* K_val,
@@ -249,6 +312,11 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
   }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
                               cudaMemcpyHostToDevice));
+  if (T <= 16) TK_TRY(build_merged(ctx, op.get(), K_rowptr, K_col, K_val));
+  {
+    const char* e = getenv("TTK_SPMM_PERTERM");
+    op->spmm_perterm = e && e[0] == '1';
+  }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_kl, T_kl, sizeof(int) * T, cudaMemcpyHostToDevice));
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_ku, T_ku, sizeof(int) * T, cudaMemcpyHostToDevice));
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_off, band_off.data(), sizeof(int64_t) * (T + 1),
@@ -268,6 +336,8 @@ extern "C" int tk_op_destroy(tk_op* op) {
   cudaFree(op->band_ku);
   cudaFree(op->band_off);
   cudaFree(op->band);
+  cudaFree(op->recptr);
+  cudaFree(op->rec);
   delete op;
   return TK_OK;
 }
@@ -961,7 +1031,18 @@ extern "C" int tk_axpby(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const 
     ctx->err = "tk_axpby: output capacity < rank sums";
     return TK_ECAP;
   }
-  TK_TRY(tk_axpby_cores(ctx, a_dev, x, b_dev, y, z));
+  {
+    // algorithmic bytes: every core entry of x and y read once, every entry of z written once
+    // (the zero blocks of z's middle core are written, not read)
+    const double R1 = (double)(x->r1 + y->r1), R2 = (double)(x->r2 + y->r2);
+    const double bytes = 8.0 * (2.0 * x->n_x * R1 +
+                                (x->r1 * x->r2 + y->r1 * y->r2 + R1 * R2) * x->n_xi +
+                                2.0 * R2 * x->n_t);
+    TagScope ts(ctx, "axpby");
+    const int id = tk_prof_begin(ctx, "axpby", 0.0, bytes);
+    TK_TRY(tk_axpby_cores(ctx, a_dev, x, b_dev, y, z));
+    tk_prof_end(ctx, id);
+  }
   z->r1 = x->r1 + y->r1;
   z->r2 = x->r2 + y->r2;
   return TK_OK;

@@ -69,6 +69,12 @@ struct tk_op {
   int* band_ku = nullptr;      // T
   int64_t* band_off = nullptr; // T+1 prefix offsets into band
   double* band = nullptr;      // concatenated LAPACK band arrays
+  // column-merged copy of all T terms (T <= 16, <= 32 distinct columns per row; k_apply.cu
+  // spmm_merged_k): row i's record at rec + recptr[i] is [gn][gn words col | term-mask << 32]
+  // [values (as doubles) in (column, term) order]
+  int64_t* recptr = nullptr;   // n_x + 1
+  int64_t* rec = nullptr;
+  bool spmm_perterm = false;   // TTK_SPMM_PERTERM=1: use the per-term kernel
   std::vector<int64_t> h_nnz;  // host copy of per-term nnz
   int max_kl = 0, max_ku = 0;
 };

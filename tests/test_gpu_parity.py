@@ -96,6 +96,27 @@ def test_apply_parity_random_ragged(seed, ctx):
         assert rel(a, b) <= 1e-13
 
 
+@pytest.mark.parametrize("T,n_x,density,r1,perterm", [
+    (17, 60, 0.1, 8, False),    # T > 16: the per-term kernel
+    (16, 80, 0.6, 64, False),   # rows with > 32 distinct columns and > 256 values (unstaged)
+    (9, 200, 0.02, 66, False),  # two column chunks, ragged second chunk
+    (5, 150, 0.3, 7, False),    # odd r: scalar lanes
+    (6, 150, 0.3, 40, True),    # TTK_SPMM_PERTERM=1
+])
+def test_apply_spmm_paths(T, n_x, density, r1, perterm, ctx, monkeypatch):
+    """Both SpMM kernels (column-merged for T <= 16, per-term otherwise or on request) and the
+    merged kernel's group / staging limits, vs the oracle apply."""
+    if perterm:
+        monkeypatch.setenv("TTK_SPMM_PERTERM", "1")
+    rng = np.random.default_rng(T * 1000 + n_x)
+    op = random_operator(rng, n_x, 3, 5, T, density=density, max_band=1)
+    x = random_tt(rng, n_x, 3, 5, r1, 2)
+    y_o = otT.apply_op(op, x)
+    y_g = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x)).cores_numpy()
+    for a, b in zip(y_g, y_o):
+        assert rel(a, b) <= 1e-13
+
+
 def test_apply_capacity_and_shape_errors(ctx):
     rng = np.random.default_rng(3)
     op = random_operator(rng, 10, 3, 4, 2)
