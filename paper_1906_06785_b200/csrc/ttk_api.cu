@@ -93,9 +93,62 @@ int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
   return TK_OK;
 }
 
+CritScope::CritScope(tk_ctx* ctx) : c(ctx) {
+  static const bool serial = getenv("TTK_SERIAL") != nullptr;
+  if (serial) return;
+  if (!ctx->crit) {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return;
+    if (cudaStreamCreateWithPriority(&ctx->crit, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      ctx->crit = nullptr;
+      return;
+    }
+    for (auto& e : ctx->crit_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  user = ctx->stream;
+  cudaEventRecord(ctx->crit_ev[0], user);
+  cudaStreamWaitEvent(ctx->crit, ctx->crit_ev[0], 0);
+  ctx->stream = ctx->crit;
+  on = true;
+}
+CritScope::~CritScope() {
+  if (!on) return;
+  cudaEventRecord(c->crit_ev[1], c->crit);
+  cudaStreamWaitEvent(user, c->crit_ev[1], 0);
+  c->stream = user;
+}
+
+int tk_side_fork(tk_ctx* ctx) {
+  if (!ctx->side) {
+    int lo = 0, hi = 0;
+    TK_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TK_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo));
+    for (auto& e : ctx->side_ev) TK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  TK_CUDA_TRY(ctx, cudaEventRecord(ctx->side_ev[0], ctx->stream));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->side_ev[0], 0));
+  return TK_OK;
+}
+int tk_side_join(tk_ctx* ctx) {
+  if (!ctx->side) return TK_OK;
+  TK_CUDA_TRY(ctx, cudaEventRecord(ctx->side_ev[1], ctx->side));
+  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->side_ev[1], 0));
+  return TK_OK;
+}
+
 extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
   if (!ctx) return TK_OK;
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    for (auto e : ctx->side_ev) cudaEventDestroy(e);
+  }
+  if (ctx->crit) {
+    cudaStreamSynchronize(ctx->crit);
+    cudaStreamDestroy(ctx->crit);
+    for (auto e : ctx->crit_ev) cudaEventDestroy(e);
+  }
   for (auto& s : ctx->aux)
     if (s) {
       cudaStreamSynchronize(s);
@@ -140,11 +193,17 @@ extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
   if (!ctx) return TK_EARG;
   TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   std::string out;
+  static const bool tl = getenv("TTK_TIMELINE") != nullptr;
   for (auto& r : ctx->recs) {
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
     char line[256];
-    snprintf(line, sizeof(line), "%s %.6f %.6e %.6e\n", r.cat, ms, r.flops, r.bytes);
+    if (tl) {  // timeline: start offset (ms) from the first record, for overlap analysis
+      cudaEventElapsedTime(&t0, ctx->recs[0].a, r.a);
+      snprintf(line, sizeof(line), "%s %.6f %.6e %.6e %.4f\n", r.cat, ms, r.flops, r.bytes, t0);
+    } else {
+      snprintf(line, sizeof(line), "%s %.6f %.6e %.6e\n", r.cat, ms, r.flops, r.bytes);
+    }
     out += line;
   }
   if (buf && len) {
@@ -362,9 +421,14 @@ static int check_tt(tk_ctx* ctx, const tk_tt* x, const char* who) {
 
 // ============================================================================ apply
 // The space and time cores of y = A x: Y1 = [K_k U1]_k (SpMM), Y3 = [U3 T_k^T]_k (band).
-static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y) {
+// side: the SpMM runs on the side stream (forked here; the caller joins before it reads Y1)
+static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y,
+                            bool side = false) {
   const int64_t R1 = op->T * x->r1, R2 = op->T * x->r2;
+  if (side) TK_TRY(tk_side_fork(ctx));
   {
+    std::unique_ptr<OnSide> on;
+    if (side) on.reset(new OnSide(ctx));
     // algorithmic bytes: read U1 once, write Y1 once, read the CSR (12 B/nnz + rowptr)
     double nnz = 0;
     for (auto v : op->h_nnz) nnz += (double)v;
@@ -790,7 +854,11 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
   if (!ctx) return TK_EARG;
-  const int st = round_impl(ctx, x, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out);
+  int st;
+  {
+    CritScope cs(ctx);
+    st = round_impl(ctx, x, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out);
+  }
   pool_settle(ctx);
   return st;
 }
@@ -814,7 +882,12 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
     ctx->err = "tk_apply_round: output capacity < (T r1, T r2)";
     return TK_ECAP;
   }
-  TK_TRY(apply_space_time(ctx, op, x, y));
+  // the SpMM (HBM-bound, all SMs) overlaps the latency-bound sweep of the small cores; the
+  // round joins the side stream before its first read of Y1 (bond 1)
+  static const bool serial = getenv("TTK_SERIAL") != nullptr;
+  CritScope cs(ctx);  // (declared before every buffer below: joins back after they are freed)
+  TK_TRY(apply_space_time(ctx, op, x, y, !serial));
+  SideJoin sj(ctx, !serial);  // (round_impl joins before bond 1; this covers early returns)
   DevBuf blk;
   TK_TRY(blk.get(ctx, R1 * x->n_xi * x->r2));
   {
@@ -888,6 +961,7 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
     q2_id = false;
   }
   // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
+  TK_TRY(tk_side_join(ctx));  // U1 written by a side-stream SpMM (tk_apply_round)
   DevBuf W, GW1, V1, V2, Vt, lam, fl1;
   TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1, fl1));
   DevBuf sig1, scr;
@@ -919,15 +993,21 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
     TK_TRY(sync_read(ctx, s.data(), sig1.p, sizeof(double) * k2));
     for (int64_t i = 0; i < R1; i++) sigma1_out[i] = i < k2 ? s[i] : 0.0;
   }
-  // U1_new = W V2[:, :r1] diag(1/sig)  -> x->U1 (n_x x r1)
+  // U1_new = W V2[:, :r1] diag(1/sig)  -> x->U1 (n_x x r1), on the side stream: the DMMA-bound
+  // reconstruction overlaps the latency-bound bond-2 chain (joined before return; W and F1
+  // are released only after the join)
+  static const bool serial = getenv("TTK_SERIAL") != nullptr;
+  DevBuf F1;
+  TK_TRY(F1.get(ctx, k2 * r1));
+  TK_TRY(tk_col_scale(ctx, k2, r1, V2.p, k2, F1.p, r1, sig1.p, 1));
+  if (!serial) TK_TRY(tk_side_fork(ctx));
+  SideJoin sj(ctx, !serial);  // destroyed before F1 and W
   {
-    DevBuf F1;
-    TK_TRY(F1.get(ctx, k2 * r1));
-    TK_TRY(tk_col_scale(ctx, k2, r1, V2.p, k2, F1.p, r1, sig1.p, 1));
+    std::unique_ptr<OnSide> on;
+    if (!serial) on.reset(new OnSide(ctx));
     TagScope t(ctx, "bond1.form_U1");
     TK_TRY(tk_dgemm(ctx, false, false, n_x, r1, k2, 1.0, W.p, k2, F1.p, r1, 0.0, x->U1, r1));
   }
-  W.release();
   // C = (Vt[:, :r1] diag(sig))^T Q2   (r1 x N2)
   DevBuf S1, C;
   TK_TRY(S1.get(ctx, k2 * r1));
@@ -975,6 +1055,9 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
       TK_TRY(tk_dgemm(ctx, true, true, r2, n_t, k3, 1.0, S2.p, r2, Q3c.p, k3, 0.0, x->U3, n_t));
     }
   }
+  if (!serial) TK_TRY(tk_side_join(ctx));
+  W.release();
+  F1.release();
   x->r1 = r1;
   x->r2 = r2;
   TK_CUDA_TRY(ctx, cudaGetLastError());

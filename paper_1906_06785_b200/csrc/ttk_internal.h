@@ -39,6 +39,45 @@ struct tk_ctx {
   // forked from / joined to `stream` with events; created on first use
   cudaStream_t aux[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> fork_ev;
+  // one more side stream for independent big work (the apply's SpMM while the small cores are
+  // swept, the bond-1 reconstruction while bond 2 runs): side_ev[0] forks, side_ev[1] joins
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
+  // the rounding's latency-bound critical path runs on an internal highest-priority stream
+  // (forked from / joined back to the caller's stream per call), so the block scheduler hands
+  // SMs to it before the side stream's big kernels (which cannot be preempted)
+  cudaStream_t crit = nullptr;
+  cudaEvent_t crit_ev[2] = {nullptr, nullptr};
+};
+// Scoped move of a whole library call onto ctx->crit (fork from the caller's stream on entry,
+// join back on exit).
+struct CritScope {
+  tk_ctx* c;
+  cudaStream_t user = nullptr;
+  bool on = false;
+  explicit CritScope(tk_ctx* ctx);
+  ~CritScope();
+};
+// Fork: work issued on ctx->side after this call runs after everything issued so far on
+// ctx->stream.  Join: work issued on ctx->stream after this call runs after everything issued
+// so far on ctx->side.
+int tk_side_fork(tk_ctx* ctx);
+int tk_side_join(tk_ctx* ctx);
+// Joins the side stream on scope exit (also on early error returns) when armed.
+struct SideJoin {
+  tk_ctx* c;
+  bool armed;
+  SideJoin(tk_ctx* ctx, bool a) : c(ctx), armed(a) {}
+  ~SideJoin() {
+    if (armed) tk_side_join(c);
+  }
+};
+// Scoped redirection of the context's launches to the side stream.
+struct OnSide {
+  tk_ctx* c;
+  cudaStream_t old;
+  explicit OnSide(tk_ctx* ctx) : c(ctx), old(ctx->stream) { ctx->stream = ctx->side; }
+  ~OnSide() { c->stream = old; }
 };
 // Lazily created side streams and a pool of at least n sync events (timing disabled).
 int tk_aux_streams(tk_ctx* ctx, size_t n_events);
