@@ -61,7 +61,7 @@ struct TileGeom {
 // Load a BMN x BK tile of an operand into shared memory.
 //   KMAJOR: global element (k, m) at G[(k0+k)*ld + m0+m]   (contiguous in m)
 //   else  : global element (k, m) at G[(m0+m)*ld + k0+k]   (contiguous in k)
-template <bool KMAJOR, int BMN, bool VEC2>
+template <bool KMAJOR, int BMN, bool VEC2, int NTH = NT>
 __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__ G, int64_t ld,
                                           int64_t m0, int64_t mlim, int64_t k0, int64_t klim,
                                           int tid) {
@@ -69,7 +69,7 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   if (VEC2) {
     constexpr int PAIRS = BMN * BK / 2;
 #pragma unroll
-    for (int e = tid; e < PAIRS; e += NT) {
+    for (int e = tid; e < PAIRS; e += NTH) {
       int k, m;
       int64_t gk, gm;
       const double* src;
@@ -95,7 +95,7 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   } else {
     constexpr int ELEMS = BMN * BK;
 #pragma unroll
-    for (int e = tid; e < ELEMS; e += NT) {
+    for (int e = tid; e < ELEMS; e += NTH) {
       int k, m;
       if (KMAJOR) {
         k = e / BMN;
@@ -112,38 +112,38 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   }
 }
 
-// A_KMAJOR == transA ; B_KMAJOR == !transB
-template <bool A_KMAJOR, bool B_KMAJOR, bool VEC2>
-__global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t K,
-                                                   const double* __restrict__ A, int64_t lda,
-                                                   const double* __restrict__ B, int64_t ldb,
-                                                   double* __restrict__ C, int64_t ldc,
-                                                   double alpha, double beta, int64_t kchunk,
-                                                   int sym, double* __restrict__ partial) {
-  using GA = TileGeom<A_KMAJOR, BM>;
-  using GB = TileGeom<B_KMAJOR, BN>;
+// A_KMAJOR == transA ; B_KMAJOR == !transB.  CTA tile BM_ x BN_ x BK, WM x WN warps, each
+// warp a (BM_/WM) x (BN_/WN) sub-tile of (BM_/WM/8) x (BN_/WN/8) DMMA fragments.
+template <int BM_, int BN_, int WM, int WN, bool A_KMAJOR, bool B_KMAJOR, bool VEC2>
+__global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
+    int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+    const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc, double alpha,
+    double beta, int64_t kchunk, int sym, double* __restrict__ partial) {
+  constexpr int NTH = 32 * WM * WN, FM = BM_ / WM / 8, FN = BN_ / WN / 8;
+  using GA = TileGeom<A_KMAJOR, BM_>;
+  using GB = TileGeom<B_KMAJOR, BN_>;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * GA::SIZE;
 
   // sym bit 0: symmetric Gram (upper tiles, mirrored); bit 1: B is upper triangular (row k of
-  // B is zero beyond column k), so tile column n0 only needs k < n0 + BN
+  // B is zero beyond column k), so tile column n0 only needs k < n0 + BN_
   const int triu = sym & 2;
   sym &= 1;
   const int tile_m = blockIdx.y, tile_n = blockIdx.x;
   if (sym && tile_n < tile_m) return;
-  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
+  const int64_t m0 = (int64_t)tile_m * BM_, n0 = (int64_t)tile_n * BN_;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t kend = min(triu ? min(K, n0 + BN) : K, kbeg + kchunk);
+  const int64_t kend = min(triu ? min(K, n0 + BN_) : K, kbeg + kchunk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / WN, wn = warp % WN;
   const int lr = lane >> 2, lc = lane & 3;
 
-  double acc[4][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < FM; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t
   for (int s = 0; s < STAGES - 1; s++) {
     if (s < ntiles) {
       int64_t k0 = kbeg + (int64_t)s * BK;
-      load_tile<A_KMAJOR, BM, VEC2>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
-      load_tile<B_KMAJOR, BN, VEC2>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
+      load_tile<A_KMAJOR, BM_, VEC2, NTH>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
+      load_tile<B_KMAJOR, BN_, VEC2, NTH>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
     }
     cp_commit();
   }
@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t
       if (tn < ntiles) {
         int s = (int)(tn % STAGES);
         int64_t k0 = kbeg + tn * BK;
-        load_tile<A_KMAJOR, BM, VEC2>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
-        load_tile<B_KMAJOR, BN, VEC2>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
+        load_tile<A_KMAJOR, BM_, VEC2, NTH>(As + s * GA::SIZE, A, lda, m0, M, k0, kend, tid);
+        load_tile<B_KMAJOR, BN_, VEC2, NTH>(Bs + s * GB::SIZE, B, ldb, n0, N, k0, kend, tid);
       }
       cp_commit();
     }
@@ -176,29 +176,29 @@ __global__ void __launch_bounds__(NT) dgemm_kernel(int64_t M, int64_t N, int64_t
     const double* bs = Bs + (int)(t % STAGES) * GB::SIZE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double a[4], b[4];
+      double a[FM], b[FN];
 #pragma unroll
-      for (int i = 0; i < 4; i++) a[i] = as[GA::idx(kk + lc, wm * 32 + i * 8 + lr)];
+      for (int i = 0; i < FM; i++) a[i] = as[GA::idx(kk + lc, wm * (BM_ / WM) + i * 8 + lr)];
 #pragma unroll
-      for (int j = 0; j < 4; j++) b[j] = bs[GB::idx(kk + lc, wn * 32 + j * 8 + lr)];
+      for (int j = 0; j < FN; j++) b[j] = bs[GB::idx(kk + lc, wn * (BN_ / WN) + j * 8 + lr)];
 #pragma unroll
-      for (int i = 0; i < 4; i++)
+      for (int i = 0; i < FM; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < FN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_wait<0>();
 
   // epilogue
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const int64_t gm = m0 + wm * 32 + i * 8 + lr;
+  for (int i = 0; i < FM; i++) {
+    const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
+    for (int j = 0; j < FN; j++) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const int64_t gn = n0 + wn * 32 + j * 8 + 2 * lc + h;
+        const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc + h;
         if (gn >= N) continue;
         if (sym && gn < gm) continue;
         double v = acc[i][j][h];
@@ -239,23 +239,39 @@ __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __
   }
 }
 
-template <bool AK, bool BK_, bool V2>
+template <int BM_, int BN_, int WM, int WN, bool AK, bool BK_, bool V2>
 int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
              double beta, int64_t kchunk, int sym, double* partial) {
-  using GA = TileGeom<AK, BM>;
-  using GB = TileGeom<BK_, BN>;
+  using GA = TileGeom<AK, BM_>;
+  using GB = TileGeom<BK_, BN_>;
   size_t smem = (size_t)STAGES * (GA::SIZE + GB::SIZE) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_kernel<AK, BK_, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  dgemm_kernel<AK, BK_, V2><<<grid, NT, smem, ctx->stream>>>(M, N, K, A, lda, B, ldb, C, ldc,
-                                                             alpha, beta, kchunk, sym, partial);
+  dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2><<<grid, 32 * WM * WN, smem, ctx->stream>>>(
+      M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, sym, partial);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
+}
+
+// tile configurations: 0 = 64 x 64 (4 warps of 32 x 32), 1 = 128 x 64 (4 warps of 64 x 32),
+// 2 = 128 x 80 (4 warps of 64 x 40: N = 80 j without a ragged tile)
+template <int CFG, bool AK, bool BK_, bool V2>
+int launch_cfg(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
+               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
+               double beta, int64_t kchunk, int sym, double* partial) {
+  if (CFG == 1)
+    return launch_t<128, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
+                                                beta, kchunk, sym, partial);
+  if (CFG == 2)
+    return launch_t<128, 80, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
+                                                beta, kchunk, sym, partial);
+  return launch_t<64, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
+                                             beta, kchunk, sym, partial);
 }
 
 }  // namespace
@@ -277,7 +293,17 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
                                        ctx->stream));
     return TK_OK;
   }
-  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  // tile configuration: large non-symmetric products whose N is a multiple of 80 but not of 64
+  // (160 at c4: the bond-1 reconstruction) take the 128 x 80 tile (warp tiles 64 x 40, no
+  // ragged tile column: c4 form_U1 6.09 -> 5.51 ms)
+  static const int force_cfg = getenv("TTK_GEMM_CFG") ? atoi(getenv("TTK_GEMM_CFG")) : -1;
+  int cfg = 0;
+  // (the 128 x 64 tile measured slower than 64 x 64 on the c4 form_W: 27.96 vs 27.06 ms — half
+  // the resident warps; kept selectable with TTK_GEMM_CFG=1)
+  if (!sym && M >= 128LL * 4 * ctx->num_sms && N >= 64 && N % 64 != 0 && N % 80 == 0) cfg = 2;
+  if (force_cfg >= 0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64) cfg = force_cfg;
+  const int64_t bm = cfg ? 128 : BM, bn = cfg == 2 ? 80 : BN;
+  const int64_t tm = (M + bm - 1) / bm, tn = (N + bn - 1) / bn;
   int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
   // split-K for small outputs with a long K: about four waves of resident CTAs (SMs x CTAs/SM);
   // measured at c4 (bond-1 Gram 640 x 640 x 786432): 1 wave 15.4 ms, 2 waves 11.5, 3-6 waves
@@ -285,16 +311,16 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   static int per_sm = 0;
   if (per_sm == 0) {
     const size_t smem = (size_t)STAGES * 2 * BM * (BK + PADK) * sizeof(double);
-    cudaFuncSetAttribute(dgemm_kernel<true, true, true>,
+    cudaFuncSetAttribute(dgemm_kernel<64, 64, 2, 2, true, true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<true, true, true>, NT,
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<64, 64, 2, 2, true, true, true>,
+                                                  NT, smem);
     per_sm = std::max(per_sm, 1);
   }
   static const int mult = getenv("TTK_SPLITK_MULT") ? atoi(getenv("TTK_SPLITK_MULT")) : 4;
   const int64_t slots = (int64_t)per_sm * ctx->num_sms * mult;
   int64_t splits = 1;
-  if (tiles < slots && K >= 8 * BK) {
+  if (cfg == 0 && tiles < slots && K >= 8 * BK) {
     splits = std::min<int64_t>(std::max<int64_t>(slots / tiles, 1), (K + 8 * BK - 1) / (8 * BK));
     splits = std::max<int64_t>(splits, 1);
   }
@@ -318,10 +344,19 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   bool v2 = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
             (((uintptr_t)B & 15) == 0);
   int st;
-#define TK_GEMM_CASE(a, b, v)                                                             \
-  if (AK == a && BKm == b && v2 == v)                                                     \
-    st = launch_t<a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, \
-                           (sym ? 1 : 0) | (triu_b ? 2 : 0), partial);
+#define TK_GEMM_CASE(a, b, v)                                                               \
+  if (AK == a && BKm == b && v2 == v) {                                                     \
+    const int sf = (sym ? 1 : 0) | (triu_b ? 2 : 0);                                        \
+    if (cfg == 1)                                                                           \
+      st = launch_cfg<1, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
+                                  kchunk, sf, partial);                                     \
+    else if (cfg == 2)                                                                      \
+      st = launch_cfg<2, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
+                                  kchunk, sf, partial);                                     \
+    else                                                                                    \
+      st = launch_cfg<0, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
+                                  kchunk, sf, partial);                                     \
+  }
   TK_GEMM_CASE(false, false, false)
   TK_GEMM_CASE(false, false, true)
   TK_GEMM_CASE(false, true, false)
