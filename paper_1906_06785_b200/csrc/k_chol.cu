@@ -461,7 +461,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
       const int jb = std::min(NBR, n - j0);
       if (j0 + jb < n)
         TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
-                        Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true));
+                        Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true, false, state + 1));
     }
     return TK_OK;
   }
@@ -486,7 +486,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     if (j0 + jb < n) {
       // Hw -= Ro[j0:j0+jb, :]^T Ro[j0:j0+jb, :]   (rows of a stopped panel are zero: no-op)
       TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
-                      Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true));
+                      Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true, false, state + 1));
     }
   }
   return TK_OK;

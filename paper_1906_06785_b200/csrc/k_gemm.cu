@@ -118,8 +118,10 @@ template <int BM_, int BN_, int WM, int WN, bool A_KMAJOR, bool B_KMAJOR, bool V
 __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
     int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
     const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc, double alpha,
-    double beta, int64_t kchunk, int sym, double* __restrict__ partial) {
+    double beta, int64_t kchunk, int sym, double* __restrict__ partial,
+    const int* __restrict__ skip) {
   constexpr int NTH = 32 * WM * WN, FM = BM_ / WM / 8, FN = BN_ / WN / 8;
+  if (skip && *skip) return;  // device-side no-op flag (a finished pivoted Cholesky)
   using GA = TileGeom<A_KMAJOR, BM_>;
   using GB = TileGeom<B_KMAJOR, BN_>;
   extern __shared__ __align__(16) double smem[];
@@ -221,7 +223,8 @@ __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
 
 __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ P,
                               double* __restrict__ C, int64_t ldc, double alpha, double beta,
-                              int sym) {
+                              int sym, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   int64_t total = M * N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -242,7 +245,7 @@ __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __
 template <int BM_, int BN_, int WM, int WN, bool AK, bool BK_, bool V2>
 int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
-             double beta, int64_t kchunk, int sym, double* partial) {
+             double beta, int64_t kchunk, int sym, double* partial, const int* skip) {
   using GA = TileGeom<AK, BM_>;
   using GB = TileGeom<BK_, BN_>;
   size_t smem = (size_t)STAGES * (GA::SIZE + GB::SIZE) * sizeof(double);
@@ -253,7 +256,7 @@ int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const doub
     attr_set = true;
   }
   dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2><<<grid, 32 * WM * WN, smem, ctx->stream>>>(
-      M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, sym, partial);
+      M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, sym, partial, skip);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
@@ -263,22 +266,22 @@ int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const doub
 template <int CFG, bool AK, bool BK_, bool V2>
 int launch_cfg(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
-               double beta, int64_t kchunk, int sym, double* partial) {
+               double beta, int64_t kchunk, int sym, double* partial, const int* skip) {
   if (CFG == 1)
     return launch_t<128, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                                beta, kchunk, sym, partial);
+                                                beta, kchunk, sym, partial, skip);
   if (CFG == 2)
     return launch_t<128, 80, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                                beta, kchunk, sym, partial);
+                                                beta, kchunk, sym, partial, skip);
   return launch_t<64, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                             beta, kchunk, sym, partial);
+                                             beta, kchunk, sym, partial, skip);
 }
 
 }  // namespace
 
 int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-             double beta, double* C, int64_t ldc, bool sym, bool triu_b) {
+             double beta, double* C, int64_t ldc, bool sym, bool triu_b, const int* skip) {
   if (M <= 0 || N <= 0) return TK_OK;
   if (sym && M != N) {
     ctx->err = "tk_dgemm: sym requires M == N";
@@ -349,13 +352,13 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
     const int sf = (sym ? 1 : 0) | (triu_b ? 2 : 0);                                        \
     if (cfg == 1)                                                                           \
       st = launch_cfg<1, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
-                                  kchunk, sf, partial);                                     \
+                                  kchunk, sf, partial, skip);                                     \
     else if (cfg == 2)                                                                      \
       st = launch_cfg<2, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
-                                  kchunk, sf, partial);                                     \
+                                  kchunk, sf, partial, skip);                                     \
     else                                                                                    \
       st = launch_cfg<0, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
-                                  kchunk, sf, partial);                                     \
+                                  kchunk, sf, partial, skip);                                     \
   }
   TK_GEMM_CASE(false, false, false)
   TK_GEMM_CASE(false, false, true)
@@ -371,7 +374,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
     int64_t total = M * N;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * ctx->num_sms);
     splitk_reduce<<<blocks, 256, 0, ctx->stream>>>(M, N, (int)splits, partial, C, ldc, alpha,
-                                                   beta, sym ? 1 : 0);
+                                                   beta, sym ? 1 : 0, skip);
     TK_LAUNCH_CHECK(ctx);
   }
   tk_prof_end(ctx, prof_id);

@@ -176,9 +176,11 @@ struct DevBuf {
 //        computed and mirrored.  Split-K with a deterministic reduction is chosen internally.
 //   triu_b: op(B) is upper triangular (K x N, zero below the diagonal): each tile column skips
 //        the zero K range.
+//   skip (nullable, device int): the launch is a no-op when *skip != 0 (read by every CTA).
 int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-             double beta, double* C, int64_t ldc, bool sym = false, bool triu_b = false);
+             double beta, double* C, int64_t ldc, bool sym = false, bool triu_b = false,
+             const int* skip = nullptr);
 
 // Symmetric eigen-decomposition by parallel cyclic two-sided Jacobi.
 //   A: n x n symmetric (device, row-major, ld = n), destroyed.
