@@ -83,8 +83,12 @@ extern "C" int tk_ctx_create(tk_ctx** out, void* stream) {
 }
 
 int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
+  // highest priority, like ctx->crit: the QR's trailing updates are on the critical path and
+  // must not queue behind the side stream's big GEMMs
+  int lo = 0, hi = 0;
+  TK_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
   for (auto& s : ctx->aux)
-    if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
   while (ctx->fork_ev.size() < n_events) {
     cudaEvent_t e;
     TK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
