@@ -627,28 +627,44 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
 // W = Z V (M x k) and its Gram GW = W^T W.  pass2() finishes: lam (k, descending
 // eigenvalues of GW = squared singular values of Z), V2 (k x k), Vt = V V2.
 // floor (out, 1 device double): rounding-noise level of G_W entries for pass 2's skip test.
+// Stride of the bond-1 pass-1 row sample (>= 8R rows, s <= 16).
+static int64_t pass1_stride(int64_t M, int64_t R) {
+  static const bool full = getenv("TTK_FULL_PASS1_GRAM") != nullptr;
+  return full ? 1 : std::max<int64_t>(1, std::min<int64_t>(16, M / (8 * R)));
+}
+// The sampled pass-1 Gram Y_s^T Y_s (R x R) of bond 1.
+static int pass1_gram(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, double* GY) {
+  const int64_t s = pass1_stride(M, R);
+  TagScope t(ctx, "bond1.gram_Y");
+  return tk_dgemm(ctx, true, false, R, R, (M + s - 1) / s, 1.0, Y, R * s, Y, R * s, 0.0, GY, R,
+                  true);
+}
+
+// gy_pre (nullable): the sampled Gram of Y, already computed (pass1_gram; tk_apply_round
+// computes it on the side stream right after the SpMM).
 int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const double* Lm,
-                 int64_t k, DevBuf& W, DevBuf& GW, DevBuf& V, DevBuf& floor) {
+                 int64_t k, DevBuf& W, DevBuf& GW, DevBuf& V, DevBuf& floor,
+                 const double* gy_pre = nullptr) {
   DevBuf GY, GZ, T1, P, lam;
   TK_TRY(GZ.get(ctx, k * k));
   TK_TRY(floor.get(ctx, 1));
   int64_t s = 1;
+  const double* gy = nullptr;
   TagScope tag0(ctx, Lm ? "bond1.small" : "bond2.small");
   if (Lm) {
-    TK_TRY(GY.get(ctx, R * R));
-    {
-      // Pass 1 only has to supply an orthogonal basis that roughly follows the dominant
-      // directions (accuracy comes from pass 2 on the explicit W), so its Gram is taken over
-      // a strided sample of >= 8R rows (every s-th spatial row, s <= 16): 1/s of the flops
-      // with the same pass-2 convergence.
-      static const bool full = getenv("TTK_FULL_PASS1_GRAM") != nullptr;
-      s = full ? 1 : std::max<int64_t>(1, std::min<int64_t>(16, M / (8 * R)));
-      TagScope t(ctx, "bond1.gram_Y");
-      TK_TRY(tk_dgemm(ctx, true, false, R, R, (M + s - 1) / s, 1.0, Y, R * s, Y, R * s, 0.0, GY.p,
-                      R, true));
+    // Pass 1 only has to supply an orthogonal basis that roughly follows the dominant
+    // directions (accuracy comes from pass 2 on the explicit W), so its Gram is taken over
+    // a strided sample of >= 8R rows (every s-th spatial row, s <= 16): 1/s of the flops
+    // with the same pass-2 convergence.
+    s = pass1_stride(M, R);
+    gy = gy_pre;
+    if (!gy) {
+      TK_TRY(GY.get(ctx, R * R));
+      TK_TRY(pass1_gram(ctx, M, R, Y, GY.p));
+      gy = GY.p;
     }
     TK_TRY(T1.get(ctx, R * k));
-    TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, GY.p, R, Lm, k, 0.0, T1.p, k));
+    TK_TRY(tk_dgemm(ctx, false, false, R, k, R, 1.0, gy, R, Lm, k, 0.0, T1.p, k));
     TK_TRY(tk_dgemm(ctx, true, false, k, k, R, 1.0, Lm, k, T1.p, k, 0.0, GZ.p, k));
     TK_TRY(tk_symmetrize(ctx, k, GZ.p));
   } else {
@@ -665,7 +681,7 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
     TK_TRY(tk_dgemm(ctx, false, false, R, k, k, 1.0, Lm, k, V.p, k, 0.0, P.p, k));
     PV = P.p;
     // ||Y||_F^2 ~ s * trace(sampled Gram); P = L V
-    TK_TRY(tk_noise_floor(ctx, GY.p, R, (double)s, P.p, R * k, R, k, floor.p));
+    TK_TRY(tk_noise_floor(ctx, gy, R, (double)s, P.p, R * k, R, k, floor.p));
   } else {
     TK_TRY(tk_noise_floor(ctx, GZ.p, k, 1.0, nullptr, 0, R, k, floor.p));  // P = V orthogonal
   }
@@ -853,7 +869,8 @@ int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
 // size rb1 x n_xi x rb2, packed in y2blk (the fused apply+round); x->U2 is then output only.
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                       double* sigma2_out, double* discarded_out, double* norm_out,
-                      const double* y2blk = nullptr, int64_t rb1 = 0, int64_t rb2 = 0);
+                      const double* y2blk = nullptr, int64_t rb1 = 0, int64_t rb2 = 0,
+                      const double* gy_pre = nullptr);
 
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
@@ -891,6 +908,12 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   static const bool serial = getenv("TTK_SERIAL") != nullptr;
   CritScope cs(ctx);  // (declared before every buffer below: joins back after they are freed)
   TK_TRY(apply_space_time(ctx, op, x, y, !serial));
+  DevBuf gyb;  // bond 1's sampled pass-1 Gram, also on the side stream behind the SpMM
+  if (!serial) {
+    OnSide on(ctx);
+    TK_TRY(gyb.get(ctx, R1 * R1));
+    TK_TRY(pass1_gram(ctx, op->n_x, R1, y->U1, gyb.p));
+  }
   SideJoin sj(ctx, !serial);  // (round_impl joins before bond 1; this covers early returns)
   DevBuf blk;
   TK_TRY(blk.get(ctx, R1 * x->n_xi * x->r2));
@@ -910,7 +933,7 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   y->r1 = R1;
   y->r2 = R2;
   const int st = round_impl(ctx, y, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out,
-                            blk.p, x->r1, x->r2);
+                            blk.p, x->r1, x->r2, gyb.p);
   blk.release();
   pool_settle(ctx);
   return st;
@@ -918,7 +941,7 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
 
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                       double* sigma2_out, double* discarded_out, double* norm_out,
-                      const double* y2blk, int64_t rb1, int64_t rb2) {
+                      const double* y2blk, int64_t rb1, int64_t rb2, const double* gy_pre) {
   TK_TRY(check_tt(ctx, x, "tk_round"));
   if (!(tol >= 0.0) || !std::isfinite(tol)) {
     ctx->err = "tk_round: tol must be finite and >= 0";
@@ -967,7 +990,7 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
   TK_TRY(tk_side_join(ctx));  // U1 written by a side-stream SpMM (tk_apply_round)
   DevBuf W, GW1, V1, V2, Vt, lam, fl1;
-  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1, fl1));
+  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1, fl1, gy_pre));
   DevBuf sig1, scr;
   TK_TRY(scr.get(ctx, 16));
   int* info1 = (int*)scr.p;
