@@ -191,7 +191,37 @@ __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
   }
   cp_wait<0>();
 
-  // epilogue
+  // epilogue.  Fast path (no symmetric mirror, N and ldc even, C 16-byte aligned): each lane's
+  // two adjacent outputs as one 16-byte store (the scalar stores stalled on the LSU: 17 % of the
+  // form_W warp samples sat in the epilogue)
+  const bool vec_out = !sym && (N % 2 == 0) &&
+                       (partial ? true : ((ldc % 2 == 0) && (((uintptr_t)C & 15) == 0)));
+  if (vec_out) {
+#pragma unroll
+    for (int i = 0; i < FM; i++) {
+      const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int j = 0; j < FN; j++) {
+        const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc;
+        if (gn >= N) continue;
+        if (partial) {
+          *(double2*)(partial + ((int64_t)blockIdx.z * M + gm) * N + gn) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          double2 o = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+          double2* cp = (double2*)(C + gm * ldc + gn);
+          if (beta != 0.0) {
+            const double2 c = *cp;
+            o.x += beta * c.x;
+            o.y += beta * c.y;
+          }
+          *cp = o;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < FM; i++) {
     const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
