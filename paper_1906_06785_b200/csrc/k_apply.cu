@@ -162,8 +162,12 @@ __global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm
 // entries are still summed in ascending column order, as in each term's sorted CSR row (the
 // zero padding adds exact zeros).  The row's T r outputs are streamed once at the end.
 //
-// Each row is ONE contiguous record in `rec` (int64 words): [gn][gn words col | mask << 32]
-// [values as doubles], at rec + recptr[i].  The row loop is software-pipelined: while row i is
+// Each row is ONE contiguous record in `rec` (int64 words): [row | gn << 32][gn words
+// col | mask << 32][values as doubles], at rec + recptr[i].  Record i is NOT row i: the host
+// stores the rows in a breadth-first (Cuthill-McKee) order of the merged pattern, so rows that
+// gather the same U1 rows (at c4 a velocity row and the pressure rows it couples to, 2 N^2
+// apart in the natural order) are processed at the same time and U1 is read from DRAM about
+// once instead of twice.  The row loop is software-pipelined: while row i is
 // computed, the record of the warp's next row (RW words per lane, one coalesced load) and the
 // record pointer of the row after it are already in flight, so the dependent global loads
 // (pointer -> record) leave the critical path; only the U1 row gathers (L2) remain on it.
@@ -224,7 +228,8 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
 #pragma unroll
     for (int m = 0; m < RW; m++) rs[lane + 32 * m] = cur[m];
     __syncwarp();
-    const int gn = (int)rs[0];
+    const int gn = (int)(rs[0] >> 32);
+    const int64_t row = (int64_t)(rs[0] & 0xffffffffLL);  // records are in locality order
     const long long w = lane < gn ? rs[1 + lane] : 0LL;
     const unsigned mask = (unsigned)(w >> 32);
     const int cnt = __popc(mask);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
       cols[lane] = lane < gn ? (int)(w & 0xffffffffLL) : 0;
     }
     __syncwarp();
-    double* yrow = Y1 + i * R;
+    double* yrow = Y1 + row * R;
     for (int c0 = 0; c0 < r; c0 += CW) {
       const int cc = c0 + (V2 ? 2 * lane : lane);
       const bool okc = cc < r;

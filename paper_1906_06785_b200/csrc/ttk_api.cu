@@ -242,11 +242,13 @@ static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
                         const int32_t* const* K_col, const double* const* K_val) {
   const int T = op->T;
   const int64_t n_x = op->n_x;
-  std::vector<int64_t> recptr(n_x + 1, 0), rec, words;
-  std::vector<double> vals;
+  if (n_x >= ((int64_t)1 << 31)) return TK_OK;
+  // merged per-row lists (distinct columns with term masks, values in (column, term) order)
+  std::vector<int64_t> wptr(n_x + 1, 0), vptr(n_x + 1, 0), words, vals_all;
   int64_t tot = 0;
   for (int k = 0; k < T; k++) tot += K_rowptr[k][n_x];
-  rec.reserve(tot + tot / 4 + 2 * n_x + 16);
+  words.reserve(tot / 2 + 16);
+  vals_all.reserve(tot);
   struct E {
     int32_t c;
     int32_t k;
@@ -255,8 +257,6 @@ static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
   std::vector<E> ents;
   for (int64_t i = 0; i < n_x; i++) {
     ents.clear();
-    words.clear();
-    vals.clear();
     for (int k = 0; k < T; k++)
       for (int32_t p = K_rowptr[k][i]; p < K_rowptr[k][i + 1]; p++)
         ents.push_back({K_col[k][p], k, K_val[k][p]});
@@ -272,20 +272,64 @@ static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
         double v = 0.0;
         while (q < ents.size() && ents[q].c == c && ents[q].k == k) v += ents[q++].v;
         mask |= 1u << k;
-        vals.push_back(v);
+        int64_t b;
+        memcpy(&b, &v, sizeof(b));
+        vals_all.push_back(b);
       }
       words.push_back((int64_t)(uint32_t)c | ((int64_t)mask << 32));
     }
+    wptr[i + 1] = (int64_t)words.size();
+    vptr[i + 1] = (int64_t)vals_all.size();
     // the merged kernel keeps one row's distinct columns in one warp's lanes
-    if (words.size() > 32) return TK_OK;  // per-term kernel for this operator
-    rec.push_back((int64_t)words.size());
-    rec.insert(rec.end(), words.begin(), words.end());
-    for (double v : vals) {
-      int64_t b;
-      memcpy(&b, &v, sizeof(b));
-      rec.push_back(b);
+    if (wptr[i + 1] - wptr[i] > 32) return TK_OK;  // per-term kernel for this operator
+  }
+  // processing order: breadth-first over the symmetrised merged pattern (Cuthill-McKee, no
+  // reversal), each component from its lowest unvisited row
+  std::vector<int32_t> order;
+  order.reserve(n_x);
+  {
+    std::vector<int64_t> tptr(n_x + 1, 0);
+    for (int64_t i = 0; i < n_x; i++)
+      for (int64_t w = wptr[i]; w < wptr[i + 1]; w++) tptr[(words[w] & 0xffffffffLL) + 1]++;
+    for (int64_t i = 0; i < n_x; i++) tptr[i + 1] += tptr[i];
+    std::vector<int32_t> tcol(tptr[n_x]);
+    std::vector<int64_t> fill(tptr.begin(), tptr.end() - 1);
+    for (int64_t i = 0; i < n_x; i++)
+      for (int64_t w = wptr[i]; w < wptr[i + 1]; w++)
+        tcol[fill[words[w] & 0xffffffffLL]++] = (int32_t)i;
+    std::vector<char> seen(n_x, 0);
+    std::vector<int32_t> nb;
+    for (int64_t s0 = 0; s0 < n_x; s0++) {
+      if (seen[s0]) continue;
+      seen[s0] = 1;
+      size_t head = order.size();
+      order.push_back((int32_t)s0);
+      while (head < order.size()) {
+        const int32_t u = order[head++];
+        nb.clear();
+        for (int64_t w = wptr[u]; w < wptr[u + 1]; w++) nb.push_back((int32_t)(words[w] & 0xffffffffLL));
+        for (int64_t t = tptr[u]; t < tptr[u + 1]; t++) nb.push_back(tcol[t]);
+        std::sort(nb.begin(), nb.end());
+        for (int32_t v : nb)
+          if (!seen[v]) {
+            seen[v] = 1;
+            order.push_back(v);
+          }
+      }
     }
-    recptr[i + 1] = (int64_t)rec.size();
+  }
+  static const bool natural = getenv("TTK_SPMM_NATURAL") != nullptr;
+  if (natural)
+    for (int64_t i = 0; i < n_x; i++) order[i] = (int32_t)i;
+  std::vector<int64_t> recptr(n_x + 1, 0), rec;
+  rec.reserve(words.size() + vals_all.size() + n_x + 16);
+  for (int64_t pos = 0; pos < n_x; pos++) {
+    const int64_t i = order[pos];
+    const int64_t gn = wptr[i + 1] - wptr[i];
+    rec.push_back(i | (gn << 32));
+    rec.insert(rec.end(), words.begin() + wptr[i], words.begin() + wptr[i + 1]);
+    rec.insert(rec.end(), vals_all.begin() + vptr[i], vals_all.begin() + vptr[i + 1]);
+    recptr[pos + 1] = (int64_t)rec.size();
   }
   auto up = [&](void** d, const void* h, size_t b) -> int {
     TK_CUDA_TRY(ctx, cudaMalloc(d, b ? b : 8));
