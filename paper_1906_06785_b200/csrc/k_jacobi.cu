@@ -715,7 +715,7 @@ int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lsk
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev,
                   double rs_tol, int64_t rs_rmax, const double* abs_floor_dev, const double* V0,
-                  int mv) {
+                  int mv, double stop_rel) {
   if (n <= 0) return TK_OK;
   const int n_pad = ((n + JS - 1) / JS) * JS;
   if (!V0) mv = n;
@@ -773,7 +773,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   a.offmax = offmax;
   // relative mode: a sweep whose largest applied relative coupling is <= 1e-10 leaves
   // couplings of O(1e-20) behind (quadratic convergence): stop after it
-  a.stop_rel = rel_tol > 0.0 ? 1e-10 : 0.0;
+  a.stop_rel = rel_tol > 0.0 ? (stop_rel > 0.0 ? stop_rel : 1e-10) : 0.0;
   static const bool dbg = getenv("TTK_DEBUG") != nullptr;
   DevBuf tsb;
   a.tstamp = nullptr;

@@ -772,7 +772,8 @@ int cholqr_pass(tk_ctx* ctx, int64_t rows, int64_t c, const double* A, double* Q
 int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, DevBuf& lam,
                DevBuf& V2) {
   // small problems: one plain Jacobi (a single 64-wide block pair) is cheaper than two
-  if (k > tk_pchol_max_n() || k <= 128) return TK_EARG;
+  static const int64_t min_k = getenv("TTK_PASS2_CHOL_MIN") ? atoi(getenv("TTK_PASS2_CHOL_MIN")) : 64;
+  if (k > tk_pchol_max_n() || k <= min_k) return TK_EARG;
   TagScope tag(ctx, "pass2_chol");
   DevBuf Ro, pv, st, rem, X, V0, Y, nrm, V1, Qv, T1, Gp, lam2, V2p;
   TK_TRY(Ro.get(ctx, k * k));
@@ -791,8 +792,11 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
   Ro.release();
   TK_TRY(lam2.get(ctx, kc));
   TK_TRY(Y.get(ctx, k * kc));
+  // (the refinement Jacobi of step (3) restores the full accuracy, so this one may stop as
+  // soon as the couplings are small: its last, confirming sweep is left to the refinement)
+  static const double stop1 = getenv("TTK_PASS2_STOP1") ? atof(getenv("TTK_PASS2_STOP1")) : 1e-3;
   TK_TRY(tk_jacobi_eig(ctx, kc, X.p, lam2.p, Y.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
-                       nullptr, nullptr, 0.0, 0, floor, V0.p, (int)k));
+                       nullptr, nullptr, 0.0, 0, floor, V0.p, (int)k, stop1));
   TK_TRY(nrm.get(ctx, kc));
   TK_TRY(tk_col_norms(ctx, k, kc, Y.p, kc, nrm.p));
   TK_TRY(V1.get(ctx, k * kc));

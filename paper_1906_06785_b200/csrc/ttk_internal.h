@@ -193,11 +193,14 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 //   Out: [0] effective threshold, [1] bound on the unresolved block's largest eigenvalue.
 //   V0 (nullable, mv x n row-major): the rotations are accumulated onto V0 instead of the
 //   identity, and V (mv x n) returns V0 J with columns permuted like lam.
+//   stop_rel (> 0): stop after a sweep whose largest rotated relative coupling is <= stop_rel
+//   (default 1e-10).
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev = nullptr,
                   double rs_tol = 0.0, int64_t rs_rmax = 0,
                   const double* abs_floor_dev = nullptr, const double* V0 = nullptr,
-                  int mv = 0);
+                  int mv = 0,
+                  double stop_rel = 0.0);
 // Rounding-noise floor of a pass-2 Gram W^T W with W = fl(Y P) (K = inner dimension, k = its
 // columns): tau = (4 eps)^2 K (trG_scale * trG[0]) ||P||_F^2 / k, written to out[0] (device).
 // P == nullptr means an orthogonal P (||P||_F^2 = k).
