@@ -52,3 +52,32 @@ def g_by_quadrature(indices, m: int, p: int) -> list[np.ndarray]:
 def gauss_legendre_nodes(q: int) -> np.ndarray:
     """Roots of P_q (library routine), for the m = 1 eigenvalue pin."""
     return npleg.leggauss(q)[0]
+
+
+def h_by_quadrature(indices, m: int, p: int) -> list[np.ndarray]:
+    """[H_l]_rs = <psi_l psi_r psi_s> for every multi-index l (PAPER.md:132 with the random field
+    expanded in the chaos basis, as eq:N_kron PAPER.md:327 uses it), by tensorised
+    Gauss-Legendre quadrature: each 1-D integrand has degree <= 3p, q = (3p)//2 + 2 points are
+    exact."""
+    q = (3 * p) // 2 + 2
+    x, w = npleg.leggauss(q)
+    w = w / 2.0
+    xi = math.sqrt(3.0) * x
+    psi = [_psi_1d(a, xi) for a in range(p + 1)]
+    t1 = np.zeros((p + 1, p + 1, p + 1))
+    for a in range(p + 1):
+        for b in range(p + 1):
+            for c in range(p + 1):
+                t1[a, b, c] = np.sum(w * psi[a] * psi[b] * psi[c])
+    n = len(indices)
+    out = []
+    for lam in indices:
+        h = np.zeros((n, n))
+        for r, al in enumerate(indices):
+            for s, be in enumerate(indices):
+                v = 1.0
+                for d in range(m):
+                    v *= t1[lam[d], al[d], be[d]]
+                h[r, s] = v
+        out.append(h)
+    return out

@@ -1,4 +1,5 @@
-"""The five named configurations of BASELINE.json (``configs``), as read in DESIGN.md.
+"""The five named configurations of BASELINE.json (``configs``), as read in DESIGN.md, plus c6
+(NEXT-1: the TT convection operator, not a BASELINE.json config).
 
 c1..c4: apply + round on a seeded operator and input TT.  c5: one 20-step low-rank GMRES
 cycle on the c2 operator.  nu values for c3/c4 are unstated in BASELINE.json; the c2 rule
@@ -26,6 +27,8 @@ class Config:
     input_kind: str       # "gauss" (N(0,1) cores) or "decay" (0.7^i spectra)
     gmres_steps: int = 0  # c5 only
     rhs_ranks: tuple = field(default=(0, 0))
+    operator: str = "oseen"  # "convection": the TT convection operator N(u~) (NEXT-1, c6)
+    velocity_ranks: tuple = field(default=(0, 0))  # ranks of the velocity TT u~ (c6)
 
     @property
     def n_x(self) -> int:
@@ -33,6 +36,8 @@ class Config:
 
     @property
     def n_terms(self) -> int:
+        if self.operator == "convection":  # one term per (alpha_1, alpha_2), eq:N_kron
+            return self.velocity_ranks[0] * self.velocity_ranks[1]
         # time-mass + mean Oseen + m KL terms + (R_w - 1) wind terms (R8)
         return 2 + self.m + (self.wind_rank - 1)
 
@@ -48,6 +53,11 @@ CONFIGS = {
     "c4": Config("c4", 3, 512, 8, 3, 512, 1.0 / 512, _nus(8), 5, (64, 64), 1e-6, 160, "decay"),
     "c5": Config("c5", 4, 64, 4, 3, 64, 1.0 / 64, _nus(4), 1, (20, 20), 1e-6, 0, "decay",
                  gmres_steps=20, rhs_ranks=(8, 8)),
+    # NEXT-1, not a BASELINE.json config: apply + round of the TT convection
+    # operator N(u~) of eq:N_kron on the c2 sizes, u~ a seeded decaying
+    # velocity TT of ranks (4, 4) -> 16 terms, x the c2-style input (20, 20) -> (320, 320)
+    "c6": Config("c6", 5, 64, 4, 3, 64, 1.0 / 64, _nus(4), 1, (20, 20), 1e-8, 80, "decay",
+                 operator="convection", velocity_ranks=(4, 4)),
 }
 
 

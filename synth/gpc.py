@@ -63,3 +63,46 @@ def g_matrices(m: int, p: int) -> list[np.ndarray]:
             g[j, i] = v
         gs.append(g)
     return gs
+
+
+def _triple_1d(a: int, b: int, c: int) -> float:
+    """<psi_a psi_b psi_c> in one variable (psi_n = sqrt(2n+1) P_n(xi/sqrt3), xi ~ U[-sqrt3,
+    sqrt3]): sqrt((2a+1)(2b+1)(2c+1)) times E[P_a P_b P_c] = (a b c; 0 0 0)^2 (the squared
+    Wigner 3j symbol with zero projections; Adams/Neumann closed form):
+        s = a+b+c even, |a-b| <= c <= a+b, g = s/2:
+        (a b c; 0 0 0)^2 = (s-2a)! (s-2b)! (s-2c)! / (s+1)! * (g! / ((g-a)! (g-b)! (g-c)!))^2
+    and 0 otherwise."""
+    s = a + b + c
+    if s % 2 or c > a + b or c < abs(a - b):
+        return 0.0
+    g = s // 2
+    f = math.factorial
+    w2 = (f(s - 2 * a) * f(s - 2 * b) * f(s - 2 * c) / f(s + 1)) * \
+        (f(g) / (f(g - a) * f(g - b) * f(g - c))) ** 2
+    return math.sqrt((2 * a + 1) * (2 * b + 1) * (2 * c + 1)) * w2
+
+
+def h_matrices(m: int, p: int) -> list[np.ndarray]:
+    """[H_1, ..., H_{n_xi}] with [H_l]_{rs} = <psi_l psi_r psi_s> (the Galerkin
+    matrices of a random field expanded in the chaos basis itself, used by the TT convection
+    operator eq:N_kron PAPER.md:327), l in the multi_indices order; product of 1-D triple
+    products over the m variables.  H_1 = I (psi_1 = 1) and H_{e_i} = G_i (psi_{e_i} = xi_i)."""
+    idx = multi_indices(m, p)
+    n = len(idx)
+    t1 = {}
+    out = []
+    for lam in idx:
+        h = np.zeros((n, n))
+        for r, al in enumerate(idx):
+            for s_, be in enumerate(idx):
+                v = 1.0
+                for d in range(m):
+                    key = (lam[d], al[d], be[d])
+                    if key not in t1:
+                        t1[key] = _triple_1d(*key)
+                    v *= t1[key]
+                    if v == 0.0:
+                        break
+                h[r, s_] = v
+        out.append(h)
+    return out

@@ -57,3 +57,13 @@ def make_rhs_tt(cfg: Config, n_xi: int):
     rng = np.random.default_rng([cfg.index, 2])
     u1, u2, u3 = random_tt(rng, cfg.n_x, n_xi, cfg.n_t, cfg.rhs_ranks[0], cfg.rhs_ranks[1], "gauss")
     return u1 / np.linalg.norm(u1), u2 / np.linalg.norm(u2), u3 / np.linalg.norm(u3)
+
+
+def make_velocity_tt(cfg: Config, n_xi: int):
+    """c6 velocity u~ for the convection operator N(u~): decaying cores of ranks velocity_ranks
+    (the low-rank truncation T_eps_conv(u) of eq:eps_conv stands behind it),
+    scaled so the wind has O(1) magnitude on the grid."""
+    rng = np.random.default_rng([cfg.index, 3])
+    u1, u2, u3 = random_tt(rng, cfg.n_x, n_xi, cfg.n_t, cfg.velocity_ranks[0],
+                           cfg.velocity_ranks[1], "decay")
+    return u1 * np.sqrt(cfg.n_x / 3.0), u2 / np.linalg.norm(u2), u3 * np.sqrt(cfg.n_t)
