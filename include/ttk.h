@@ -152,6 +152,24 @@ int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps, doub
                    double* history_out, int* steps_done, double* explicit_out,
                    double* step_ms_out);
 
+/* Complete, restarted low-rank GMRES: Alg. 3 with
+ * P = I, restarted every `restart` Arnoldi steps with z_0 <- z, the stopping test
+ * ||s_k|| <= tol_gmres ||b|| (line 2) and the truncated solution update
+ * z <- T_eps_soln(z + sum_i y_i v_i) of eq:eps_soln; reading R19 of
+ * within a cycle the test uses the Givens least-squares residual, z_k and the
+ * explicit s_k = T_tol(b - A z_k) (lines 13-14) are formed at the end of each cycle.
+ *   tol        : truncation tolerance eps_gmres of every T (line 5, MGS, lines 10, 14)
+ *   eps_soln   : tolerance of the solution update (< 0: use tol)
+ *   z          : OUT, caller-owned TT with capacity (TK_ECAP if the solution's ranks exceed
+ *                it); mode sizes must be the operator's
+ *   explicit_out (HOST, max_cycles + 1): ||s_0|| = ||T(b)||, then ||s|| after every cycle
+ *   ls_out (HOST, nullable, max_cycles * (restart + 1)): per cycle the least-squares history
+ *   cycles_done (HOST), steps_out (HOST, nullable, max_cycles): Arnoldi steps per cycle.
+ * Blocking. */
+int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart, int max_cycles,
+                   double tol, double tol_gmres, double eps_soln, tk_tt* z, double* explicit_out,
+                   double* ls_out, int* cycles_done, int* steps_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@ Readings (R15):
   * least-squares residual |g_{k+1}| from Givens rotations of H-bar after every step (line 12)
   * breakdown when h_{k+1,k} <= 1e-14 ||T(L v_k)||
   * z = sum_i y_i v_i accumulated as z <- T(z + y_i v_i); explicit residual ||T(b - L z)||.
+gmres_solve: the complete, restarted Alg. 3 (NEXT-2; reading R19 in its docstring).
 """
 from __future__ import annotations
 
@@ -28,7 +29,11 @@ def givens(a: float, b: float):
     return a / r, b / r
 
 
-def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6):
+def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6, stop_abs: float = 0.0,
+                explicit: bool = True):
+    """One cycle.  stop_abs > 0: stop once the least-squares residual |g_{k+1}| <= stop_abs
+    (Alg. 3 line 2 with the Givens estimate, R19).  explicit=False skips the explicit
+    residual T(b - L z) (the restarted solver forms its own)."""
     s0 = tt.round_tt(b, tol)
     beta = tt.norm(s0)
     v = [tt.scale(1.0 / beta, s0)]
@@ -64,7 +69,7 @@ def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6):
         g[k] = c * g[k]
         hist.append(abs(g[k + 1]))
         k_done = k + 1
-        if hn <= 1e-14 * nav:
+        if hn <= 1e-14 * nav or hist[-1] <= stop_abs:
             break
         v.append(tt.scale(1.0 / hn, x))
         ranks.append(tt.ranks(v[-1]))
@@ -74,5 +79,34 @@ def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6):
     z = tt.scale(y[0], v[0])
     for i in range(1, k_done):
         z = tt.round_tt(tt.axpby(1.0, z, y[i], v[i]), tol)
+    if not explicit:
+        return dict(history=np.array(hist), explicit=None, y=y, z=z, ranks=ranks, steps=k_done)
     r = tt.round_tt(tt.axpby(1.0, b, -1.0, tt.apply_op(op, z)), tol)
     return dict(history=np.array(hist), explicit=tt.norm(r), y=y, z=z, ranks=ranks, steps=k_done)
+
+
+def gmres_solve(op, b, restart: int = 20, max_cycles: int = 5, tol: float = 1e-6,
+                tol_gmres: float = 1e-8, eps_soln: float | None = None):
+    """Complete low-rank GMRES (NEXT-2): Alg. 3 with P = I,
+    restarted every `restart` steps (z_0 <- z), the stopping test ||s_k|| <= tol_gmres ||b||
+    (line 2) and the truncated solution update of eq:eps_soln.  Reading
+    R19: inside a cycle the test uses the Givens least-squares residual; z_k (line 13, here
+    z <- T_eps_soln(z + sum_i y_i v_i)) and the explicit s_k = T(b - L z_k) (line 14) are formed
+    at the end of every cycle (and their norm decides the outer stop).  Returns the solution
+    TT, the explicit residual norms (s_0 first) and the per-cycle least-squares histories."""
+    eps_soln = tol if eps_soln is None else eps_soln
+    bnorm = tt.norm(b)
+    s = tt.round_tt(b, tol)  # z_0 = 0: s_0 = T(b)
+    explicit = [tt.norm(s)]
+    ls = []
+    z = None
+    for _cycle in range(max_cycles):
+        if explicit[-1] <= tol_gmres * bnorm:
+            break
+        res = gmres_cycle(op, s, restart, tol, stop_abs=tol_gmres * bnorm, explicit=False)
+        ls.append(res["history"])
+        dz = res["z"]
+        z = tt.round_tt(dz if z is None else tt.axpby(1.0, z, 1.0, dz), eps_soln)
+        s = tt.round_tt(tt.axpby(1.0, b, -1.0, tt.apply_op(op, z)), tol)
+        explicit.append(tt.norm(s))
+    return dict(z=z, explicit=np.array(explicit), ls=ls, cycles=len(ls))

@@ -1267,9 +1267,13 @@ int clone_tt(tk_ctx* ctx, const tk_tt* src, OwnedTT& dst) {
 
 }  // namespace
 
-extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps,
-                              double tol, double* history_out, int* steps_done,
-                              double* explicit_out, double* step_ms_out) {
+// One cycle (tk_gmres_cycle), plus what the restarted solver needs: stop once the Givens
+// least-squares residual is <= stop_abs (Alg. 3 line 2, R19) and hand back the
+// iterate z = sum_i y_i v_i (z_out, nullable) instead of / besides its explicit residual.
+static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps, double tol,
+                            double stop_abs, double* history_out, int* steps_done,
+                            double* explicit_out, double* step_ms_out,
+                            std::unique_ptr<OwnedTT>* z_out) {
   if (!ctx || !op || !history_out || !steps_done || steps < 1) return TK_EARG;
   TK_TRY(check_tt(ctx, b, "tk_gmres_cycle(b)"));
   if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t) {
@@ -1347,7 +1351,7 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     g[k] = c * g[k];
     history_out[k + 1] = std::fabs(g[k + 1]);
     k_done = k + 1;
-    bool breakdown = hn <= 1e-14 * nav;
+    bool breakdown = hn <= 1e-14 * nav || history_out[k + 1] <= stop_abs;
     if (!breakdown) {
       TK_TRY(tk_scale(ctx, &x->t, d_hn, 1));
       V.push_back(std::move(x));
@@ -1358,7 +1362,7 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     if (breakdown) break;
   }
   *steps_done = k_done;
-  if (explicit_out) {
+  if (explicit_out || z_out) {
     // y = R^{-1} g  (back substitution on the rotated H-bar)
     std::vector<double> y(k_done, 0.0);
     for (int i = k_done - 1; i >= 0; i--) {
@@ -1377,6 +1381,10 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
       TK_TRY(tk_round(ctx, &z2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
       z = std::move(z2);
     }
+    if (!explicit_out) {
+      *z_out = std::move(z);
+      return TK_OK;
+    }
     auto az = std::make_unique<OwnedTT>();
     TK_TRY(az->make(ctx, n_x, n_xi, n_t, T * z->t.r1, T * z->t.r2));
     TK_TRY(tk_apply_op(ctx, op, &z->t, &az->t));
@@ -1386,6 +1394,95 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     TK_TRY(tk_round(ctx, &r->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
     TK_TRY(tk_norm(ctx, &r->t, d_hn));
     TK_TRY(sync_read(ctx, explicit_out, d_hn, sizeof(double)));
+    if (z_out) *z_out = std::move(z);
   }
+  return TK_OK;
+}
+
+extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps,
+                              double tol, double* history_out, int* steps_done,
+                              double* explicit_out, double* step_ms_out) {
+  return gmres_cycle_impl(ctx, op, b, steps, tol, 0.0, history_out, steps_done, explicit_out,
+                          step_ms_out, nullptr);
+}
+
+// Complete, restarted low-rank GMRES (NEXT-2; Alg. 3 with P = I, eq:eps_soln; R19).
+extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart,
+                              int max_cycles, double tol, double tol_gmres, double eps_soln,
+                              tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
+                              int* steps_out) {
+  if (!ctx || !op || !z || !explicit_out || !cycles_done || restart < 1 || max_cycles < 0 ||
+      !(tol >= 0.0) || !(tol_gmres >= 0.0))
+    return TK_EARG;
+  TK_TRY(check_tt(ctx, b, "tk_gmres_solve(b)"));
+  if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t || z->n_x != op->n_x ||
+      z->n_xi != op->n_xi || z->n_t != op->n_t) {
+    ctx->err = "tk_gmres_solve: mode sizes differ from the operator's";
+    return TK_ESHAPE;
+  }
+  if (eps_soln < 0.0) eps_soln = tol;
+  const int64_t n_x = b->n_x, n_xi = b->n_xi, n_t = b->n_t;
+  const int T = op->T;
+  DevBuf sc;
+  TK_TRY(sc.get(ctx, 1));
+  TK_TRY(tk_norm(ctx, b, sc.p));
+  double bnorm;
+  TK_TRY(sync_read(ctx, &bnorm, sc.p, sizeof(double)));
+  // s_0 = T(b)  (z_0 = 0)
+  auto s_ = std::make_unique<OwnedTT>();
+  TK_TRY(clone_tt(ctx, b, *s_));
+  TK_TRY(tk_round(ctx, &s_->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_norm(ctx, &s_->t, sc.p));
+  TK_TRY(sync_read(ctx, explicit_out, sc.p, sizeof(double)));
+  std::unique_ptr<OwnedTT> zt;
+  int cyc = 0;
+  for (; cyc < max_cycles; cyc++) {
+    if (explicit_out[cyc] <= tol_gmres * bnorm) break;
+    std::vector<double> hist(restart + 1, 0.0);
+    int done = 0;
+    std::unique_ptr<OwnedTT> dz;
+    TK_TRY(gmres_cycle_impl(ctx, op, &s_->t, restart, tol, tol_gmres * bnorm, hist.data(), &done,
+                            nullptr, nullptr, &dz));
+    if (ls_out)
+      for (int i = 0; i <= restart; i++)
+        ls_out[(size_t)cyc * (restart + 1) + i] = i <= done ? hist[i] : 0.0;
+    if (steps_out) steps_out[cyc] = done;
+    // z <- T_eps_soln(z + dz)   (eq:eps_soln)
+    if (!zt) {
+      zt = std::move(dz);
+    } else {
+      auto z2 = std::make_unique<OwnedTT>();
+      TK_TRY(z2->make(ctx, n_x, n_xi, n_t, zt->t.r1 + dz->t.r1, zt->t.r2 + dz->t.r2));
+      TK_TRY(tk_axpby_host(ctx, 1.0, &zt->t, 1.0, &dz->t, &z2->t));
+      zt = std::move(z2);
+    }
+    TK_TRY(tk_round(ctx, &zt->t, eps_soln, 0, nullptr, nullptr, nullptr, nullptr));
+    // s = T(b - L z)   (line 14)
+    auto az = std::make_unique<OwnedTT>();
+    TK_TRY(az->make(ctx, n_x, n_xi, n_t, T * zt->t.r1, T * zt->t.r2));
+    TK_TRY(tk_apply_op(ctx, op, &zt->t, &az->t));
+    auto s2 = std::make_unique<OwnedTT>();
+    TK_TRY(s2->make(ctx, n_x, n_xi, n_t, b->r1 + az->t.r1, b->r2 + az->t.r2));
+    TK_TRY(tk_axpby_host(ctx, 1.0, b, -1.0, &az->t, &s2->t));
+    TK_TRY(tk_round(ctx, &s2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    s_ = std::move(s2);
+    TK_TRY(tk_norm(ctx, &s_->t, sc.p));
+    TK_TRY(sync_read(ctx, explicit_out + cyc + 1, sc.p, sizeof(double)));
+  }
+  *cycles_done = cyc;
+  if (!zt) {  // b rounded to (numerically) zero or max_cycles == 0: z = 0
+    TK_TRY(set_zero_tt(ctx, z));
+    return TK_OK;
+  }
+  if (zt->t.r1 > z->cap1 || zt->t.r2 > z->cap2) {
+    ctx->err = "tk_gmres_solve: solution ranks exceed z's capacity";
+    return TK_ECAP;
+  }
+  z->r1 = zt->t.r1;
+  z->r2 = zt->t.r2;
+  TK_TRY(tk_copy2d(ctx, n_x, z->r1, zt->t.U1, z->r1, z->U1, z->r1));
+  TK_TRY(tk_copy2d(ctx, z->r1 * n_xi, z->r2, zt->t.U2, z->r2, z->U2, z->r2));
+  TK_TRY(tk_copy2d(ctx, z->r2, n_t, zt->t.U3, n_t, z->U3, n_t));
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return TK_OK;
 }

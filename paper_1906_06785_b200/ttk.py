@@ -22,7 +22,8 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_ctx_profile", "tk_ctx_profile_dump",
             "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round",
             "tk_apply_round", "tk_dot",
-            "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle"]
+            "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle",
+            "tk_gmres_solve"]
 
 
 class TkError(RuntimeError):
@@ -73,6 +74,8 @@ def lib():
     L.tk_axpby_host.argtypes = [P, D, TTP, D, TTP, TTP]
     L.tk_scale.argtypes = [P, TTP, P, I]
     L.tk_gmres_cycle.argtypes = [P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
+    L.tk_gmres_solve.argtypes = [P, P, TTP, I, I, D, D, D, TTP, DP, DP, ctypes.POINTER(I),
+                                 ctypes.POINTER(I)]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
@@ -336,3 +339,28 @@ def gmres_cycle(op: Operator, b: TT, steps: int = 20, tol: float = 1e-6):
     k = done.value
     return dict(history=np.array(hist[: k + 1]), steps=k, explicit=expl.value,
                 step_ms=np.array(ms[:k]))
+
+
+def gmres_solve(op: Operator, b: TT, restart: int = 20, max_cycles: int = 5, tol: float = 1e-6,
+                tol_gmres: float = 1e-8, eps_soln: float = -1.0, cap: tuple | None = None):
+    """Complete restarted low-rank GMRES (tk_gmres_solve; Alg. 3 + eq:eps_soln, P = I).
+    Returns dict(z, explicit, ls, cycles, steps).  cap: rank capacity of z (default bounded by
+    the mode sizes and 512)."""
+    ctx = op.ctx
+    if cap is None:
+        cap = (max(1, min(b.n_x, b.n_xi * b.n_t, 512)), max(1, min(b.n_t, b.n_x * b.n_xi, 512)))
+    z = TT(b.n_x, b.n_xi, b.n_t, cap[0], cap[1])
+    D = ctypes.c_double
+    expl = (D * (max_cycles + 1))()
+    ls = (D * (max(max_cycles, 1) * (restart + 1)))()
+    steps = (ctypes.c_int * max(max_cycles, 1))()
+    done = ctypes.c_int()
+    bs, zs = b.struct(), z.struct()
+    ctx.check(lib().tk_gmres_solve(ctx._h, op._h, ctypes.byref(bs), int(restart), int(max_cycles),
+                                   float(tol), float(tol_gmres), float(eps_soln), ctypes.byref(zs),
+                                   expl, ls, ctypes.byref(done), steps))
+    z._update(zs)
+    c = done.value
+    lsv = np.array(ls[: c * (restart + 1)]).reshape(c, restart + 1) if c else np.zeros((0, restart + 1))
+    return dict(z=z, explicit=np.array(expl[: c + 1]), cycles=c, steps=list(steps[:c]),
+                ls=[row[: steps[i] + 1] for i, row in enumerate(lsv)])
