@@ -70,6 +70,8 @@ const char* tk_last_error(const tk_ctx* ctx);
 int64_t tk_ctx_launch_count(const tk_ctx* ctx);
 /* Profiling: enable != 0 clears the record list and starts recording CUDA events around
  * every kernel (tagged with its phase and its algorithmic flop and byte counts); 0 stops.
+ * enable == 2 records only the heavy launches (>= 1e8 algorithmic flops or bytes): the event
+ * pairs around the many small kernels of the latency-bound chain cost ~2 ms per c4 step.
  * tk_ctx_profile_dump synchronises the stream and writes one line per record,
  * "<phase> <ms> <flops> <bytes>\n", into buf (truncated to len); returns the number of
  * records. */

@@ -352,6 +352,85 @@ __global__ void max_diag_tol_k(int n, const double* __restrict__ H, double rel,
   }
 }
 
+// Unpivoted blocked Cholesky, one 32-column panel per launch (the CholeskyQR passes: pivot ==
+// false).  Every CTA factors the 32 x 32 diagonal block in warp 0 (lane c holds column c in
+// registers; a step is one broadcast row through shared memory, no block-wide barriers),
+// then each thread solves R11^T x = Hw[panel rows, c] for its own column c beyond the block
+// (forward substitution against R11 in shared memory).  The trailing update is the DMMA GEMM.
+// Stops (state[1] = 1, state[0] = rank) at the first column whose Schur diagonal is <= tol,
+// the semantics of the pivoted kernels with pivot == false.
+constexpr int UCT = 128;
+__global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const double* __restrict__ Hw,
+                                                          double* __restrict__ Ro,
+                                                          int* __restrict__ piv,
+                                                          int* __restrict__ state,
+                                                          const double* __restrict__ tol_dev) {
+  __shared__ double R11[32][33];
+  __shared__ double s_row[32];
+  __shared__ int s_kb;
+  if (state[1]) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int jb = min(32, n - j0);
+  if (tid < 32) {
+    const double tol = tol_dev[0];
+    double a[32];
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+      a[i] = (i < jb && lane < jb) ? Hw[(int64_t)(j0 + i) * n + j0 + lane] : 0.0;
+    int kb = jb;
+    for (int j = 0; j < jb; j++) {
+      double aj = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; i++)
+        if (i == j) aj = a[i];
+      const double d = __shfl_sync(0xffffffffu, aj, j);
+      if (!(d > tol)) {  // warp-uniform: rank reached
+        kb = j;
+        break;
+      }
+      const double r = sqrt(d);
+      const double rowj = lane == j ? r : (lane > j && lane < jb ? aj / r : 0.0);
+      s_row[lane] = rowj;
+      R11[j][lane] = rowj;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; i++)
+        if (i > j) a[i] = fma(-s_row[i], rowj, a[i]);
+      __syncwarp();
+    }
+    for (int j = kb; j < 32; j++) R11[j][lane] = 0.0;
+    if (lane == 0) s_kb = kb;
+    if (blockIdx.x == 0) {
+      for (int i = 0; i < kb; i++)
+        if (lane < jb) Ro[(int64_t)(j0 + i) * n + j0 + lane] = R11[i][lane];
+      if (lane < jb) piv[j0 + lane] = j0 + lane;
+      if (lane == 0) {
+        state[0] = j0 + kb;
+        if (kb < jb) state[1] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  const int kb = s_kb;
+  const int c = j0 + 32 + blockIdx.x * UCT + tid;
+  if (c < n && kb > 0) {
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; i++) x[i] = i < kb ? Hw[(int64_t)(j0 + i) * n + c] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i < kb) {
+        x[i] /= R11[i][i];
+#pragma unroll
+        for (int t = i + 1; t < 32; t++) x[t] = fma(-R11[i][t], x[i], x[t]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+      if (i < kb) Ro[(int64_t)(j0 + i) * n + c] = x[i];
+  }
+}
+
 constexpr int TS_H = 64;
 
 // Inverse of every 64 x 64 (or smaller, last) diagonal block of the upper triangular R,
@@ -438,6 +517,26 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   if (rem_out) TK_CUDA_TRY(ctx, cudaMemsetAsync(rem_out, 0, sizeof(double), ctx->stream));
   max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
   TK_LAUNCH_CHECK(ctx);
+  static const bool no_unpiv = getenv("TTK_CHOL_UNPIV_PANEL") != nullptr;
+  if (!pivot && !rem_out && !no_unpiv) {
+    // unpivoted: blocked right-looking with a warp-level diagonal factorisation (no pivot search)
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
+      const int rest = n - j0 - 32;
+      const int grid = std::max(1, (rest + UCT - 1) / UCT);
+      chol_unpiv_panel_k<<<grid, UCT, 0, ctx->stream>>>(n, j0, Hw.p, Ro, piv, state, tol.p);
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
+      if (rest > 0) {
+        const int c1 = j0 + 32;
+        // Hw[c1:, c1:] -= R12^T R12  (R12 = Ro[j0:j0+32, c1:]; no-op once stopped)
+        TK_TRY(tk_dgemm(ctx, true, false, rest, rest, 32, -1.0, Ro + (int64_t)j0 * n + c1, n,
+                        Ro + (int64_t)j0 * n + c1, n, 1.0, Hw.p + (int64_t)c1 * n + c1, n, true,
+                        false, state + 1));
+      }
+    }
+    return TK_OK;
+  }
   // register variant (n <= 2 PT): nb = 16 panel rows in registers, broadcast reads of the pivot
   // column from shared memory
   static const bool no_reg = getenv("TTK_PCHOL_SMEM") != nullptr;

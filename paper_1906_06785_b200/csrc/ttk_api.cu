@@ -167,6 +167,9 @@ extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
 // ============================================================================ profiling
 int tk_prof_begin(tk_ctx* ctx, const char* cat, double flops, double bytes) {
   if (!ctx->prof) return -1;
+  // level 1: the event pairs of the many small launches of the latency-bound chain cost ~2 ms
+  // per c4 step; only the heavy launches are recorded
+  if (ctx->prof_level < 2 && flops < 1e8 && bytes < 1e8) return -1;
   while (ctx->ev_pool.size() < ctx->ev_used + 2) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return -1;
@@ -186,6 +189,7 @@ void tk_prof_end(tk_ctx* ctx, int id) {
 extern "C" int tk_ctx_profile(tk_ctx* ctx, int enable) {
   if (!ctx) return TK_EARG;
   ctx->prof = enable != 0;
+  ctx->prof_level = enable == 2 ? 1 : 2;  // enable == 2: heavy launches only
   if (enable) {
     ctx->recs.clear();
     ctx->ev_used = 0;

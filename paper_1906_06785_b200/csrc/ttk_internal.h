@@ -28,6 +28,7 @@ struct tk_ctx {
   size_t pinned_bytes = 0;
   // profiling (tk_ctx_profile): per-launch event pairs, tagged by the current phase
   bool prof = false;
+  int prof_level = 2;  // 1: only launches with >= 1e8 algorithmic flops or bytes; 2: all
   const char* tag = "misc";
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
