@@ -43,6 +43,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--breakdown", action="store_true", help="per-phase times to stderr")
+    p.add_argument("--group-space", action="store_true",
+                   help="optional exact factor grouping of the space core (SURVEY 8d; reported "
+                        "separately, the literal T r growth is the primary line)")
     return p.parse_args()
 
 
@@ -255,6 +258,7 @@ def run_ours(args, cfg, op, x):
     stream = torch.cuda.current_stream()
     ctx = ttk.default_context()
     gop = ttk.Operator.from_kronsum(op, ctx)
+    groups = gop.group_space(True) if args.group_space else None
     xg = ttk.TT.from_cores(*x)
     T = op.T
     ycap = ttk.TT(op.n_x, op.n_xi, op.n_t, T * xg.r1, T * xg.r2)
@@ -458,7 +462,10 @@ def run_ours(args, cfg, op, x):
             "metric": METRIC, "value": replica_throughput(world, args.steps, total_ms), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(cfg, op), "ranks_out": list(ranks_out),
+            "data": "synthetic", "config": dict(workload_config(cfg, op), **(
+                {"workload": f"{cfg.name}: apply+round, space factors grouped (optional, exact)",
+                 "space_groups": groups} if groups is not None else {})),
+            "ranks_out": list(ranks_out),
             "roofline": roofline, "spmm_gbs": spmm_gbs,
             "spmm_frac": spmm_gbs / peaks["hbm_gbs"] if spmm_gbs else None,
             "spmm_frac_of_8tbs_spec": spmm_gbs / 8000.0 if spmm_gbs else None,

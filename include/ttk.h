@@ -92,6 +92,16 @@ int tk_op_create(tk_ctx* ctx, tk_op** op, int T, int64_t n_x, int64_t n_xi, int6
                  const int* T_ku, const double* const* T_band);
 int tk_op_destroy(tk_op* op);
 int tk_op_terms(const tk_op* op);
+/* Optional exact factor grouping of the space core (OFF by default — the literal
+ * T r rank growth is the primary shape).  At tk_op_create the library groups terms whose K_k
+ * has the same CSR structure as an earlier term's and is BITWISE proportional to it
+ * (K_k = c K_j checked entry by entry in fp64, e.g. nu_l L with nu_l = nu_0 2^-l), so that
+ * K_k U1 = c (K_j U1) exactly.  With enable != 0, tk_apply_round then stores the grown space
+ * core in the factored form Y1 = Y1' E (Y1' = [K_g U1] over the G group representatives) and
+ * runs bond 1 on Y1' with L2' = E L2 — the same operator, the same rounded result up to
+ * rounding order, fewer flops.  tk_apply_op and tk_round are unaffected.  Returns G (== T when
+ * nothing groups; enabling is then a no-op) or TK_EARG. */
+int tk_op_group_space(tk_op* op, int enable);
 
 /* y = A x   (PAPER.md:239-244 eq:Xz).  Per term k: K_k U1, G_k x_2 U2,
  * U3 T_k^T; terms are concatenated: y ranks = (T*x.r1, T*x.r2), y.U1 = [K_0 U1 | ... ],

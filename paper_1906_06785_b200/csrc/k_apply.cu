@@ -362,8 +362,23 @@ __global__ void time_apply_k(int T, int r2, int n_t, const int* __restrict__ kl,
 
 }  // namespace
 
-int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1) {
+int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1,
+                         bool grouped) {
   const int64_t n_x = op->n_x;
+  if (grouped) {
+    // the representatives of the spatial groups only (tk_op_group_space): Y1' = [K_g U1]_g
+    tk_op g = *op;
+    g.T = op->n_groups;
+    g.recptr = op->g_recptr;
+    g.rec = op->g_rec;
+    g.spmm_perterm = false;
+    g.n_groups = 0;
+    g.g_recptr = nullptr;
+    g.g_rec = nullptr;
+    const int st = tk_launch_spmm_multi(ctx, &g, r, U1, Y1, false);
+    // g's vectors are copies; nothing to free (the device arrays belong to op)
+    return st;
+  }
   const int threads = 256;
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);

@@ -414,3 +414,29 @@ int tk_swap_mid(tk_ctx* ctx, int64_t nb, int64_t np, int64_t nq, int64_t nw, con
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
+
+namespace {
+__global__ void group_rows_k(int T, int G, int64_t r, int64_t c, const int* __restrict__ group,
+                             const double* __restrict__ coef, const double* __restrict__ L,
+                             double* __restrict__ Lg) {
+  const int64_t n = (int64_t)G * r * c;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e % c, ga = e / c, a = ga % r;
+    const int g = (int)(ga / r);
+    double s = 0.0;
+    for (int k = 0; k < T; k++)
+      if (group[k] == g) s = fma(coef[k], L[((int64_t)k * r + a) * c + j], s);
+    Lg[e] = s;
+  }
+}
+}  // namespace
+
+int tk_group_rows(tk_ctx* ctx, int T, int G, int64_t r, int64_t c, const int* group,
+                  const double* coef, const double* L, double* Lg) {
+  const int64_t n = (int64_t)G * r * c;
+  if (n <= 0) return TK_OK;
+  group_rows_k<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(T, G, r, c, group, coef, L, Lg);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}

@@ -242,10 +242,9 @@ static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
 // distinct columns over all terms in ascending order, each as col | (term mask << 32), and the
 // values in (column, term) order.  Duplicate (column, term) entries are summed.  Not built (the
 // per-term kernel runs) when a row has more than 32 distinct columns.
-static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
-                        const int32_t* const* K_col, const double* const* K_val) {
-  const int T = op->T;
-  const int64_t n_x = op->n_x;
+static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K_rowptr,
+                        const int32_t* const* K_col, const double* const* K_val,
+                        int64_t** out_recptr, int64_t** out_rec) {
   if (n_x >= ((int64_t)1 << 31)) return TK_OK;
   // merged per-row lists (distinct columns with term masks, values in (column, term) order)
   std::vector<int64_t> wptr(n_x + 1, 0), vptr(n_x + 1, 0), words, vals_all;
@@ -340,9 +339,41 @@ static int build_merged(tk_ctx* ctx, tk_op* op, const int32_t* const* K_rowptr,
     if (b) TK_CUDA_TRY(ctx, cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice));
     return TK_OK;
   };
-  TK_TRY(up((void**)&op->recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
-  TK_TRY(up((void**)&op->rec, rec.data(), sizeof(int64_t) * rec.size()));
+  TK_TRY(up((void**)out_recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
+  TK_TRY(up((void**)out_rec, rec.data(), sizeof(int64_t) * rec.size()));
   return TK_OK;
+}
+
+// Spatial groups: term k joins the group of an earlier representative j when K_k has the same
+// CSR structure and K_k = c K_j BITWISE (c = val_k[0] / val_j[0], every entry checked in fp64),
+// e.g. the KL terms nu_l L with nu_l = nu_0 2^-l.  Then K_k U1 = c (K_j U1) exactly.
+static void find_groups(int T, int64_t n_x, const int32_t* const* rp, const int32_t* const* cl,
+                        const double* const* vl, std::vector<int>& group,
+                        std::vector<double>& coef, std::vector<int>& reps) {
+  group.assign(T, -1);
+  coef.assign(T, 1.0);
+  reps.clear();
+  for (int k = 0; k < T; k++) {
+    const int64_t nnz = rp[k][n_x];
+    for (size_t g = 0; g < reps.size() && group[k] < 0; g++) {
+      const int j = reps[g];
+      if (rp[j][n_x] != nnz || nnz == 0) continue;
+      if (memcmp(rp[j], rp[k], sizeof(int32_t) * (n_x + 1)) != 0) continue;
+      if (memcmp(cl[j], cl[k], sizeof(int32_t) * nnz) != 0) continue;
+      if (vl[j][0] == 0.0) continue;
+      const double c = vl[k][0] / vl[j][0];
+      bool ok = std::isfinite(c) && c != 0.0;
+      for (int64_t e = 0; ok && e < nnz; e++) ok = (c * vl[j][e] == vl[k][e]);
+      if (ok) {
+        group[k] = (int)g;
+        coef[k] = c;
+      }
+    }
+    if (group[k] < 0) {
+      group[k] = (int)reps.size();
+      reps.push_back(k);
+    }
+  }
 }
 
 extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_t n_xi,
@@ -423,7 +454,33 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
   }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
                               cudaMemcpyHostToDevice));
-  if (T <= 16) TK_TRY(build_merged(ctx, op.get(), K_rowptr, K_col, K_val));
+  if (T <= 16) TK_TRY(build_merged(ctx, T, n_x, K_rowptr, K_col, K_val, &op->recptr, &op->rec));
+  {
+    std::vector<int> group, reps;
+    std::vector<double> coef;
+    find_groups(T, n_x, K_rowptr, K_col, K_val, group, coef, reps);
+    op->n_groups = (int)reps.size();
+    if (op->n_groups < T && op->n_groups <= 16) {
+      std::vector<const int32_t*> grp, gcl;
+      std::vector<const double*> gvl;
+      for (int j : reps) {
+        grp.push_back(K_rowptr[j]);
+        gcl.push_back(K_col[j]);
+        gvl.push_back(K_val[j]);
+      }
+      TK_TRY(build_merged(ctx, op->n_groups, n_x, grp.data(), gcl.data(), gvl.data(),
+                          &op->g_recptr, &op->g_rec));
+      TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_group, sizeof(int) * T));
+      TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_coef, sizeof(double) * T));
+      TK_CUDA_TRY(ctx, cudaMemcpy(op->d_group, group.data(), sizeof(int) * T,
+                                  cudaMemcpyHostToDevice));
+      TK_CUDA_TRY(ctx, cudaMemcpy(op->d_coef, coef.data(), sizeof(double) * T,
+                                  cudaMemcpyHostToDevice));
+      if (!op->g_rec) op->n_groups = T;  // (a group row with > 32 distinct columns: no grouping)
+    } else {
+      op->n_groups = T;
+    }
+  }
   {
     const char* e = getenv("TTK_SPMM_PERTERM");
     op->spmm_perterm = e && e[0] == '1';
@@ -449,10 +506,19 @@ extern "C" int tk_op_destroy(tk_op* op) {
   cudaFree(op->band);
   cudaFree(op->recptr);
   cudaFree(op->rec);
+  cudaFree(op->g_recptr);
+  cudaFree(op->g_rec);
+  cudaFree(op->d_group);
+  cudaFree(op->d_coef);
   delete op;
   return TK_OK;
 }
 extern "C" int tk_op_terms(const tk_op* op) { return op ? op->T : 0; }
+extern "C" int tk_op_group_space(tk_op* op, int enable) {
+  if (!op) return TK_EARG;
+  op->group_space = enable != 0 && op->n_groups < op->T;
+  return op->n_groups;
+}
 
 // ============================================================================ validation
 static int check_tt(tk_ctx* ctx, const tk_tt* x, const char* who) {
@@ -475,8 +541,9 @@ static int check_tt(tk_ctx* ctx, const tk_tt* x, const char* who) {
 // The space and time cores of y = A x: Y1 = [K_k U1]_k (SpMM), Y3 = [U3 T_k^T]_k (band).
 // side: the SpMM runs on the side stream (forked here; the caller joins before it reads Y1)
 static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y,
-                            bool side = false) {
-  const int64_t R1 = op->T * x->r1, R2 = op->T * x->r2;
+                            bool side = false, bool grouped = false) {
+  const int64_t R2 = op->T * x->r2;
+  const int64_t R1 = (grouped ? op->n_groups : op->T) * x->r1;  // columns the SpMM writes
   if (side) TK_TRY(tk_side_fork(ctx));
   {
     std::unique_ptr<OnSide> on;
@@ -484,10 +551,12 @@ static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt*
     // algorithmic bytes: read U1 once, write Y1 once, read the CSR (12 B/nnz + rowptr)
     double nnz = 0;
     for (auto v : op->h_nnz) nnz += (double)v;
+    if (grouped) nnz *= (double)op->n_groups / op->T;  // (approximate: group representatives)
     double bytes = 8.0 * x->n_x * x->r1 + 8.0 * x->n_x * R1 + 12.0 * nnz +
-                   4.0 * op->T * (x->n_x + 1);
-    int id = tk_prof_begin(ctx, "spmm_multi", 2.0 * nnz * x->r1, bytes);
-    TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1));
+                   4.0 * (grouped ? op->n_groups : op->T) * (x->n_x + 1);
+    int id = tk_prof_begin(ctx, grouped ? "spmm_grouped" : "spmm_multi", 2.0 * nnz * x->r1,
+                           bytes);
+    TK_TRY(tk_launch_spmm_multi(ctx, op, (int)x->r1, x->U1, y->U1, grouped));
     tk_prof_end(ctx, id);
   }
   {
@@ -922,7 +991,7 @@ int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                       double* sigma2_out, double* discarded_out, double* norm_out,
                       const double* y2blk = nullptr, int64_t rb1 = 0, int64_t rb2 = 0,
-                      const double* gy_pre = nullptr);
+                      const double* gy_pre = nullptr, const tk_op* gop = nullptr);
 
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
@@ -959,12 +1028,16 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   // round joins the side stream before its first read of Y1 (bond 1)
   static const bool serial = getenv("TTK_SERIAL") != nullptr;
   CritScope cs(ctx);  // (declared before every buffer below: joins back after they are freed)
-  TK_TRY(apply_space_time(ctx, op, x, y, !serial));
+  // opt-in exact factor grouping (tk_op_group_space): the space core is produced in the
+  // factored form Y1 = Y1' E, Y1' = [K_g U1]_g over the G group representatives
+  const bool grouped = op->group_space && op->n_groups < op->T;
+  const int64_t R1s = (grouped ? op->n_groups : op->T) * x->r1;  // columns of the stored Y1
+  TK_TRY(apply_space_time(ctx, op, x, y, !serial, grouped));
   DevBuf gyb;  // bond 1's sampled pass-1 Gram, also on the side stream behind the SpMM
   if (!serial) {
     OnSide on(ctx);
-    TK_TRY(gyb.get(ctx, R1 * R1));
-    TK_TRY(pass1_gram(ctx, op->n_x, R1, y->U1, gyb.p));
+    TK_TRY(gyb.get(ctx, R1s * R1s));
+    TK_TRY(pass1_gram(ctx, op->n_x, R1s, y->U1, gyb.p));
   }
   SideJoin sj(ctx, !serial);  // (round_impl joins before bond 1; this covers early returns)
   DevBuf blk;
@@ -985,7 +1058,7 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   y->r1 = R1;
   y->r2 = R2;
   const int st = round_impl(ctx, y, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out,
-                            blk.p, x->r1, x->r2, gyb.p);
+                            blk.p, x->r1, x->r2, gyb.p, grouped ? op : nullptr);
   blk.release();
   pool_settle(ctx);
   return st;
@@ -993,7 +1066,8 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
 
 static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                       double* sigma2_out, double* discarded_out, double* norm_out,
-                      const double* y2blk, int64_t rb1, int64_t rb2, const double* gy_pre) {
+                      const double* y2blk, int64_t rb1, int64_t rb2, const double* gy_pre,
+                      const tk_op* gop) {
   TK_TRY(check_tt(ctx, x, "tk_round"));
   if (!(tol >= 0.0) || !std::isfinite(tol)) {
     ctx->err = "tk_round: tol must be finite and >= 0";
@@ -1042,7 +1116,19 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   // ---- step D: SVD of Z = U1 L2 (n_x x k2), space bond truncation
   TK_TRY(tk_side_join(ctx));  // U1 written by a side-stream SpMM (tk_apply_round)
   DevBuf W, GW1, V1, V2, Vt, lam, fl1;
-  TK_TRY(svd_two_pass(ctx, n_x, R1, x->U1, L2, k2, W, GW1, V1, fl1, gy_pre));
+  // grouped space core (gop != nullptr): x->U1 holds Y1' (n_x x G rb1) with Y1 = Y1' E, so
+  // Z = Y1 L2 = Y1' (E L2): bond 1 runs on Y1' with L2' = E L2 (G rb1 x k2)
+  DevBuf L2g;
+  const double* L2z = L2;
+  int64_t R1z = R1;
+  if (gop) {
+    R1z = (int64_t)gop->n_groups * rb1;
+    TK_TRY(L2g.get(ctx, R1z * k2));
+    TK_TRY(tk_group_rows(ctx, gop->T, gop->n_groups, rb1, k2, gop->d_group, gop->d_coef, L2,
+                         L2g.p));
+    L2z = L2g.p;
+  }
+  TK_TRY(svd_two_pass(ctx, n_x, R1z, x->U1, L2z, k2, W, GW1, V1, fl1, gy_pre));
   DevBuf sig1, scr;
   TK_TRY(scr.get(ctx, 16));
   int* info1 = (int*)scr.p;

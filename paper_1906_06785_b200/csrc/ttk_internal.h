@@ -115,6 +115,14 @@ struct tk_op {
   int64_t* recptr = nullptr;   // n_x + 1
   int64_t* rec = nullptr;
   bool spmm_perterm = false;   // TTK_SPMM_PERTERM=1: use the per-term kernel
+  // spatial groups (tk_op_group_space, SURVEY.md 8d "optional exact factor grouping"): terms
+  // whose K_k is bitwise proportional to a representative share its group; K_k = coef[k] K_g.
+  int n_groups = 0;            // number of groups (== T when nothing groups)
+  bool group_space = false;    // opt-in: the fused apply+round stores Y1 as Y1' = [K_g U1]_g
+  int* d_group = nullptr;      // T (device): group of term k
+  double* d_coef = nullptr;    // T (device)
+  int64_t* g_recptr = nullptr; // merged SpMM records of the group representatives
+  int64_t* g_rec = nullptr;
   std::vector<int64_t> h_nnz;  // host copy of per-term nnz
   int max_kl = 0, max_ku = 0;
 };
@@ -232,7 +240,11 @@ int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X
                     double* S);
 
 // Apply kernels
-int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1);
+int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1,
+                         bool grouped = false);
+// Lg[g r + a, j] = sum_{k : group[k] == g} coef[k] L[k r + a, j]   (L: T r x c, Lg: G r x c)
+int tk_group_rows(tk_ctx* ctx, int T, int G, int64_t r, int64_t c, const int* group,
+                  const double* coef, const double* L, double* Lg);
 int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const double* U2,
                           double* Y2, bool compact = false);
 int tk_launch_time_apply(tk_ctx* ctx, const tk_op* op, int r2, const double* U3, double* Y3);

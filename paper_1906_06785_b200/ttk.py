@@ -23,7 +23,7 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round",
             "tk_apply_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle",
-            "tk_gmres_solve"]
+            "tk_gmres_solve", "tk_op_group_space"]
 
 
 class TkError(RuntimeError):
@@ -63,6 +63,7 @@ def lib():
                                ctypes.POINTER(I), ctypes.POINTER(I), PP]
     L.tk_op_destroy.argtypes = [P]
     L.tk_op_terms.argtypes = [P]
+    L.tk_op_group_space.argtypes = [P, I]
     TTP = ctypes.POINTER(tk_tt)
     DP = ctypes.POINTER(D)
     L.tk_apply_op.argtypes = [P, P, TTP, TTP]
@@ -213,6 +214,14 @@ class Operator:
     @classmethod
     def from_kronsum(cls, op, ctx=None):
         return cls(op.n_x, op.n_xi, op.n_t, op.terms, ctx)
+
+    def group_space(self, enable: bool = True) -> int:
+        """Opt-in exact factor grouping of the space core in tt_apply_round
+        (tk_op_group_space); returns the number of spatial groups G (T: nothing groups)."""
+        g = lib().tk_op_group_space(self._h, 1 if enable else 0)
+        if g < 0:
+            raise TkError(g, "tk_op_group_space")
+        return g
 
     def __del__(self):
         try:

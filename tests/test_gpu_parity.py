@@ -338,3 +338,39 @@ def test_gmres_cycle_parity_c5(ctx):
     assert np.max(np.abs(h - hr)) <= 1e-8 * hr[0], (h, hr)
     assert res["explicit"] == pytest.approx(ref["explicit"], rel=1e-6, abs=1e-8 * hr[0])
     print("c5 GMRES ms/step:", np.round(res["step_ms"], 2).tolist())
+
+
+# ----------------------------------------------------------------------------- optional grouping
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_apply_round_grouped_space(name, ctx):
+    """SURVEY 8d optional exact factor grouping (tk_op_group_space): the KL terms nu_l L with
+    nu_l = nu_0 2^-l are bitwise proportional, so the space core is produced as Y1' E; the
+    rounded result must meet the same parity bars as the literal path."""
+    cfg = CONFIGS[name]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    g = gpu_op(op, ctx)
+    G = g.group_space(True)
+    assert G == 3 if name == "c2" else G == 4  # time-mass, Oseen, KL group (+ c3's wind term)
+    y = otT.apply_op(op, x)
+    check_round(y, cfg.tol, cfg.rmax, ctx, dense=False,
+                gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), cfg.tol, cfg.rmax,
+                                               want_info=True))
+
+
+def test_apply_round_grouped_random(ctx):
+    """Constructed proportional terms (K_2 = 0.5 K_0, K_3 = -0.25 K_1) on a random operator."""
+    from synth.operator import KronSumOp, Term
+    rng = np.random.default_rng(21)
+    base = random_operator(rng, 70, 4, 9, 2, density=0.1, max_band=1)
+    t0, t1 = base.terms
+    terms = [t0, t1,
+             Term("p0", 0, 0, rng.standard_normal((1, 9)), rng.standard_normal((4, 4)), t0.K * 0.5),
+             Term("p1", 1, 0, rng.standard_normal((2, 9)), rng.standard_normal((4, 4)), t1.K * -0.25)]
+    op = KronSumOp(70, 4, 9, terms)
+    x = random_tt(rng, 70, 4, 9, 3, 2)
+    g = gpu_op(op, ctx)
+    assert g.group_space(True) == 2
+    y = otT.apply_op(op, x)
+    check_round(y, 1e-8, 0, ctx, dense=True,
+                gpu=lambda: ttk.tt_apply_round(g, ttk.TT.from_cores(*x), 1e-8, 0, want_info=True))
