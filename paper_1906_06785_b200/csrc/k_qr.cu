@@ -447,15 +447,32 @@ __global__ void __launch_bounds__(32 * QB)
     // W = V_prev^T C (QB x QB): thread -> (q, jj, half); V_prev rows streamed from global
     // (each warp reads two q's of a row: near-broadcast), C from shared memory
     {
-      const int jj = tid % QB, q = (tid / QB) % QB, h = tid / (QB * QB);
-      double acc0 = 0.0, acc1 = 0.0;
-      int i = h;
-      for (; i + 2 < mt; i += 4) {
-        acc0 = fma(__ldg(Vprev + (int64_t)i * QB + q), psm[i * LD + jj], acc0);
-        acc1 = fma(__ldg(Vprev + (int64_t)(i + 2) * QB + q), psm[(i + 2) * LD + jj], acc1);
+      // warp w sums the rows i = w, w + 16, ...; lane l owns q = l / 2 and the 8 columns
+      // jj = 8 (l & 1) + u: one broadcast load of V_prev[i][q] and 8 shared-memory reads of
+      // row i of C per row, the rows' loads independent (the former thread-per-(q, jj) loop was
+      // a dependent chain of ~mt/4 L2 loads: most of the 15 us "load" phase at m = 896).
+      // Per-warp partials, then a fixed-order reduction (deterministic).
+      double* part = psm + (size_t)mt * LD;  // 16 x QB x QB partials (extra dynamic smem)
+      const int q = lane >> 1, j0 = 8 * (lane & 1);
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[u] = 0.0;
+#pragma unroll 4
+      for (int i = j; i < mt; i += QB) {
+        const double v = __ldg(Vprev + (int64_t)i * QB + q);
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = fma(v, psm[i * LD + j0 + u], acc[u]);
       }
-      for (; i < mt; i += 2) acc0 = fma(__ldg(Vprev + (int64_t)i * QB + q), psm[i * LD + jj], acc0);
-      s_w[h][q][jj] = acc0 + acc1;
+#pragma unroll
+      for (int u = 0; u < 8; u++) part[(j * QB + q) * QB + j0 + u] = acc[u];
+      __syncthreads();
+      if (tid < QB * QB) {
+        const int qq = tid / QB, jj = tid % QB;
+        double t = 0.0;
+        for (int w = 0; w < QB; w++) t += part[(w * QB + qq) * QB + jj];
+        s_w[0][qq][jj] = t;
+        s_w[1][qq][jj] = 0.0;
+      }
     }
     __syncthreads();
     // C -= (V_prev T_prev^T) W
@@ -849,7 +866,8 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     const double* VTtq0 = p > 0 ? VTtb.p + (size_t)(p - 1) * n * QB : nullptr;
     if (mt <= 32 * 28) {
       // register-resident columns
-      const size_t rsmem = sizeof(double) * (size_t)mt * (QB + 1);
+      // the loaded panel (mt x (QB+1)) + the look-ahead's per-warp partials (16 x QB x QB)
+      const size_t rsmem = sizeof(double) * ((size_t)mt * (QB + 1) + (size_t)QB * QB * QB);
       const double* Pp = Aw.p + (int64_t)(j0 - off) * n + j0;
       // the trailing update of panel p-2 measured the block this panel would work on
       const double* sqp = nullptr;
