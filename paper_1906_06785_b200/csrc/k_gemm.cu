@@ -114,8 +114,10 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
 
 // A_KMAJOR == transA ; B_KMAJOR == !transB.  CTA tile BM_ x BN_ x BK, WM x WN warps, each
 // warp a (BM_/WM) x (BN_/WN) sub-tile of (BM_/WM/8) x (BN_/WN/8) DMMA fragments.
-template <int BM_, int BN_, int WM, int WN, bool A_KMAJOR, bool B_KMAJOR, bool VEC2>
-__global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
+// BETA: C is read (beta != 0); the beta == 0 instantiations never touch C before writing it
+// and keep <= 128 registers (4 CTAs per SM for the 64 x 64 tile).
+template <int BM_, int BN_, int WM, int WN, bool A_KMAJOR, bool B_KMAJOR, bool VEC2, bool BETA>
+__global__ void __launch_bounds__(32 * WM * WN, (BETA ? 3 : 0)) dgemm_kernel(
     int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
     const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc, double alpha,
     double beta, int64_t kchunk, int sym, double* __restrict__ partial,
@@ -191,33 +193,109 @@ __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
   }
   cp_wait<0>();
 
+  if (!BETA) {
+    // epilogue.  Fast path (no symmetric mirror, N and ldc even, C 16-byte aligned): each lane's
+    // two adjacent outputs as one 16-byte store (the scalar stores stalled on the LSU: 17 % of the
+    // form_W warp samples sat in the epilogue)
+    const bool vec_out = !sym && (N % 2 == 0) &&
+                         (partial ? true : ((ldc % 2 == 0) && (((uintptr_t)C & 15) == 0)));
+    if (vec_out) {
+  #pragma unroll
+      for (int i = 0; i < FM; i++) {
+        const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
+        if (gm >= M) continue;
+  #pragma unroll
+        for (int j = 0; j < FN; j++) {
+          const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc;
+          if (gn >= N) continue;
+          if (partial) {
+            *(double2*)(partial + ((int64_t)blockIdx.z * M + gm) * N + gn) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+          } else {
+            double2 o = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+            double2* cp = (double2*)(C + gm * ldc + gn);
+            if (beta != 0.0) {
+              const double2 c = *cp;
+              o.x += beta * c.x;
+              o.y += beta * c.y;
+            }
+            *cp = o;
+          }
+        }
+      }
+      return;
+    }
+  #pragma unroll
+    for (int i = 0; i < FM; i++) {
+      const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
+      if (gm >= M) continue;
+  #pragma unroll
+      for (int j = 0; j < FN; j++) {
+  #pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc + h;
+          if (gn >= N) continue;
+          if (sym && gn < gm) continue;
+          double v = acc[i][j][h];
+          if (partial) {
+            partial[((int64_t)blockIdx.z * M + gm) * N + gn] = v;
+          } else {
+            double o = alpha * v;
+            if (beta != 0.0) o += beta * C[gm * ldc + gn];
+            C[gm * ldc + gn] = o;
+            if (sym && gn != gm) {
+              double o2 = alpha * v;
+              if (beta != 0.0) o2 += beta * C[gn * ldc + gm];
+              C[gn * ldc + gm] = o2;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
   // epilogue.  Fast path (no symmetric mirror, N and ldc even, C 16-byte aligned): each lane's
   // two adjacent outputs as one 16-byte store (the scalar stores stalled on the LSU: 17 % of the
   // form_W warp samples sat in the epilogue)
   const bool vec_out = !sym && (N % 2 == 0) &&
                        (partial ? true : ((ldc % 2 == 0) && (((uintptr_t)C & 15) == 0)));
+  // With beta != 0 every output needs a read of C: the reads of one fragment row i are issued
+  // together BEFORE its stores (the compiler cannot move a load of C above a store to C, so the
+  // former load-compute-store per element cost one L2 round trip each: ~20 us for a 64 x 64
+  // symmetric tile, the trailing updates of the Cholesky panels).
   if (vec_out) {
 #pragma unroll
     for (int i = 0; i < FM; i++) {
       const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
       if (gm >= M) continue;
+      if (partial) {
+#pragma unroll
+        for (int j = 0; j < FN; j++) {
+          const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc;
+          if (gn < N)
+            *(double2*)(partial + ((int64_t)blockIdx.z * M + gm) * N + gn) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+        continue;
+      }
+      double2 cv[FN];
+      if (BETA) {
+#pragma unroll
+        for (int j = 0; j < FN; j++) {
+          const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc;
+          cv[j] = gn < N ? *(const double2*)(C + gm * ldc + gn) : make_double2(0.0, 0.0);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < FN; j++) {
         const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc;
         if (gn >= N) continue;
-        if (partial) {
-          *(double2*)(partial + ((int64_t)blockIdx.z * M + gm) * N + gn) =
-              make_double2(acc[i][j][0], acc[i][j][1]);
-        } else {
-          double2 o = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
-          double2* cp = (double2*)(C + gm * ldc + gn);
-          if (beta != 0.0) {
-            const double2 c = *cp;
-            o.x += beta * c.x;
-            o.y += beta * c.y;
-          }
-          *cp = o;
+        double2 o = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        if (BETA) {
+          o.x += beta * cv[j].x;
+          o.y += beta * cv[j].y;
         }
+        *(double2*)(C + gm * ldc + gn) = o;
       }
     }
     return;
@@ -226,6 +304,18 @@ __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
   for (int i = 0; i < FM; i++) {
     const int64_t gm = m0 + wm * (BM_ / WM) + i * 8 + lr;
     if (gm >= M) continue;
+    double cn[FN][2], cmir[FN][2];
+    if (BETA && !partial) {
+#pragma unroll
+      for (int j = 0; j < FN; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t gn = n0 + wn * (BN_ / WN) + j * 8 + 2 * lc + h;
+          const bool ok = gn < N && !(sym && gn < gm);
+          cn[j][h] = ok ? C[gm * ldc + gn] : 0.0;
+          cmir[j][h] = (ok && sym && gn != gm) ? C[gn * ldc + gm] : 0.0;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < FN; j++) {
 #pragma unroll
@@ -238,11 +328,11 @@ __global__ void __launch_bounds__(32 * WM * WN) dgemm_kernel(
           partial[((int64_t)blockIdx.z * M + gm) * N + gn] = v;
         } else {
           double o = alpha * v;
-          if (beta != 0.0) o += beta * C[gm * ldc + gn];
+          if (BETA) o += beta * cn[j][h];
           C[gm * ldc + gn] = o;
           if (sym && gn != gm) {
             double o2 = alpha * v;
-            if (beta != 0.0) o2 += beta * C[gn * ldc + gm];
+            if (BETA) o2 += beta * cmir[j][h];
             C[gn * ldc + gm] = o2;
           }
         }
@@ -272,7 +362,7 @@ __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __
   }
 }
 
-template <int BM_, int BN_, int WM, int WN, bool AK, bool BK_, bool V2>
+template <int BM_, int BN_, int WM, int WN, bool AK, bool BK_, bool V2, bool BETA>
 int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
              double beta, int64_t kchunk, int sym, double* partial, const int* skip) {
@@ -281,11 +371,11 @@ int launch_t(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const doub
   size_t smem = (size_t)STAGES * (GA::SIZE + GB::SIZE) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2>,
+    cudaFuncSetAttribute(dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2, BETA>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2><<<grid, 32 * WM * WN, smem, ctx->stream>>>(
+  dgemm_kernel<BM_, BN_, WM, WN, AK, BK_, V2, BETA><<<grid, 32 * WM * WN, smem, ctx->stream>>>(
       M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, sym, partial, skip);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
@@ -297,14 +387,18 @@ template <int CFG, bool AK, bool BK_, bool V2>
 int launch_cfg(tk_ctx* ctx, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A,
                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
                double beta, int64_t kchunk, int sym, double* partial, const int* skip) {
+  // beta != 0 only on the 64 x 64 tile (the caller maps it there)
+  if (beta != 0.0 && !partial)
+    return launch_t<64, 64, 2, 2, AK, BK_, V2, true>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc,
+                                                     alpha, beta, kchunk, sym, partial, skip);
   if (CFG == 1)
-    return launch_t<128, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                                beta, kchunk, sym, partial, skip);
+    return launch_t<128, 64, 2, 2, AK, BK_, V2, false>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc,
+                                                       alpha, beta, kchunk, sym, partial, skip);
   if (CFG == 2)
-    return launch_t<128, 80, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                                beta, kchunk, sym, partial, skip);
-  return launch_t<64, 64, 2, 2, AK, BK_, V2>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha,
-                                             beta, kchunk, sym, partial, skip);
+    return launch_t<128, 80, 2, 2, AK, BK_, V2, false>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc,
+                                                       alpha, beta, kchunk, sym, partial, skip);
+  return launch_t<64, 64, 2, 2, AK, BK_, V2, false>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc,
+                                                    alpha, beta, kchunk, sym, partial, skip);
 }
 
 }  // namespace
@@ -333,8 +427,11 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   int cfg = 0;
   // (the 128 x 64 tile measured slower than 64 x 64 on the c4 form_W: 27.96 vs 27.06 ms — half
   // the resident warps; kept selectable with TTK_GEMM_CFG=1)
-  if (!sym && M >= 128LL * 4 * ctx->num_sms && N >= 64 && N % 64 != 0 && N % 80 == 0) cfg = 2;
-  if (force_cfg >= 0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64) cfg = force_cfg;
+  if (beta == 0.0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64 && N % 64 != 0 &&
+      N % 80 == 0)
+    cfg = 2;
+  if (force_cfg >= 0 && beta == 0.0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64)
+    cfg = force_cfg;
   const int64_t bm = cfg ? 128 : BM, bn = cfg == 2 ? 80 : BN;
   const int64_t tm = (M + bm - 1) / bm, tn = (N + bn - 1) / bn;
   int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
@@ -344,10 +441,10 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   static int per_sm = 0;
   if (per_sm == 0) {
     const size_t smem = (size_t)STAGES * 2 * BM * (BK + PADK) * sizeof(double);
-    cudaFuncSetAttribute(dgemm_kernel<64, 64, 2, 2, true, true, true>,
+    cudaFuncSetAttribute(dgemm_kernel<64, 64, 2, 2, true, true, true, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dgemm_kernel<64, 64, 2, 2, true, true, true>,
-                                                  NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, dgemm_kernel<64, 64, 2, 2, true, true, true, false>, NT, smem);
     per_sm = std::max(per_sm, 1);
   }
   static const int mult = getenv("TTK_SPLITK_MULT") ? atoi(getenv("TTK_SPLITK_MULT")) : 4;

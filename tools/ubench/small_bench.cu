@@ -63,6 +63,35 @@ int main(int argc, char** argv) {
     }
     return 0;
   }
+  if (!strcmp(what, "gemmsmall")) {
+    // latency of the small DMMA GEMMs of the Cholesky trailing updates: sym n x n x 32, and a
+    // plain n x n x 32 product, 200 back-to-back launches each (profiling off)
+    tk_ctx* c2;
+    cudaStream_t st2;
+    cudaStreamCreate(&st2);
+    tk_ctx_create(&c2, st2);
+    double *A, *C;
+    cudaMalloc(&A, sizeof(double) * 32 * n);
+    cudaMalloc(&C, sizeof(double) * n * n);
+    cudaMemset(A, 0, sizeof(double) * 32 * n);
+    cudaMemset(C, 0, sizeof(double) * n * n);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int sym = 1; sym >= 0; sym--) {
+      for (int rep = 0; rep < 2; rep++) {
+        cudaEventRecord(e0, st2);
+        for (int i = 0; i < 200; i++)
+          tk_dgemm(c2, true, false, n, n, 32, -1.0, A, n, A, n, 1.0, C, n, sym != 0);
+        cudaEventRecord(e1, st2);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("gemm n=%d K=32 sym=%d: %.2f us per launch\n", n, sym, ms * 1e3 / 200);
+      }
+    }
+    return 0;
+  }
   tk_ctx* ctx;
   cudaStream_t st;
   cudaStreamCreate(&st);
