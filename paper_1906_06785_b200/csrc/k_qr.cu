@@ -717,11 +717,19 @@ __global__ void __launch_bounds__(AR_T) apply_reflector_k(int m, int nc, const d
         d[u] = fma(x.y, w[2 * q + 1], d[u]);
       }
     }
+    // all AR_U reads of C before the stores (the compiler cannot prove the rows distinct —
+    // ldc is a runtime value — so a load after a store waited for it: one L2 round trip per row)
+    double cv[AR_U];
+#pragma unroll
+    for (int u = 0; u < AR_U; u++) {
+      const int i = i0 + u * AR_G;
+      cv[u] = i < m ? C[(int64_t)i * ldc + gc] : 0.0;
+    }
 #pragma unroll
     for (int u = 0; u < AR_U; u++) {
       const int i = i0 + u * AR_G;
       if (i < m) {
-        const double v = C[(int64_t)i * ldc + gc] - d[u];
+        const double v = cv[u] - d[u];
         C[(int64_t)i * ldc + gc] = v;
         if (i >= rowskip) sq = fma(v, v, sq);
       }

@@ -85,10 +85,14 @@ extern "C" int tk_ctx_create(tk_ctx** out, void* stream) {
 int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
   // highest priority, like ctx->crit: the QR's trailing updates are on the critical path and
   // must not queue behind the side stream's big GEMMs
+  // (one level below ctx->crit, whose QR panel kernels need a whole SM: when an SM frees up,
+  // the pending panel is dispatched before more update blocks; TTK_AUX_PRIO_EQUAL=1: same level)
   int lo = 0, hi = 0;
   TK_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  static const bool eq = getenv("TTK_AUX_PRIO_EQUAL") != nullptr;
+  const int pr = (eq || hi >= lo) ? hi : hi + 1;
   for (auto& s : ctx->aux)
-    if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+    if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, pr));
   while (ctx->fork_ev.size() < n_events) {
     cudaEvent_t e;
     TK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
