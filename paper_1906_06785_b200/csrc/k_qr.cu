@@ -26,6 +26,7 @@
 namespace {
 
 constexpr int QB = 16;     // panel width
+constexpr int kQrPoll = 8; // host polls of the early-stop flag every kQrPoll panels
 constexpr int QT = 512;    // threads of the panel kernel
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -963,6 +964,18 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     if (nnext > 0) {
       if (p > 0) TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evR[p - 1], 0));
       TK_TRY(factor(p + 1));
+    }
+    // Every kQrPoll panels the host reads the early-stop flag (one s0 synchronisation): once
+    // the numerical rank is reached the remaining panels and reflector updates would only
+    // return early, but each still costs its launch and event latencies (c4: ~40 of the 56
+    // panels of the rank-128 time-core Gram).
+    if (!no_stop && (p + 1) % kQrPoll == 0 && p + 2 < np) {
+      int st = 0;
+      TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned ? ctx->pinned : &st, stop_at, sizeof(int),
+                                       cudaMemcpyDeviceToHost, s0));
+      TK_CUDA_TRY(ctx, cudaStreamSynchronize(s0));
+      if (ctx->pinned) st = *(int*)ctx->pinned;
+      if (st <= p + 1) break;
     }
   }
   // join: everything on s1 / s2 before s0 continues (and before the scratch buffers are freed)
