@@ -497,6 +497,17 @@ int grid_for(tk_ctx* ctx, int64_t total) {
 
 }  // namespace
 
+// Host poll of the stop flag (state[1]) every kCholPoll panels: once the factorisation has
+// stopped the remaining panel launches and (skipped) updates only cost launch latency.
+constexpr int kCholPoll = 4;
+static int chol_stopped(tk_ctx* ctx, const int* state, bool* stopped) {
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, state + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  *stopped = *(int*)ctx->pinned != 0;
+  return TK_OK;
+}
+
 int tk_pchol_max_n() { return 4096; }
 
 int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* tol_abs_dev,
@@ -534,6 +545,11 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
                         Ro + (int64_t)j0 * n + c1, n, 1.0, Hw.p + (int64_t)c1 * n + c1, n, true,
                         false, state + 1));
       }
+      if (ctx->pinned && (j0 / 32 + 1) % kCholPoll == 0 && rest > 32) {
+        bool stopped = false;
+        TK_TRY(chol_stopped(ctx, state, &stopped));
+        if (stopped) break;
+      }
     }
     return TK_OK;
   }
@@ -561,6 +577,11 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
       if (j0 + jb < n)
         TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
                         Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true, false, state + 1));
+      if (ctx->pinned && (j0 / NBR + 1) % kCholPoll == 0 && j0 + 2 * NBR < n) {
+        bool stopped = false;
+        TK_TRY(chol_stopped(ctx, state, &stopped));
+        if (stopped) break;
+      }
     }
     return TK_OK;
   }
@@ -586,6 +607,11 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
       // Hw -= Ro[j0:j0+jb, :]^T Ro[j0:j0+jb, :]   (rows of a stopped panel are zero: no-op)
       TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
                       Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true, false, state + 1));
+    }
+    if (ctx->pinned && (j0 / nb + 1) % kCholPoll == 0 && j0 + 2 * nb < n) {
+      bool stopped = false;
+      TK_TRY(chol_stopped(ctx, state, &stopped));
+      if (stopped) break;
     }
   }
   return TK_OK;
