@@ -117,6 +117,31 @@ def test_apply_spmm_paths(T, n_x, density, r1, perterm, ctx, monkeypatch):
         assert rel(a, b) <= 1e-13
 
 
+def test_apply_spmm_long_records(ctx):
+    """Merged SpMM rows whose record exceeds the 96 staged words (<= 32 distinct columns but
+    16 terms on each: ~20 x 16 values per row) take the unstaged path: values from global."""
+    import scipy.sparse as sp
+    from synth.operator import KronSumOp, Term
+    rng = np.random.default_rng(31)
+    n_x, T = 90, 16
+    pat = sp.random(n_x, n_x, density=0.22, random_state=rng, format="csr")
+    terms = []
+    for k in range(T):
+        K = pat.copy()
+        K.data = rng.standard_normal(K.nnz)
+        K.indices = K.indices.astype(np.int32)
+        K.indptr = K.indptr.astype(np.int32)
+        K.sort_indices()
+        terms.append(Term(f"t{k}", 0, 0, rng.standard_normal((1, 4)), rng.standard_normal((3, 3)), K))
+    op = KronSumOp(n_x, 3, 4, terms)
+    assert max(np.diff(pat.indptr)) <= 32 and max(np.diff(pat.indptr)) * (T + 1) > 96
+    x = random_tt(rng, n_x, 3, 4, 40, 2)
+    y_o = otT.apply_op(op, x)
+    y_g = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x)).cores_numpy()
+    for a, b in zip(y_g, y_o):
+        assert rel(a, b) <= 1e-13
+
+
 def test_apply_capacity_and_shape_errors(ctx):
     rng = np.random.default_rng(3)
     op = random_operator(rng, 10, 3, 4, 2)
