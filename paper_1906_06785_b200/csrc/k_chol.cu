@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
 // registers (Rp), so a step reads only the pivot column's values from shared memory (broadcast)
 // — the shared-memory variant above streams both operands of every row dot product through
 // shared memory.  The step loop is unrolled (NB compile-time) so Rp is statically indexed.
-template <int MAXC, int NB>
-__global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot,
+template <int MAXC, int NB, int NTH = PT>
+__global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivot,
                                                         const double* __restrict__ Hw,
                                                         double* __restrict__ Ro,
                                                         int* __restrict__ piv,
@@ -206,8 +206,8 @@ __global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot
                                                         const double* __restrict__ tol_dev,
                                                         double* __restrict__ rem_out) {
   extern __shared__ double sR[];  // NB x n
-  __shared__ double s_val[PT / 32];
-  __shared__ int s_idx[PT / 32];
+  __shared__ double s_val[NTH / 32];
+  __shared__ int s_idx[NTH / 32];
   __shared__ int s_p;
   __shared__ double s_dmax;
   if (state[1]) return;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot
   int bi = 0x7fffffff;
 #pragma unroll
   for (int m = 0; m < MAXC; m++) {
-    const int c = tid + m * PT;
+    const int c = tid + m * NTH;
     live[m] = c < n && !retired[c];
     d[m] = live[m] ? Hw[(int64_t)c * n + c] : -INFINITY;
     if (d[m] > bv) {
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot
   } else {
 #pragma unroll
     for (int m = 0; m < MAXC; m++)
-      if (tid + m * PT == j0) {
+      if (tid + m * NTH == j0) {
         s_p = j0;
         s_dmax = d[m];
       }
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot
     bi = 0x7fffffff;
 #pragma unroll
     for (int m = 0; m < MAXC; m++) {
-      const int c = tid + m * PT;
+      const int c = tid + m * NTH;
       if (c >= n) continue;
       double out = 0.0;
       if (c == p) {
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_reg_k(int n, int j0, int pivot
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < MAXC; m++)
-        if (tid + m * PT == j + 1) {
+        if (tid + m * NTH == j + 1) {
           s_p = j + 1;
           s_dmax = d[m];
         }
@@ -556,6 +556,34 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   // register variant (n <= 2 PT): nb = 16 panel rows in registers, broadcast reads of the pivot
   // column from shared memory
   static const bool no_reg = getenv("TTK_PCHOL_SMEM") != nullptr;
+  // 512 < n <= 1024: the register variant with 1024 threads (16 panel rows in registers)
+  if (!no_reg && n > PT && n <= 2 * PT && !getenv("TTK_PCHOL_NO_REG1024")) {
+    constexpr int NBR = 16;
+    const size_t rsmem = (size_t)NBR * n * sizeof(double);
+    static size_t rattr = 0;
+    if (rsmem > 48 * 1024 && rattr < rsmem) {
+      cudaFuncSetAttribute(pchol_panel_reg_k<1, NBR, 2 * PT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      rattr = rsmem;
+    }
+    for (int j0 = 0; j0 < n; j0 += NBR) {
+      const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
+      pchol_panel_reg_k<1, NBR, 2 * PT><<<1, 2 * PT, rsmem, ctx->stream>>>(
+          n, j0, pivot ? 1 : 0, Hw.p, Ro, piv, state, tol.p, rem_out);
+      TK_LAUNCH_CHECK(ctx);
+      tk_prof_end(ctx, pid);
+      const int jb = std::min(NBR, n - j0);
+      if (j0 + jb < n)
+        TK_TRY(tk_dgemm(ctx, true, false, n, n, jb, -1.0, Ro + (int64_t)j0 * n, n,
+                        Ro + (int64_t)j0 * n, n, 1.0, Hw.p, n, true, false, state + 1));
+      if (ctx->pinned && (j0 / NBR + 1) % (2 * kCholPoll) == 0 && j0 + 2 * NBR < n) {
+        bool stopped = false;
+        TK_TRY(chol_stopped(ctx, state, &stopped));
+        if (stopped) break;
+      }
+    }
+    return TK_OK;
+  }
   if (!no_reg && n <= PT) {
     // one column per thread: 32 panel rows fit in registers (for two columns per thread only
     // 16 do, and the doubled number of rank-nb updates then costs more than it saves)
