@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(PT) pchol_panel_k(int n, int j0, int nb, int p
       }
       return;
     }
-    const double r = sqrt(dmax), rinv = 1.0 / r;
+    const double rinv = rsqrt(dmax), r = dmax * rinv;  // one special function per step
     // row j of Ro:  Ro[j, c] = (Hw[p, c] - sum_{t < s} sR[t, p] sR[t, c]) / r, then the next
     // pivot candidate among the updated live columns
     const double* hrow = Hw + (int64_t)p * n;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
       }
       return;
     }
-    const double r = sqrt(dmax), rinv = 1.0 / r;
+    const double rinv = rsqrt(dmax), r = dmax * rinv;  // one special function per step
     double pc[NB];
 #pragma unroll
     for (int t = 0; t < NB; t++) pc[t] = t < s ? sR[t * n + p] : 0.0;
@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const d
                                                           const double* __restrict__ tol_dev) {
   __shared__ double R11[32][33];
   __shared__ double s_row[32];
+  __shared__ double s_dinv[32];  // 1 / R11[i][i]
   __shared__ int s_kb;
   if (state[1]) return;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -388,10 +389,11 @@ __global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const d
         kb = j;
         break;
       }
-      const double r = sqrt(d);
-      const double rowj = lane == j ? r : (lane > j && lane < jb ? aj / r : 0.0);
+      const double rinv = rsqrt(d), r = d * rinv;  // one special function on the chain
+      const double rowj = lane == j ? r : (lane > j && lane < jb ? aj * rinv : 0.0);
       s_row[lane] = rowj;
       R11[j][lane] = rowj;
+      if (lane == j) s_dinv[j] = rinv;
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < 32; i++)
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const d
 #pragma unroll
     for (int i = 0; i < 32; i++) {
       if (i < kb) {
-        x[i] /= R11[i][i];
+        x[i] *= s_dinv[i];
 #pragma unroll
         for (int t = i + 1; t < 32; t++) x[t] = fma(-R11[i][t], x[i], x[t]);
       }
