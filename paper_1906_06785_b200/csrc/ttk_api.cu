@@ -872,8 +872,20 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
   // (the refinement Jacobi of step (3) restores the full accuracy, so this one may stop as
   // soon as the couplings are small: its last, confirming sweep is left to the refinement)
   static const double stop1 = getenv("TTK_PASS2_STOP1") ? atof(getenv("TTK_PASS2_STOP1")) : 1e-3;
-  TK_TRY(tk_jacobi_eig(ctx, kc, X.p, lam2.p, Y.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
-                       nullptr, nullptr, 0.0, 0, floor, V0.p, (int)k, stop1));
+  static const bool onto_v0 = getenv("TTK_JACOBI_ONTO_V0") != nullptr;
+  if (!onto_v0 && k >= kc + 64) {
+    // accumulate the rotations into J (kc x kc) and apply them to V0 = R^T (k x kc) once: the
+    // Jacobi's per-round tile phase then updates kc instead of k rows (fewer work items when
+    // the factorisation truncated: c5 rounds k ~ 1300, kc ~ 1000)
+    DevBuf J;
+    TK_TRY(J.get(ctx, (int64_t)kc * kc));
+    TK_TRY(tk_jacobi_eig(ctx, kc, X.p, lam2.p, J.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
+                         nullptr, nullptr, 0.0, 0, floor, nullptr, 0, stop1));
+    TK_TRY(tk_dgemm(ctx, false, false, k, kc, kc, 1.0, V0.p, kc, J.p, kc, 0.0, Y.p, kc));
+  } else {
+    TK_TRY(tk_jacobi_eig(ctx, kc, X.p, lam2.p, Y.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
+                         nullptr, nullptr, 0.0, 0, floor, V0.p, (int)k, stop1));
+  }
   TK_TRY(nrm.get(ctx, kc));
   TK_TRY(tk_col_norms(ctx, k, kc, Y.p, kc, nrm.p));
   TK_TRY(V1.get(ctx, k * kc));
