@@ -501,7 +501,7 @@ int grid_for(tk_ctx* ctx, int64_t total) {
 
 // Host poll of the stop flag (state[1]) every kCholPoll panels: once the factorisation has
 // stopped the remaining panel launches and (skipped) updates only cost launch latency.
-constexpr int kCholPoll = 4;
+constexpr int kCholPoll = 2;
 static int chol_stopped(tk_ctx* ctx, const int* state, bool* stopped) {
   TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, state + 1, sizeof(int), cudaMemcpyDeviceToHost,
                                    ctx->stream));
