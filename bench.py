@@ -117,8 +117,15 @@ class Clocks:
 # DRAM traffic of the largest dgemm launch from one `ncu --set full` capture (the per-launch
 # average over all dgemm launches is not captured, so `traffic` stays null and the capture is
 # quoted beside it): profiles/r01/ncu_dgemm_formW.txt
-DGEMM_TRAFFIC = {"launch": "bond1.form_W (786432 x 640 x 896)", "dram_bytes": 9.65e9,
-                 "algorithmic_bytes": 9.67e9, "source": "profiles/r01/ncu_dgemm_formW.txt"}
+DGEMM_TRAFFIC = {
+    "note": "DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) of the dominant "
+            "dgemm launches of one c4 step vs their algorithmic bytes; the roofline's 'traffic' "
+            "stays null because 'achieved' averages ~45 heavy launches of mixed shapes",
+    "form_W (786432 x 640 x 896)": {"dram_bytes": 9.64e9, "algorithmic_bytes": 9.67e9, "ms": 26.98},
+    "gram_W (640 x 640 x 786432, sym, split-K 32)": {"dram_bytes": 6.61e9,
+                                                     "algorithmic_bytes": 4.03e9, "ms": 10.89},
+    "form_U1 (786432 x 160 x 640)": {"dram_bytes": 5.03e9, "algorithmic_bytes": 5.03e9, "ms": 5.07},
+    "source": "profiles/r01/dgemm_traffic_h.csv (+ .json), profiles/r01/ncu_d_formW.txt"}
 
 
 # FP64 tensor-pipe ceiling measured on this pool's B200 (register-only DMMA m8n8k4 chains,
