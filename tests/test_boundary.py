@@ -59,3 +59,13 @@ def test_product_package_never_imports_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_new_entry_points_reject_null_arguments(so):
+    """tk_op_group_space / tk_gmres_solve validate their arguments before any CUDA call."""
+    so.tk_op_group_space.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    assert so.tk_op_group_space(None, 1) == -3
+    so.tk_gmres_solve.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 2 + \
+        [ctypes.c_double] * 3 + [ctypes.c_void_p] * 5
+    assert so.tk_gmres_solve(None, None, None, 4, 2, 1e-8, 1e-6, -1.0, None, None, None, None,
+                             None) == -3
