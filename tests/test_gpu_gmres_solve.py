@@ -62,3 +62,20 @@ def test_gmres_solve_zero_rhs(ctx):
                         max_cycles=2, tol=1e-8, tol_gmres=1e-6)
     assert g["cycles"] == 0
     assert np.all(g["z"].cores_numpy()[0] == 0.0)
+
+
+def test_gmres_solve_parity_c5_operator(ctx):
+    """The c5 operator (c2 sizes, 6 terms) and right-hand side, two restarts of 4 steps at the
+    config's truncation tolerance: explicit residuals and the solution vs the oracle."""
+    cfg = CONFIGS["c5"]
+    op = build_operator(cfg)
+    b = make_rhs_tt(cfg, op.n_xi)
+    o = o_solve(op, b, restart=4, max_cycles=2, tol=cfg.tol, tol_gmres=0.0)
+    g = ttk.gmres_solve(ttk.Operator.from_kronsum(op, ctx), ttk.TT.from_cores(*b), restart=4,
+                        max_cycles=2, tol=cfg.tol, tol_gmres=0.0)
+    bn = otT.norm(b)
+    assert g["cycles"] == o["cycles"] == 2
+    assert np.max(np.abs(g["explicit"] - o["explicit"])) <= 1e-8 * bn
+    # the solution: ||z_g - z_o|| via the orthogonalised difference TT (too large to densify)
+    d = otT.round_tt(otT.axpby(1.0, g["z"].cores_numpy(), -1.0, o["z"]), 0.0)
+    assert np.linalg.norm(d[2]) <= 1e-8 * otT.norm(o["z"])
