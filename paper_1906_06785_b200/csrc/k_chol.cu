@@ -67,6 +67,44 @@ __device__ __forceinline__ void block_argmax(double bv, int bi, double* s_val, i
   __syncthreads();
 }
 
+// Block-wide argmax with ONE barrier: every warp reduces the per-warp candidates itself, so the
+// result lands in registers of all threads (no second barrier / shared broadcast).  The
+// per-warp candidate arrays are double-buffered by call parity: a warp may still be reading
+// buffer `par` of this call while faster warps write buffer `par ^ 1` of the next one.
+template <int NW>
+__device__ __forceinline__ void block_argmax_reg(double bv, int bi, double (*s_val)[NW],
+                                                 int (*s_idx)[NW], int par, int& p_out,
+                                                 double& dmax_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[par][warp] = bv;
+    s_idx[par][warp] = bi;
+  }
+  __syncthreads();
+  bv = lane < NW ? s_val[par][lane] : -INFINITY;
+  bi = lane < NW ? s_idx[par][lane] : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  p_out = bi;
+  dmax_out = bv;
+}
+
 // Panel of nb pivot steps (one CTA).  Shared memory: the panel's rows of Ro for every column
 // (sR[t * n + c], t < nb) and the live Schur diagonal sd[c] (-inf once retired).  A step: row
 // j of Ro for the pivot p, the Schur diagonal update, and — fused into the same pass over the
@@ -206,10 +244,13 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
                                                         const double* __restrict__ tol_dev,
                                                         double* __restrict__ rem_out) {
   extern __shared__ double sR[];  // NB x n
-  __shared__ double s_val[NTH / 32];
-  __shared__ int s_idx[NTH / 32];
+  __shared__ double s_val[2][NTH / 32];
+  __shared__ int s_idx[2][NTH / 32];
   __shared__ int s_p;
   __shared__ double s_dmax;
+  int par = 0;           // parity of the argmax buffers
+  int cur_p = 0;         // pivot of the next step (registers, every thread)
+  double cur_dmax = 0.0;
   if (state[1]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double tol = tol_dev[0];
@@ -231,7 +272,8 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
     for (int t = 0; t < NB; t++) Rp[m][t] = 0.0;
   }
   if (pivot) {
-    block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);
+    block_argmax_reg<NTH / 32>(bv, bi, s_val, s_idx, par, cur_p, cur_dmax);
+    par ^= 1;
   } else {
 #pragma unroll
     for (int m = 0; m < MAXC; m++)
@@ -240,13 +282,15 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
         s_dmax = d[m];
       }
     __syncthreads();
+    cur_p = s_p;
+    cur_dmax = s_dmax;
   }
 #pragma unroll
   for (int s = 0; s < NB; s++) {
     const int j = j0 + s;
     if (j >= n) break;
-    const int p = s_p;
-    const double dmax = s_dmax;
+    const int p = cur_p;
+    const double dmax = cur_dmax;
     if (!(dmax > tol) || p >= n) {  // uniform: rank reached (or nothing left / non-finite)
       if (tid == 0) {
         state[0] = j;
@@ -260,11 +304,11 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         __syncthreads();
-        if (lane == 0) s_val[warp] = t;
+        if (lane == 0) s_val[par][warp] = t;
         __syncthreads();
         if (tid == 0) {
           double tt = 0.0;
-          for (int w = 0; w < (int)(blockDim.x >> 5); w++) tt += s_val[w];
+          for (int w = 0; w < (int)(blockDim.x >> 5); w++) tt += s_val[par][w];
           rem_out[0] = tt;
         }
       }
@@ -315,7 +359,8 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
       state[0] = j + 1;
     }
     if (pivot) {
-      block_argmax(bv, bi, s_val, s_idx, &s_p, &s_dmax);  // also orders this step's writes
+      block_argmax_reg<NTH / 32>(bv, bi, s_val, s_idx, par, cur_p, cur_dmax);  // (its barrier
+      par ^= 1;                                     // also orders this step's writes)
     } else {
       __syncthreads();
 #pragma unroll
@@ -329,6 +374,8 @@ __global__ void __launch_bounds__(NTH) pchol_panel_reg_k(int n, int j0, int pivo
         s_dmax = -INFINITY;
       }
       __syncthreads();
+      cur_p = s_p;
+      cur_dmax = s_dmax;
     }
   }
 }
