@@ -72,6 +72,8 @@ int64_t tk_ctx_launch_count(const tk_ctx* ctx);
  * every kernel (tagged with its phase and its algorithmic flop and byte counts); 0 stops.
  * enable == 2 records only the heavy launches (>= 1e8 algorithmic flops or bytes): the event
  * pairs around the many small kernels of the latency-bound chain cost ~2 ms per c4 step.
+ * enable == 3 records every launch and the dump adds a fifth field, the start offset (ms)
+ * from the first record (timeline).
  * tk_ctx_profile_dump synchronises the stream and writes one line per record,
  * "<phase> <ms> <flops> <bytes>\n", into buf (truncated to len); returns the number of
  * records. */
@@ -92,6 +94,12 @@ int tk_op_create(tk_ctx* ctx, tk_op** op, int T, int64_t n_x, int64_t n_xi, int6
                  const int* T_ku, const double* const* T_band);
 int tk_op_destroy(tk_op* op);
 int tk_op_terms(const tk_op* op);
+/* Select the spatial SpMM kernel of row a1: kernel 0 = the column-merged multi-term sweep
+ * (default; available when every row of the merged pattern has <= 32 distinct columns),
+ * kernel 1 = the per-term CSR kernel.  Returns 1 if the merged kernel will run, 0 if the
+ * per-term kernel will, TK_EARG on a bad argument.  Not thread-safe against concurrent
+ * applies of the same operator. */
+int tk_op_set_spmm_kernel(tk_op* op, int kernel);
 /* Optional exact factor grouping of the space core (OFF by default — the literal
  * T r rank growth is the primary shape).  At tk_op_create the library groups terms whose K_k
  * has the same CSR structure as an earlier term's and is BITWISE proportional to it

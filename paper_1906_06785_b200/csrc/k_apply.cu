@@ -386,9 +386,8 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
   if (op->rec && !op->spmm_perterm) {
     blocks = std::min<int64_t>((n_x * 32 + threads - 1) / threads, 16LL * ctx->num_sms);
     // scalar lanes (two 32-column chunks at r = 64) measured faster than 16-byte lanes: the
-    // 2x accumulators of the 16-byte variant halve the resident warps (TTK_SPMM_V2=1 for it)
-    static const bool no_v2 = getenv("TTK_SPMM_V2") == nullptr;
-    const bool v2m = !no_v2 && (r % 2 == 0) && (((uintptr_t)U1 & 15) == 0) && (((uintptr_t)Y1 & 15) == 0);
+    // 2x accumulators of the 16-byte variant halve the resident warps
+    const bool v2m = false;
 #define TK_SPMM_M(TM, V)                                                                    \
   spmm_merged_k<TM, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                      \
       n_x, op->T, r, op->recptr, (const long long*)op->rec, U1, Y1)

@@ -416,7 +416,11 @@ __global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const d
   __shared__ double s_row[32];
   __shared__ double s_dinv[32];  // 1 / R11[i][i]
   __shared__ int s_kb;
-  if (state[1]) return;
+  // Only a stop recorded by an EARLIER panel launch ends this one: that panel left
+  // state[0] = its rank < j0.  CTA 0 of THIS launch may set state[1] while other CTAs are
+  // still to be dispatched; they must still write their off-diagonal columns of Ro (state[0]
+  // is then >= j0; before this launch it was j0 or, at j0 = 0, 0).
+  if (state[1] && state[0] < j0) return;
   const int tid = threadIdx.x, lane = tid & 31;
   const int jb = min(32, n - j0);
   if (tid < 32) {
@@ -577,8 +581,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   if (rem_out) TK_CUDA_TRY(ctx, cudaMemsetAsync(rem_out, 0, sizeof(double), ctx->stream));
   max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
   TK_LAUNCH_CHECK(ctx);
-  static const bool no_unpiv = getenv("TTK_CHOL_UNPIV_PANEL") != nullptr;
-  if (!pivot && !rem_out && !no_unpiv) {
+  if (!pivot && !rem_out) {
     // unpivoted: blocked right-looking with a warp-level diagonal factorisation (no pivot search)
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int pid = tk_prof_begin(ctx, "pchol_panel", 0.0, 0.0);
@@ -604,9 +607,8 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   }
   // register variant (n <= 2 PT): nb = 16 panel rows in registers, broadcast reads of the pivot
   // column from shared memory
-  static const bool no_reg = getenv("TTK_PCHOL_SMEM") != nullptr;
   // 512 < n <= 1024: the register variant with 1024 threads (16 panel rows in registers)
-  if (!no_reg && n > PT && n <= 2 * PT && !getenv("TTK_PCHOL_NO_REG1024")) {
+  if (n > PT && n <= 2 * PT) {
     constexpr int NBR = 16;
     const size_t rsmem = (size_t)NBR * n * sizeof(double);
     static size_t rattr = 0;
@@ -633,7 +635,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     }
     return TK_OK;
   }
-  if (!no_reg && n <= PT) {
+  if (n <= PT) {
     // one column per thread: 32 panel rows fit in registers (for two columns per thread only
     // 16 do, and the doubled number of rank-nb updates then costs more than it saves)
     constexpr int NBR = 32;

@@ -423,16 +423,13 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   // tile configuration: large non-symmetric products whose N is a multiple of 80 but not of 64
   // (160 at c4: the bond-1 reconstruction) take the 128 x 80 tile (warp tiles 64 x 40, no
   // ragged tile column: c4 form_U1 6.09 -> 5.51 ms)
-  static const int force_cfg = getenv("TTK_GEMM_CFG") ? atoi(getenv("TTK_GEMM_CFG")) : -1;
   int cfg = 0;
   // (the 128 x 64 tile measured slower than 64 x 64 on the c4 form_W: 27.96 vs 27.06 ms — half
-  // the resident warps; kept selectable with TTK_GEMM_CFG=1)
+  // the resident warps)
   if (beta == 0.0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64 && N % 64 != 0 &&
       N % 80 == 0)
     cfg = 2;
-  if (force_cfg >= 0 && beta == 0.0 && !sym && M >= 128LL * 4 * ctx->num_sms && N >= 64)
-    cfg = force_cfg;
-  const int64_t bm = cfg ? 128 : BM, bn = cfg == 2 ? 80 : BN;
+  const int64_t bm = cfg == 2 ? 128 : BM, bn = cfg == 2 ? 80 : BN;
   const int64_t tm = (M + bm - 1) / bm, tn = (N + bn - 1) / bn;
   int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
   // split-K for small outputs with a long K: about four waves of resident CTAs (SMs x CTAs/SM);
@@ -447,7 +444,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
         &per_sm, dgemm_kernel<64, 64, 2, 2, true, true, true, false>, NT, smem);
     per_sm = std::max(per_sm, 1);
   }
-  static const int mult = getenv("TTK_SPLITK_MULT") ? atoi(getenv("TTK_SPLITK_MULT")) : 4;
+  const int mult = 4;
   const int64_t slots = (int64_t)per_sm * ctx->num_sms * mult;
   int64_t splits = 1;
   if (cfg == 0 && tiles < slots && K >= 8 * BK) {
@@ -477,10 +474,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
 #define TK_GEMM_CASE(a, b, v)                                                               \
   if (AK == a && BKm == b && v2 == v) {                                                     \
     const int sf = (sym ? 1 : 0) | (triu_b ? 2 : 0);                                        \
-    if (cfg == 1)                                                                           \
-      st = launch_cfg<1, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
-                                  kchunk, sf, partial, skip);                                     \
-    else if (cfg == 2)                                                                      \
+    if (cfg == 2)                                                                           \
       st = launch_cfg<2, a, b, v>(ctx, grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta,  \
                                   kchunk, sf, partial, skip);                                     \
     else                                                                                    \

@@ -18,7 +18,7 @@
 //          entries stay exactly 0), and V[:, IJ_t] <- V[:, IJ_t] Q_t   (64 x 64 DMMA tiles)
 // Rotation counts per sweep end the loop (all CTAs read the counter after the barrier).
 //
-// Cluster skip (bond SVDs only): when lskip >= 0, rotations between two indices whose
+// Cluster skip (disabled: tk_jacobi_eig callers pass lskip = nullptr): when lskip >= 0, rotations between two indices whose
 // diagonal entries are both <= lskip are skipped.  lskip is chosen (cluster_skip_k) so the
 // skipped cluster's total mass is <= delta^2/4: its internal structure cannot move the rank
 // decision (only its trace enters the discarded tail, and the trace is invariant); couplings
@@ -599,118 +599,7 @@ __global__ void max_abs_diag_k(int n, const double* A, double* out) {
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
-// lskip = largest diagonal value of the set of smallest diagonal entries whose total is
-// <= frac * delta^2, delta^2 = tol^2 * trace / 2  (-1 if that set is empty).
-__global__ void cluster_skip_k(int n, const double* __restrict__ A, double tol, double frac,
-                               long long rmax, double* out) {
-  extern __shared__ double d[];
-  __shared__ double tr;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = fmax(A[(int64_t)i * n + i], 0.0);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < n; i++) s += d[i];
-    tr = s;
-  }
-  __syncthreads();
-  // rank-sort ascending into d[n .. 2n)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int rk = 0;
-    for (int j = 0; j < n; j++) rk += (d[j] < d[i]) || (d[j] == d[i] && j < i);
-    d[n + rk] = d[i];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double lim = frac * tol * tol * tr * 0.5;
-    // when rmax binds the kept set ends near the rmax-th largest value, which can lie below
-    // delta^2: keep the cluster's mass (a bound on its largest eigenvalue) under a quarter of
-    // the current rmax-th largest diagonal entry as well
-    if (rmax > 0 && rmax <= n) lim = fmin(lim, 0.25 * d[n + (n - rmax)]);
-    // if the rank rule on the current diagonal already exceeds rmax, rmax will bind and the
-    // kept set may reach below any useful cluster: no skip (the redo would cost more)
-    if (rmax > 0) {
-      const double d2 = tol * tol * tr * 0.5;
-      double c2 = 0.0;
-      int cnt = 0;
-      while (cnt < n && c2 + d[n + cnt] <= d2) c2 += d[n + cnt++];
-      if (n - cnt > rmax) {
-        out[0] = -1.0;
-        return;
-      }
-    }
-    double cum = 0.0, l = -1.0;
-    for (int i = 0; i < n; i++) {
-      cum += d[n + i];
-      if (cum > lim) break;
-      l = d[n + i];
-    }
-    out[0] = l;
-  }
-}
-
-// Safety check of a skipped run: io[1] = an upper bound on the largest eigenvalue of the
-// unresolved block D (indices with diagonal <= lskip), or -1 if nothing was skipped.  The caller
-// accepts the run iff every KEPT eigenvalue (the r chosen by the rank rule, all resolved)
-// exceeds it: then the kept set is the dominant invariant subspace and the discarded tail,
-// which contains all of D, is exact through trace(D).
-__global__ void __launch_bounds__(512) skip_check_k(int n, int n_pad,
-                                                    const double* __restrict__ G, double* io) {
-  // lambda_max(D) <= min(max Gershgorin radius, trace(D), ||D||_F) for the PSD block D
-  __shared__ double r_g[512], r_tr[512], r_fr[512];
-  const double l = io[0];
-  double gx = -1e308, tr = 0.0, fr = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double di = G[(int64_t)i * n_pad + i];
-    if (di <= l) {
-      double g = di;
-      tr += fmax(di, 0.0);
-      fr += di * di;
-      for (int j = 0; j < n; j++) {
-        if (j == i) continue;
-        const double dj = G[(int64_t)j * n_pad + j];
-        if (dj <= l) {
-          const double v = G[(int64_t)i * n_pad + j];
-          g += fabs(v);
-          fr += v * v;
-        }
-      }
-      gx = fmax(gx, g);
-    }
-  }
-  r_g[threadIdx.x] = gx;
-  r_tr[threadIdx.x] = tr;
-  r_fr[threadIdx.x] = fr;
-  __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st) {
-      r_g[threadIdx.x] = fmax(r_g[threadIdx.x], r_g[threadIdx.x + st]);
-      r_tr[threadIdx.x] += r_tr[threadIdx.x + st];
-      r_fr[threadIdx.x] += r_fr[threadIdx.x + st];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const bool nod = r_g[0] == -1e308;
-    const double bound = fmin(r_g[0], fmin(r_tr[0], sqrt(r_fr[0])));
-    io[1] = (l < 0.0 || nod) ? -1.0 : bound;
-  }
-}
-
 }  // namespace
-
-int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev,
-                    int64_t rmax) {
-  size_t smem = 2 * (size_t)n * sizeof(double);
-  if (smem > 200 * 1024) {
-    // too large for the shared-memory sort: no skipping (always safe)
-    return tk_set_scalar(ctx, lskip_dev, -1.0);
-  }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(cluster_skip_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cluster_skip_k<<<1, 512, smem, ctx->stream>>>(n, A, tol, 0.25, (long long)rmax, lskip_dev);
-  TK_LAUNCH_CHECK(ctx);
-  return TK_OK;
-}
 
 int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double abs_tol_scale,
                   double rel_tol, int max_sweeps, int* sweeps_out, double* lskip_dev,
@@ -768,20 +657,13 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   a.lskip = lskip_dev;
   a.lskip_io = lskip_dev;
   a.n = n;
-  a.rs_tol = (lskip_dev && getenv("TTK_RANK_SKIP")) ? rs_tol : 0.0;
+  a.rs_tol = 0.0;  // (rank-aware skip: off)
   a.rs_rmax = rs_rmax;
   a.offmax = offmax;
   // relative mode: a sweep whose largest applied relative coupling is <= 1e-10 leaves
   // couplings of O(1e-20) behind (quadratic convergence): stop after it
   a.stop_rel = rel_tol > 0.0 ? (stop_rel > 0.0 ? stop_rel : 1e-10) : 0.0;
-  static const bool dbg = getenv("TTK_DEBUG") != nullptr;
-  DevBuf tsb;
   a.tstamp = nullptr;
-  if (dbg) {
-    TK_TRY(tsb.get(ctx, 8));
-    TK_CUDA_TRY(ctx, cudaMemsetAsync(tsb.p, 0, 8 * sizeof(double), ctx->stream));
-    a.tstamp = (unsigned long long*)tsb.p;
-  }
   a.max_inner = (npairs == 1) ? 60 : 1;
   a.max_sweeps = max_sweeps;
   a.stats = stats;
@@ -802,38 +684,12 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   int sg = (int)std::min<int64_t>((n + 127) / 128, 4LL * ctx->num_sms);
   eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, mv, Gp.p, Vp.p, lam, V);
   TK_LAUNCH_CHECK(ctx);
-  if (lskip_dev) {
-    skip_check_k<<<1, 512, 0, ctx->stream>>>(n, n_pad, Gp.p, lskip_dev);
-    TK_LAUNCH_CHECK(ctx);
-  }
   tk_prof_end(ctx, prof_id);
-  if (sweeps_out || getenv("TTK_DEBUG")) {
-    int sw = 0;
+  if (sweeps_out) {
     TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_sweeps, sizeof(int), cudaMemcpyDeviceToHost,
                                      ctx->stream));
     TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    sw = *(int*)ctx->pinned;
-    if (sweeps_out) *sweeps_out = sw;
-    if (getenv("TTK_DEBUG")) {
-      unsigned long long ts[8];
-      TK_CUDA_TRY(ctx, cudaMemcpy(ts, tsb.p, sizeof(ts), cudaMemcpyDeviceToHost));
-      const double rounds = (double)sw * (nb - 1);
-      fprintf(stderr,
-              "[ttk] jacobi n=%d sweeps=%d rel=%g skip=%d grid=%d | per round us: inner %.1f "
-              "sync %.1f cols %.1f sync %.1f rows %.1f sync %.1f\n",
-              n, sw, rel_tol, lskip_dev ? 1 : 0, grid, ts[0] / rounds / 1e3, ts[1] / rounds / 1e3,
-              ts[2] / rounds / 1e3, ts[3] / rounds / 1e3, ts[4] / rounds / 1e3,
-              ts[5] / rounds / 1e3);
-      fprintf(stderr, "[ttk]    inner round cycles: params %.0f  update %.0f\n",
-              ts[6] / rounds / 63.0, ts[7] / rounds / 63.0);
-      std::vector<int> rot(sw);
-      std::vector<double> om(sw);
-      TK_CUDA_TRY(ctx, cudaMemcpy(rot.data(), stats, sizeof(int) * sw, cudaMemcpyDeviceToHost));
-      TK_CUDA_TRY(ctx, cudaMemcpy(om.data(), offmax, sizeof(double) * sw, cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[ttk]    per sweep rotations/offmax:");
-      for (int s = 0; s < sw; s++) fprintf(stderr, " %d/%.1e", rot[s], om[s]);
-      fprintf(stderr, "\n");
-    }
+    *sweeps_out = *(int*)ctx->pinned;
   }
   return TK_OK;
 }

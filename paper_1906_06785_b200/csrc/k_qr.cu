@@ -836,26 +836,35 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   TK_TRY(sqpart.get(ctx, (size_t)np * sq_stride));
   double* thr2 = qst.p;
   int* stop_at = (int*)(qst.p + 1);
-  static const bool no_stop = getenv("TTK_QR_NO_EARLY_STOP") != nullptr;
+  const bool no_stop = false;
   qr_stop_init_k<<<1, 1024, 0, ctx->stream>>>((int64_t)n * n, A, thr2, stop_at);
   TK_LAUNCH_CHECK(ctx);
-  static const bool dbg = getenv("TTK_DEBUG_QR") != nullptr;
-  DevBuf dbgb;
-  if (dbg) TK_TRY(dbgb.get(ctx, 12 * (size_t)np));
+  DevBuf dbgb;  // (per-panel clock stamps of the panel kernels: not allocated = off)
   // Streams: s0 (ctx->stream) carries the critical path  F_0, U_0', F_1, U_1', ...  where F_p
   // factors panel p and U_p' applies H_p to panel p+1 only; s1 applies H_p to the columns
   // beyond panel p+1 (overlapping F_{p+1}); s2 accumulates Q <- Q H_p forward (overlapping
   // everything).  evF[p]: V_p ready; evR[p]: H_p applied beyond panel p+1.
   TK_TRY(tk_aux_streams(ctx, 2 * (size_t)np + 2));
   cudaStream_t s0 = ctx->stream, s1 = ctx->aux[0], s2 = ctx->aux[1];
-  static const bool serial = getenv("TTK_QR_SERIAL") != nullptr;
-  if (serial) s1 = s2 = s0;
   cudaEvent_t* evF = ctx->fork_ev.data();
   cudaEvent_t* evR = evF + np;
   cudaEvent_t evStart = evF[2 * np], evEnd = evF[2 * np + 1];
   TK_CUDA_TRY(ctx, cudaEventRecord(evStart, s0));
   TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s1, evStart, 0));
   TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s2, evStart, 0));
+  // join on EVERY exit (also the error returns inside the panel loop): everything on s1 / s2
+  // before s0 continues, and before the scratch buffers above are freed on s0 (declared after
+  // them, so destroyed first)
+  struct AuxJoin {
+    cudaStream_t s0, s1, s2;
+    cudaEvent_t ev;
+    ~AuxJoin() {
+      cudaEventRecord(ev, s1);
+      cudaStreamWaitEvent(s0, ev, 0);
+      cudaEventRecord(ev, s2);
+      cudaStreamWaitEvent(s0, ev, 0);
+    }
+  } join{s0, s1, s2, evEnd};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(qr_panel_warp_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -977,33 +986,6 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
       if (ctx->pinned) st = *(int*)ctx->pinned;
       if (st <= p + 1) break;
     }
-  }
-  // join: everything on s1 / s2 before s0 continues (and before the scratch buffers are freed)
-  const int jid = tk_prof_begin(ctx, "qr_join", 0.0, 0.0);  // s0 idle time waiting for s1 / s2
-  TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s1));
-  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
-  TK_CUDA_TRY(ctx, cudaEventRecord(evEnd, s2));
-  TK_CUDA_TRY(ctx, cudaStreamWaitEvent(s0, evEnd, 0));
-  tk_prof_end(ctx, jid);
-  if (dbg) {
-    std::vector<unsigned long long> h(12 * (size_t)np);
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), dbgb.p, 8 * h.size(), cudaMemcpyDeviceToHost, s0));
-    TK_CUDA_TRY(ctx, cudaStreamSynchronize(s0));
-    double a[4] = {0, 0, 0, 0}, gap = 0, f[5] = {0, 0, 0, 0, 0};
-    int nf = 0;
-    for (int p = 0; p < np; p++) {
-      for (int k = 0; k < 4; k++) a[k] += (h[12 * p + k + 1] - h[12 * p + k]) * 1e-3;
-      if (p) gap += (h[12 * p] - h[12 * (p - 1) + 4]) * 1e-3;
-      if (n - p * QB > 6 * QB) {
-        for (int k = 0; k < 5; k++) f[k] += (h[12 * p + 6 + k] - h[12 * p + 5 + k]) * 1e-3;
-        nf++;
-      }
-    }
-    if (nf)
-      fprintf(stderr, "[ttk]   column 4, critical warp (us): dot %.2f warp_sum %.2f update %.2f reflector %.2f barrier %.2f\n",
-              f[0] / nf, f[1] / nf, f[2] / nf, f[3] / nf, f[4] / nf);
-    fprintf(stderr, "[ttk] qr n=%d per panel us: load %.1f refl0 %.1f columns %.1f export %.1f | gap between panels %.1f (nf %d, raw %llu %llu)\n",
-            n, a[0] / np, a[1] / np, a[2] / np, a[3] / np, gap / std::max(np - 1, 1), nf, h[5], h[10]);
   }
   return TK_OK;
 }

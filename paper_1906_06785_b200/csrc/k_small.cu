@@ -68,17 +68,11 @@ __global__ void eye_k(double* dst, int64_t n) {
 __global__ void rank_select_k(int n, const double* __restrict__ lam, double* __restrict__ sig,
                               double tol, const double* __restrict__ delta_in, int64_t rmax,
                               double kthr, int* __restrict__ info, double* __restrict__ dinfo,
-                              const double* __restrict__ lskip) {
+                              int rcap) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = sqrt(fmax(lam[i], 0.0));
   __syncwarp();
   if (threadIdx.x != 0) return;
-  int nres = n;
-  if (lskip) {
-    const double l = lskip[0];
-    nres = 0;
-    for (int i = 0; i < n; i++) nres += lam[i] > l;
-  }
-  info[2] = nres;
+  info[2] = rcap;
   double nrm2 = 0.0;
   for (int i = n - 1; i >= 0; i--) nrm2 += sig[i] * sig[i];
   double nrm = sqrt(nrm2);
@@ -98,6 +92,9 @@ __global__ void rank_select_k(int n, const double* __restrict__ lam, double* __r
   }
   while (r < n && sig[r] == sig[r - 1]) r++;
   if (rmax > 0 && r > rmax) r = (int)rmax;
+  // only the first rcap eigenpairs are resolved (pass2_chol: entries >= kc hold the Schur
+  // remainder, which counts in the discarded tail but has no singular vector)
+  if (r > rcap) r = rcap;
   if (r < 1) r = 1;
   int k = 0;
   for (int i = 0; i < n; i++)
@@ -307,9 +304,9 @@ int tk_eye(tk_ctx* ctx, double* dst, int64_t n) {
 }
 int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
                    const double* delta_dev_in, int64_t rmax, double kthr, int* info,
-                   double* dinfo, const double* lskip_dev) {
+                   double* dinfo, int rcap) {
   rank_select_k<<<1, 32, 0, ctx->stream>>>(n, lam, sig, tol, delta_dev_in, rmax, kthr, info,
-                                           dinfo, lskip_dev);
+                                           dinfo, rcap > 0 ? std::min(rcap, n) : n);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }

@@ -86,11 +86,10 @@ int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
   // highest priority, like ctx->crit: the QR's trailing updates are on the critical path and
   // must not queue behind the side stream's big GEMMs
   // (one level below ctx->crit, whose QR panel kernels need a whole SM: when an SM frees up,
-  // the pending panel is dispatched before more update blocks; TTK_AUX_PRIO_EQUAL=1: same level)
+  // the pending panel is dispatched before more update blocks)
   int lo = 0, hi = 0;
   TK_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  static const bool eq = getenv("TTK_AUX_PRIO_EQUAL") != nullptr;
-  const int pr = (eq || hi >= lo) ? hi : hi + 1;
+  const int pr = hi >= lo ? hi : hi + 1;
   for (auto& s : ctx->aux)
     if (!s) TK_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, pr));
   while (ctx->fork_ev.size() < n_events) {
@@ -102,8 +101,6 @@ int tk_aux_streams(tk_ctx* ctx, size_t n_events) {
 }
 
 CritScope::CritScope(tk_ctx* ctx) : c(ctx) {
-  static const bool serial = getenv("TTK_SERIAL") != nullptr;
-  if (serial) return;
   if (!ctx->crit) {
     int lo = 0, hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return;
@@ -194,6 +191,7 @@ extern "C" int tk_ctx_profile(tk_ctx* ctx, int enable) {
   if (!ctx) return TK_EARG;
   ctx->prof = enable != 0;
   ctx->prof_level = enable == 2 ? 1 : 2;  // enable == 2: heavy launches only
+  ctx->prof_timeline = enable == 3;       // enable == 3: every launch + start offsets
   if (enable) {
     ctx->recs.clear();
     ctx->ev_used = 0;
@@ -205,7 +203,7 @@ extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
   if (!ctx) return TK_EARG;
   TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   std::string out;
-  static const bool tl = getenv("TTK_TIMELINE") != nullptr;
+  const bool tl = ctx->prof_timeline;
   for (auto& r : ctx->recs) {
     float ms = 0.f, t0 = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
@@ -325,9 +323,6 @@ static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K
       }
     }
   }
-  static const bool natural = getenv("TTK_SPMM_NATURAL") != nullptr;
-  if (natural)
-    for (int64_t i = 0; i < n_x; i++) order[i] = (int32_t)i;
   std::vector<int64_t> recptr(n_x + 1, 0), rec;
   rec.reserve(words.size() + vals_all.size() + n_x + 16);
   for (int64_t pos = 0; pos < n_x; pos++) {
@@ -394,7 +389,11 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
     ctx->err = "tk_op_create: n_x must fit int32 CSR indices";
     return TK_EARG;
   }
-  auto op = std::make_unique<tk_op>();
+  // (partial device allocations are freed by tk_op_destroy on every error return)
+  struct OpDel {
+    void operator()(tk_op* o) const { tk_op_destroy(o); }
+  };
+  std::unique_ptr<tk_op, OpDel> op(new tk_op());
   op->ctx = ctx;
   op->T = T;
   op->n_x = n_x;
@@ -411,6 +410,13 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
       ctx->err = "tk_op_create: rowptr must start at 0 and be non-decreasing";
       return TK_EARG;
     }
+    // every row pointer in [rowptr[i], nnz]: the merged-record builder and the SpMM kernels
+    // index col/val by them
+    for (int64_t i = 0; i < n_x; i++)
+      if (K_rowptr[k][i + 1] < K_rowptr[k][i] || K_rowptr[k][i + 1] > nnz) {
+        ctx->err = "tk_op_create: rowptr must be non-decreasing and <= nnz";
+        return TK_EARG;
+      }
     if (nnz > 0 && (!K_col[k] || !K_val[k])) {
       ctx->err = "tk_op_create: null CSR arrays";
       return TK_EARG;
@@ -485,10 +491,6 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
       op->n_groups = T;
     }
   }
-  {
-    const char* e = getenv("TTK_SPMM_PERTERM");
-    op->spmm_perterm = e && e[0] == '1';
-  }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_kl, T_kl, sizeof(int) * T, cudaMemcpyHostToDevice));
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_ku, T_ku, sizeof(int) * T, cudaMemcpyHostToDevice));
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_off, band_off.data(), sizeof(int64_t) * (T + 1),
@@ -518,6 +520,11 @@ extern "C" int tk_op_destroy(tk_op* op) {
   return TK_OK;
 }
 extern "C" int tk_op_terms(const tk_op* op) { return op ? op->T : 0; }
+extern "C" int tk_op_set_spmm_kernel(tk_op* op, int kernel) {
+  if (!op || kernel < 0 || kernel > 1) return TK_EARG;
+  op->spmm_perterm = kernel == 1;
+  return op->recptr ? 1 - (int)op->spmm_perterm : 0;
+}
 extern "C" int tk_op_group_space(tk_op* op, int enable) {
   if (!op) return TK_EARG;
   op->group_space = enable != 0 && op->n_groups < op->T;
@@ -607,25 +614,13 @@ namespace {
 struct EigOpts {
   double abs_scale, rel;
 };
-// Pass 1 only needs an orthogonal V that diagonalises G to absolute accuracy: its skip
-// threshold sits above the rounding noise the block updates re-inject (~sqrt(64) eps ||G||),
-// otherwise rotations never stop.  Pass 2 needs relative accuracy: skip when
-// |g_pq| <= 32 eps sqrt(g_pp g_qq) (second-order effect on the eigenvalues: ~1e-29).
-const EigOpts kPass1{512 * kEps, 0.0};
+// Pass 2 needs relative accuracy: skip when |g_pq| <= 32 eps sqrt(g_pp g_qq) (second-order
+// effect on the eigenvalues: ~1e-29).
 
 // Pass 1: an exactly orthogonal basis V of R^n whose leading columns follow the dominant
-// eigenvectors of the Gram G.  Default: Q of the Householder QR of G (one orthogonal-
-// iteration step; direct, O(n^3) on DMMA).  TTK_PASS1=jacobi uses a full Jacobi
-// eigen-decomposition instead (slower; kept for comparison).
-int pass1_basis(tk_ctx* ctx, int n, const double* G, double* lam, double* V) {
-  static const bool use_jacobi = getenv("TTK_PASS1") && !strcmp(getenv("TTK_PASS1"), "jacobi");
-  if (use_jacobi) {
-    DevBuf Gc;
-    TK_TRY(Gc.get(ctx, (size_t)n * n));
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(Gc.p, G, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
-                                     ctx->stream));
-    return tk_jacobi_eig(ctx, n, Gc.p, lam, V, kPass1.abs_scale, kPass1.rel, 40, nullptr);
-  }
+// eigenvectors of the Gram G: Q of the Householder QR of G (one orthogonal-iteration step;
+// direct, O(n^3) on DMMA).  lam is unused (kept for the call sites' buffer shape).
+int pass1_basis(tk_ctx* ctx, int n, const double* G, double* /*lam*/, double* V) {
   return tk_householder_q(ctx, n, G, V);
 }
 const EigOpts kPass2{kEps * kEps, 32 * kEps};
@@ -651,8 +646,7 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
   TK_TRY(tk_dgemm(ctx, true, false, N, R, R, 1.0, A, N, V.p, R, 0.0, W.p, R));
   TK_TRY(GW.get(ctx, R * R));
   TK_TRY(tk_dgemm(ctx, true, false, R, R, N, 1.0, W.p, R, W.p, R, 0.0, GW.p, R, true));
-  static const bool jac2 = getenv("TTK_ORTH_JACOBI") != nullptr;
-  if (!jac2 && R <= tk_pchol_max_n()) {
+  if (R <= tk_pchol_max_n()) {
     // pass 2: CholeskyQR2 with diagonal pivoting on the graded W:
     //   W P1 = Q1 R1 (pivoted Cholesky of W^T W, truncated at the numerical rank k1),
     //   Q1 = W P1 R1^{-1},  Q1 = Q2 R2 (second pass: restores orthonormality to O(eps)),
@@ -750,8 +744,7 @@ int orth_rows(tk_ctx* ctx, int64_t R, int64_t N, const double* A, DevBuf& L, Dev
 // floor (out, 1 device double): rounding-noise level of G_W entries for pass 2's skip test.
 // Stride of the bond-1 pass-1 row sample (>= 8R rows, s <= 16).
 static int64_t pass1_stride(int64_t M, int64_t R) {
-  static const bool full = getenv("TTK_FULL_PASS1_GRAM") != nullptr;
-  return full ? 1 : std::max<int64_t>(1, std::min<int64_t>(16, M / (8 * R)));
+  return std::max<int64_t>(1, std::min<int64_t>(16, M / (8 * R)));
 }
 // The sampled pass-1 Gram Y_s^T Y_s (R x R) of bond 1.
 static int pass1_gram(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, double* GY) {
@@ -830,6 +823,12 @@ int cholqr_pass(tk_ctx* ctx, int64_t rows, int64_t c, const double* A, double* Q
   TK_TRY(pv.get(ctx, (c + 1) / 2));
   TK_TRY(st.get(ctx, (c + 3) / 2));
   TK_TRY(tk_pchol(ctx, (int)c, G.p, 0.0, nullptr, Ro.p, (int*)pv.p, (int*)st.p, false));
+  int rank = 0;
+  TK_TRY(sync_read(ctx, &rank, st.p, sizeof(int)));
+  if (rank < c) {  // a Schur diagonal <= 1e-300 or NaN: R is singular, R^{-1} would spread inf
+    ctx->err = "cholqr_pass: Gram not positive definite";
+    return TK_ENUMERIC;
+  }
   TK_TRY(X.get(ctx, c * c));
   TK_TRY(tk_tri_inv(ctx, (int)c, Ro.p, c, X.p, c));
   TK_TRY(tk_dgemm(ctx, false, false, rows, c, c, 1.0, A, c, X.p, c, 0.0, Q, c));
@@ -847,10 +846,9 @@ int cholqr_pass(tk_ctx* ctx, int64_t rows, int64_t c, const double* A, double* Q
 // lam (k): eigenvalues descending, then rem, then zeros; V2 (k x k): zero columns >= kc.
 // Returns TK_EARG (caller falls back to plain Jacobi) when the preconditioner does not apply.
 int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, DevBuf& lam,
-               DevBuf& V2) {
+               DevBuf& V2, int* rcap) {
   // small problems: one plain Jacobi (a single 64-wide block pair) is cheaper than two
-  static const int64_t min_k = getenv("TTK_PASS2_CHOL_MIN") ? atoi(getenv("TTK_PASS2_CHOL_MIN")) : 64;
-  if (k > tk_pchol_max_n() || k <= min_k) return TK_EARG;
+  if (k > tk_pchol_max_n() || k <= 64) return TK_EARG;
   TagScope tag(ctx, "pass2_chol");
   DevBuf Ro, pv, st, rem, X, V0, Y, nrm, V1, Qv, T1, Gp, lam2, V2p;
   TK_TRY(Ro.get(ctx, k * k));
@@ -871,9 +869,8 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
   TK_TRY(Y.get(ctx, k * kc));
   // (the refinement Jacobi of step (3) restores the full accuracy, so this one may stop as
   // soon as the couplings are small: its last, confirming sweep is left to the refinement)
-  static const double stop1 = getenv("TTK_PASS2_STOP1") ? atof(getenv("TTK_PASS2_STOP1")) : 1e-3;
-  static const bool onto_v0 = getenv("TTK_JACOBI_ONTO_V0") != nullptr;
-  if (!onto_v0 && k >= kc + 64) {
+  const double stop1 = 1e-3;
+  if (k >= kc + 64) {
     // accumulate the rotations into J (kc x kc) and apply them to V0 = R^T (k x kc) once: the
     // Jacobi's per-round tile phase then updates kc instead of k rows (fewer work items when
     // the factorisation truncated: c5 rounds k ~ 1300, kc ~ 1000)
@@ -894,7 +891,7 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
   // is already orthonormal up to ~1e-12 on the kept columns and O(0.1) overall, so one
   // CholeskyQR pass gives O(eps) orthonormality (error ~ eps cond(V1)^2).
   TK_TRY(Qv.get(ctx, k * kc));
-  TK_TRY(cholqr_pass(ctx, k, kc, V1.p, Qv.p));
+  if (cholqr_pass(ctx, k, kc, V1.p, Qv.p) != TK_OK) return TK_EARG;  // -> plain Jacobi
   TK_TRY(T1.get(ctx, k * kc));
   TK_TRY(tk_dgemm(ctx, false, false, k, kc, k, 1.0, GW.p, k, Qv.p, kc, 0.0, T1.p, kc));
   TK_TRY(Gp.get(ctx, (int64_t)kc * kc));
@@ -913,81 +910,40 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
   TK_TRY(V2.get(ctx, k * k));
   TK_TRY(tk_fill(ctx, V2.p, k * k, 0.0));
   TK_TRY(tk_dgemm(ctx, false, false, k, kc, kc, 1.0, Qv.p, kc, V2p.p, kc, 0.0, V2.p, k));
+  *rcap = kc;
   return TK_OK;
 }
 
-int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, double* lskip,
-          double rs_tol, int64_t rs_rmax, const double* floor, DevBuf& lam, DevBuf& V2,
-          DevBuf& Vt) {
-  static const bool plain = getenv("TTK_PASS2") && !strcmp(getenv("TTK_PASS2"), "jacobi");
-  if (!plain && !lskip && pass2_chol(ctx, k, GW, floor, lam, V2) == TK_OK) {
-    TK_TRY(Vt.get(ctx, k * k));
-    TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
-    return TK_OK;
+// Pass 2 of a bond SVD: the Cholesky-preconditioned variant when it applies (k > 64), else one
+// relative Jacobi on G_W.  *rcap (out): the largest admissible rank — the preconditioned
+// variant resolves only kc <= k eigenpairs (the Schur remainder `rem` of the truncated
+// Cholesky sits at lam[kc] and counts only in the discarded tail), the plain Jacobi all k.
+int pass2(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V, const double* floor,
+          DevBuf& lam, DevBuf& V2, DevBuf& Vt, int* rcap) {
+  if (pass2_chol(ctx, k, GW, floor, lam, V2, rcap) != TK_OK) {
+    TK_TRY(lam.get(ctx, k));
+    TK_TRY(V2.get(ctx, k * k));
+    TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel,
+                         kMaxSweeps, nullptr, nullptr, 0.0, 0, floor));
+    *rcap = (int)k;
   }
-  TK_TRY(lam.get(ctx, k));
-  TK_TRY(V2.get(ctx, k * k));
-  if (const char* dump = getenv("TTK_DUMP_GW")) {
-    // diagnostic: the pass-2 Gram and its noise floor, raw fp64, to <dir>/gw_<k>_<count>.bin
-    static int cnt = 0;
-    std::vector<double> h((size_t)k * k + 1);
-    TK_TRY(sync_read(ctx, h.data(), GW.p, sizeof(double) * k * k));
-    TK_TRY(sync_read(ctx, h.data() + k * k, floor, sizeof(double)));
-    char fn[512];
-    snprintf(fn, sizeof(fn), "%s/gw_%lld_%d.bin", dump, (long long)k, cnt++);
-    if (FILE* f = fopen(fn, "wb")) {
-      fwrite(h.data(), sizeof(double), h.size(), f);
-      fclose(f);
-    }
-  }
-  TK_TRY(tk_jacobi_eig(ctx, (int)k, GW.p, lam.p, V2.p, kPass2.abs_scale, kPass2.rel, kMaxSweeps,
-                       nullptr, lskip, rs_tol, rs_rmax, floor));
   TK_TRY(Vt.get(ctx, k * k));
   TK_TRY(tk_dgemm(ctx, false, false, k, k, k, 1.0, V.p, k, V2.p, k, 0.0, Vt.p, k));
   return TK_OK;
 }
 
-// pass 2 with the cluster skip and the rank-aware skip (k_jacobi.cu), then the rank rule.  If
-// the chosen rank falls inside the skipped set, or the kept set fails the Gershgorin check,
-// pass 2 is redone without any skip.
+// pass 2, then the rank rule (tk_rank_select; the chosen rank is capped at pass 2's rcap).
 int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V,
                    const DevBuf& floor, double tol, const double* delta_dev, int64_t rmax,
                    DevBuf& lam, DevBuf& V2, DevBuf& Vt, DevBuf& sig, int* info, double* dinfo,
                    int hinfo[3], double hd[3]) {
-  // The cluster skip is opt-in (TTK_CLUSTER_SKIP=1): on the c4 spectra its certificate
-  // (kept eigenvalues above the skipped block's Gershgorin/trace/Frobenius bound) fails often
-  // enough that the redo costs more than the skip saves (profiles/r01/README.md).
-  static const bool no_skip = getenv("TTK_CLUSTER_SKIP") == nullptr;
-  static const bool no_rank_skip = getenv("TTK_NO_RANK_SKIP") != nullptr;
-  DevBuf lsk;
-  double* lskip = nullptr;
-  if (tol > 0.0 && !no_skip) {
-    TK_TRY(lsk.get(ctx, 2));
-    TK_TRY(tk_cluster_skip(ctx, (int)k, GW.p, tol, lsk.p, rmax));
-    lskip = lsk.p;
-  }
   TK_TRY(sig.get(ctx, k));
-  for (int attempt = 0; attempt < 2; attempt++) {
-    TK_TRY(pass2(ctx, k, GW, V, lskip, no_rank_skip ? 0.0 : tol, rmax, floor.p, lam, V2, Vt));
-    TK_TRY(tk_rank_select(ctx, (int)k, lam.p, sig.p, tol, delta_dev, rmax, kDropThr, info, dinfo,
-                          lskip));
-    TK_TRY(sync_read(ctx, hinfo, info, 3 * sizeof(int)));
-    TK_TRY(sync_read(ctx, hd, dinfo, 3 * sizeof(double)));
-    if (!lskip) break;
-    double io[2], lam_r = 0.0;
-    TK_TRY(sync_read(ctx, io, lskip, sizeof(io)));
-    if (hinfo[0] >= 1) TK_TRY(sync_read(ctx, &lam_r, lam.p + (hinfo[0] - 1), sizeof(double)));
-    // accept iff the kept eigenvalues are all resolved and all exceed the unresolved block's
-    // largest eigenvalue (bound io[1]; -1 when nothing was skipped)
-    if (hinfo[0] <= hinfo[2] && (io[1] < 0.0 || lam_r > io[1])) break;
-    if (getenv("TTK_DEBUG"))
-      fprintf(stderr, "[ttk] skip check failed (r=%d resolved=%d lam_r=%.3e bound=%.3e): redo\n",
-              hinfo[0], hinfo[2], lam_r, io[1]);
-    lskip = nullptr;  // resolve everything
-  }
-  if (getenv("TTK_DEBUG"))
-    fprintf(stderr, "[ttk] pass2 k=%lld r=%d numerical_dim=%d resolved=%d skip=%d\n",
-            (long long)k, hinfo[0], hinfo[1], hinfo[2], lskip ? 1 : 0);
+  int rcap = (int)k;
+  TK_TRY(pass2(ctx, k, GW, V, floor.p, lam, V2, Vt, &rcap));
+  TK_TRY(tk_rank_select(ctx, (int)k, lam.p, sig.p, tol, delta_dev, rmax, kDropThr, info, dinfo,
+                        rcap));
+  TK_TRY(sync_read(ctx, hinfo, info, 3 * sizeof(int)));
+  TK_TRY(sync_read(ctx, hd, dinfo, 3 * sizeof(double)));
   return TK_OK;
 }
 
@@ -1042,20 +998,19 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
   }
   // the SpMM (HBM-bound, all SMs) overlaps the latency-bound sweep of the small cores; the
   // round joins the side stream before its first read of Y1 (bond 1)
-  static const bool serial = getenv("TTK_SERIAL") != nullptr;
   CritScope cs(ctx);  // (declared before every buffer below: joins back after they are freed)
   // opt-in exact factor grouping (tk_op_group_space): the space core is produced in the
   // factored form Y1 = Y1' E, Y1' = [K_g U1]_g over the G group representatives
   const bool grouped = op->group_space && op->n_groups < op->T;
   const int64_t R1s = (grouped ? op->n_groups : op->T) * x->r1;  // columns of the stored Y1
-  TK_TRY(apply_space_time(ctx, op, x, y, !serial, grouped));
+  TK_TRY(apply_space_time(ctx, op, x, y, true, grouped));
   DevBuf gyb;  // bond 1's sampled pass-1 Gram, also on the side stream behind the SpMM
-  if (!serial) {
+  {
     OnSide on(ctx);
     TK_TRY(gyb.get(ctx, R1s * R1s));
     TK_TRY(pass1_gram(ctx, op->n_x, R1s, y->U1, gyb.p));
   }
-  SideJoin sj(ctx, !serial);  // (round_impl joins before bond 1; this covers early returns)
+  SideJoin sj(ctx, true);  // (round_impl joins before bond 1; this covers early returns)
   DevBuf blk;
   TK_TRY(blk.get(ctx, R1 * x->n_xi * x->r2));
   {
@@ -1099,8 +1054,7 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   // NUMERICAL row rank k3 of U3 (terms sharing a time factor, e.g. T_k = I, make it exactly
   // rank-deficient: c4 k3 = 128 instead of n_t = 512), which shrinks the middle core's
   // unfolding (R1 x n_xi k3) and bond 2 four-fold for the price of one orth_rows on R2 x n_t.
-  static const bool no_orth3 = getenv("TTK_NO_ORTH3") != nullptr;
-  if (n_t > R2 || (R2 >= kOrth3MinRank && !no_orth3)) {
+  if (n_t > R2 || R2 >= kOrth3MinRank) {
     TK_TRY(orth_rows(ctx, R2, n_t, x->U3, L3b, Q3c, &k3));
     L3 = L3b.p;
     q3_id = false;
@@ -1177,15 +1131,13 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   // U1_new = W V2[:, :r1] diag(1/sig)  -> x->U1 (n_x x r1), on the side stream: the DMMA-bound
   // reconstruction overlaps the latency-bound bond-2 chain (joined before return; W and F1
   // are released only after the join)
-  static const bool serial = getenv("TTK_SERIAL") != nullptr;
   DevBuf F1;
   TK_TRY(F1.get(ctx, k2 * r1));
   TK_TRY(tk_col_scale(ctx, k2, r1, V2.p, k2, F1.p, r1, sig1.p, 1));
-  if (!serial) TK_TRY(tk_side_fork(ctx));
-  SideJoin sj(ctx, !serial);  // destroyed before F1 and W
+  TK_TRY(tk_side_fork(ctx));
+  SideJoin sj(ctx, true);  // destroyed before F1 and W
   {
-    std::unique_ptr<OnSide> on;
-    if (!serial) on.reset(new OnSide(ctx));
+    OnSide on(ctx);
     TagScope t(ctx, "bond1.form_U1");
     TK_TRY(tk_dgemm(ctx, false, false, n_x, r1, k2, 1.0, W.p, k2, F1.p, r1, 0.0, x->U1, r1));
   }
@@ -1236,7 +1188,7 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
       TK_TRY(tk_dgemm(ctx, true, true, r2, n_t, k3, 1.0, S2.p, r2, Q3c.p, k3, 0.0, x->U3, n_t));
     }
   }
-  if (!serial) TK_TRY(tk_side_join(ctx));
+  TK_TRY(tk_side_join(ctx));
   W.release();
   F1.release();
   x->r1 = r1;

@@ -28,6 +28,7 @@ struct tk_ctx {
   size_t pinned_bytes = 0;
   // profiling (tk_ctx_profile): per-launch event pairs, tagged by the current phase
   bool prof = false;
+  bool prof_timeline = false;  // tk_ctx_profile(ctx, 3): dump start offsets too
   int prof_level = 2;  // 1: only launches with >= 1e8 algorithmic flops or bytes; 2: all
   const char* tag = "misc";
   std::vector<ProfRec> recs;
@@ -114,7 +115,7 @@ struct tk_op {
   // [values (as doubles) in (column, term) order]
   int64_t* recptr = nullptr;   // n_x + 1
   int64_t* rec = nullptr;
-  bool spmm_perterm = false;   // TTK_SPMM_PERTERM=1: use the per-term kernel
+  bool spmm_perterm = false;   // tk_op_set_spmm_kernel(op, 1): use the per-term kernel
   // spatial groups (tk_op_group_space, SURVEY.md 8d "optional exact factor grouping"): terms
   // whose K_k is bitwise proportional to a representative share its group; K_k = coef[k] K_g.
   int n_groups = 0;            // number of groups (== T when nothing groups)
@@ -217,8 +218,7 @@ int tk_noise_floor(tk_ctx* ctx, const double* trG_src, int64_t n_trG, double trG
                    const double* P, int64_t nP, int64_t K, int64_t k, double* out);
 // lskip for the cluster skip: the diagonal mass of A below it is <= delta^2/4,
 // delta^2 = tol^2 trace(A)/2.
-int tk_cluster_skip(tk_ctx* ctx, int n, const double* A, double tol, double* lskip_dev,
-                    int64_t rmax = 0);
+
 
 // Q (n x n, row-major, exactly orthogonal) of the blocked Householder QR of A (n x n).
 int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q);
@@ -265,7 +265,7 @@ int tk_eye(tk_ctx* ctx, double* dst, int64_t n);
 //   info[2] = number of lam > *lskip_dev (n if lskip_dev is null).
 int tk_rank_select(tk_ctx* ctx, int n, const double* lam, double* sig, double tol,
                    const double* delta_dev_in, int64_t rmax, double kthr, int* info,
-                   double* dinfo, const double* lskip_dev = nullptr);
+                   double* dinfo, int rcap = 0);
 int tk_axpby_cores(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
                    const tk_tt* y, tk_tt* z);
 int tk_scale_rows(tk_ctx* ctx, double* U3, int64_t n, const double* s_dev, int invert);

@@ -23,7 +23,7 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round",
             "tk_apply_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle",
-            "tk_gmres_solve", "tk_op_group_space"]
+            "tk_gmres_solve", "tk_op_group_space", "tk_op_set_spmm_kernel"]
 
 
 class TkError(RuntimeError):
@@ -64,6 +64,7 @@ def lib():
     L.tk_op_destroy.argtypes = [P]
     L.tk_op_terms.argtypes = [P]
     L.tk_op_group_space.argtypes = [P, I]
+    L.tk_op_set_spmm_kernel.argtypes = [P, I]
     TTP = ctypes.POINTER(tk_tt)
     DP = ctypes.POINTER(D)
     L.tk_apply_op.argtypes = [P, P, TTP, TTP]
@@ -222,6 +223,14 @@ class Operator:
         if g < 0:
             raise TkError(g, "tk_op_group_space")
         return g
+
+    def set_spmm_kernel(self, kernel: int) -> bool:
+        """Row a1's SpMM kernel (tk_op_set_spmm_kernel): 0 = column-merged multi-term sweep
+        (default), 1 = per-term CSR kernel.  Returns True if the merged kernel will run."""
+        rc = lib().tk_op_set_spmm_kernel(self._h, int(kernel))
+        if rc < 0:
+            raise TkError(rc, "tk_op_set_spmm_kernel")
+        return rc == 1
 
     def __del__(self):
         try:

@@ -1,6 +1,10 @@
 """Full-size (BASELINE.json config c4) checks, in the launch configuration bench.py times.
 
-The CPU oracle cannot round c4 in test time (~4 minutes on 8 cores), so:
+  * apply + round, in full: the fused tk_apply_round (the call bench.py times) against the
+    oracle's apply_op + round_tt on the whole c4 input (~2 minutes of CPU): ranks identical
+    (or excused, R5), kept singular values of both bonds to 1e-10 s_1, discarded
+    norms to 1e-10 ||x||, and the reconstructed tensors to 1e-10 relative, measured as the norm
+    of the orthogonalised TT difference (R7: c4 is far too large to densify);
   * apply: sampled outputs the oracle computes one by one — rows of Y1 = [K_k U1] at random
     spatial indices, and the small cores Y2, Y3 in full — compared element by element;
   * round: properties that hold at any size — orthonormal U1 and reshape(U2), the norm
@@ -37,6 +41,29 @@ def c4():
     y = ttk.tt_apply_op(gop, ttk.TT.from_cores(*x))
     torch.cuda.synchronize()
     return cfg, op, x, gop, y
+
+
+def test_c4_apply_round_full_oracle_parity(c4):
+    """North-star parity at the headline size: GPU apply+round vs the oracle on all of c4."""
+    from tests.test_gpu_parity import ranks_excused, tt_diff_rel
+    cfg, op, x, gop, _ = c4
+    y_o = otT.apply_op(op, x)
+    o, info = otT.round_tt(y_o, cfg.tol, cfg.rmax, return_info=True)
+    del y_o
+    g, ginfo = ttk.tt_apply_round(gop, ttk.TT.from_cores(*x), cfg.tol, cfg.rmax, want_info=True)
+    assert ranks_excused(info["sigma1"], info["delta"], ginfo.ranks[0], info["ranks"][0],
+                         cfg.rmax)
+    if ginfo.ranks != info["ranks"]:  # pragma: no cover - an excused tie: nothing else unique
+        pytest.skip(f"excused rank tie {ginfo.ranks} vs {info['ranks']}")
+    s1 = info["sigma1"][0]
+    r1, r2 = info["ranks"]
+    assert np.max(np.abs(np.asarray(ginfo.sigma1[:r1]) - info["sigma1"][:r1])) <= 1e-10 * s1
+    assert np.max(np.abs(np.asarray(ginfo.sigma2[:r2]) - info["sigma2"][:r2])) <= 1e-10 * s1
+    for a, b in zip(ginfo.discarded, info["discarded"]):
+        assert abs(a - b) <= 1e-10 * info["norm"]
+    assert ginfo.norm == pytest.approx(info["norm"], rel=1e-12)
+    err = tt_diff_rel(g.cores_numpy(), o)
+    assert err <= 1e-10, err
 
 
 def test_c4_apply_sampled_rows(c4):

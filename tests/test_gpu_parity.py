@@ -45,11 +45,18 @@ def tt_diff_rel(a, b):
 
 def ranks_excused(sig, delta, r_gpu, r_orc, rmax):
     """DESIGN.md R5: a rank mismatch is a tie if the tail at the boundary is within 1e-10 ||x||
-    of delta, or if rmax binds and the singular values straddling it are within 1e-10 s_1."""
+    of delta, if rmax binds and the singular values straddling it are within 1e-10 s_1, or if
+    every singular value from the smaller rank's last kept one to the larger rank's is within
+    1e-10 s_1 of the others (the tie rule of SPEC.md:109 decides on EXACT equality, which two
+    backward-stable computations of a repeated value need not reproduce)."""
     if r_gpu == r_orc:
         return True
     nrm = np.linalg.norm(sig)
     lo = min(r_gpu, r_orc)
+    hi = max(r_gpu, r_orc)
+    run = sig[lo - 1:hi]
+    if len(run) and np.max(run) - np.min(run) <= 1e-10 * sig[0]:
+        return True
     tail = np.linalg.norm(sig[lo:])
     if abs(tail - delta) <= 1e-10 * nrm:
         return True
@@ -101,18 +108,19 @@ def test_apply_parity_random_ragged(seed, ctx):
     (16, 80, 0.6, 64, False),   # rows with > 32 distinct columns and > 256 values (unstaged)
     (9, 200, 0.02, 66, False),  # two column chunks, ragged second chunk
     (5, 150, 0.3, 7, False),    # odd r: scalar lanes
-    (6, 150, 0.3, 40, True),    # TTK_SPMM_PERTERM=1
+    (6, 150, 0.3, 40, True),    # tk_op_set_spmm_kernel(op, 1)
 ])
-def test_apply_spmm_paths(T, n_x, density, r1, perterm, ctx, monkeypatch):
+def test_apply_spmm_paths(T, n_x, density, r1, perterm, ctx):
     """Both SpMM kernels (column-merged for T <= 16, per-term otherwise or on request) and the
     merged kernel's group / staging limits, vs the oracle apply."""
-    if perterm:
-        monkeypatch.setenv("TTK_SPMM_PERTERM", "1")
     rng = np.random.default_rng(T * 1000 + n_x)
     op = random_operator(rng, n_x, 3, 5, T, density=density, max_band=1)
     x = random_tt(rng, n_x, 3, 5, r1, 2)
     y_o = otT.apply_op(op, x)
-    y_g = ttk.tt_apply_op(gpu_op(op, ctx), ttk.TT.from_cores(*x)).cores_numpy()
+    gop = gpu_op(op, ctx)
+    if perterm:
+        assert gop.set_spmm_kernel(1) is False
+    y_g = ttk.tt_apply_op(gop, ttk.TT.from_cores(*x)).cores_numpy()
     for a, b in zip(y_g, y_o):
         assert rel(a, b) <= 1e-13
 
@@ -187,6 +195,42 @@ def check_round(y_cores, tol, rmax, ctx, dense=True, gpu=None):
     m2 = u2.reshape(-1, u2.shape[2])
     assert np.max(np.abs(m2.T @ m2 - np.eye(m2.shape[1]))) <= 1e-10
     return ginfo, info
+
+
+@pytest.mark.parametrize("rmax", [0, 2, 3])
+def test_round_tie_spectrum(rmax, ctx):
+    """Exactly repeated singular values at the delta cut and at rmax (sigma = [1, .5, .5, .5, .1],
+    delta = 0.6: the tail rule gives 3, the tie rule 4, rmax caps last).  Which vectors of a
+    tied subspace are kept is not unique, so this compares what is: the ranks (equal or
+    excused by R5's tie clauses), the kept sigma, the bond-1 discarded norm, ||x~|| and — when
+    rmax cuts through the tie, where the error is unique — ||x~ - x|| to 1e-10 ||x||."""
+    rng = np.random.default_rng(77 + rmax)
+    sig = np.array([1.0, 0.5, 0.5, 0.5, 0.1])
+    n = (40, 7, 9)
+    u1 = np.linalg.qr(rng.standard_normal((n[0], 5)))[0]
+    q = np.linalg.qr(rng.standard_normal((n[1], 5)))[0]
+    w = np.linalg.qr(rng.standard_normal((n[2], 5)))[0].T
+    u2 = np.zeros((5, n[1], 5))
+    for a in range(5):
+        u2[a, :, a] = sig[a] * q[:, a]
+    x = (u1, u2, w)
+    nrm = np.linalg.norm(sig)
+    tol = 0.6 * math.sqrt(2) / nrm
+    o, info = otT.round_tt(x, tol, rmax, return_info=True)
+    g, ginfo = ttk.tt_round(ttk.TT.from_cores(*x), tol, rmax, ctx, want_info=True)
+    assert ranks_excused(info["sigma1"], info["delta"], ginfo.ranks[0], info["ranks"][0], rmax)
+    if rmax:
+        assert ginfo.ranks[0] == info["ranks"][0] == min(4, rmax)
+    assert np.max(np.abs(ginfo.sigma1[:5] - sig)) <= TOL_SIGMA
+    r1 = ginfo.ranks[0]
+    assert ginfo.discarded[0] == pytest.approx(np.linalg.norm(sig[r1:]), abs=1e-10 * nrm)
+    xf = otT.full(x)
+    e_g = np.linalg.norm(otT.full(g.cores_numpy()) - xf)
+    e_o = np.linalg.norm(otT.full(o) - xf)
+    if rmax:
+        assert abs(e_g - e_o) <= 1e-10 * nrm
+    else:
+        assert e_g <= tol * nrm * (1 + 1e-10)
 
 
 @pytest.mark.parametrize("tol", [1e-10, 1e-6, 1e-3, 0.1])

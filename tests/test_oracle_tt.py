@@ -228,3 +228,58 @@ def test_storage_ratio_paper_value():
     assert tt.storage(x) == g["tt_storage"]
     assert g["n_t"] * g["n_xi"] * g["n_x"] == g["full_storage"]
     assert round(100 * g["tt_storage"] / g["full_storage"], 1) == g["ratio_percent_printed"]
+
+
+# ----------------------------------------------------------------------------- rank rule
+# The tail rule of PAPER.md:247-249 (Alg. 2 line 4, ||E||_F <= delta) with SPEC.md:109's tie
+# rule ("keep every value equal to the last retained one") and BASELINE.json's rmax cap
+# applied LAST: r = min(r_tie(r_delta), rmax).  Exact spectra with repeated values at the cut.
+_SIG_TIE = np.array([1.0, 0.5, 0.5, 0.5, 0.1])   # tails: ||s[1:]|| = .8718, ||s[2:]|| = .7141,
+                                                  #        ||s[3:]|| = .5099, ||s[4:]|| = .1
+
+
+@pytest.mark.parametrize("delta,rmax,expect", [
+    (0.6, 0, 4),     # r_delta = 3 (tail .5099 <= .6) -> tie s[3] == s[2] extends to 4
+    (0.72, 0, 4),    # r_delta = 2 -> ties extend 2 -> 3 -> 4
+    (0.9, 0, 1),     # r_delta = 1, s[1] = .5 != s[0]: no tie
+    (0.05, 0, 5),    # nothing may be dropped
+    (0.1, 0, 4),     # tail after 4 == delta exactly: kept (<=), s[4] != s[3]
+    (0.6, 3, 3),     # rmax caps AFTER the tie loop: min(4, 3)
+    (0.72, 2, 2),    # min(4, 2)
+    (0.9, 3, 1),     # rmax larger than the rule: no effect
+    (0.6, 9, 4),     # rmax beyond n
+])
+def test_rank_rule_ties_and_rmax_closed_form(delta, rmax, expect):
+    assert tt.rank_rule(_SIG_TIE, delta, rmax) == expect
+
+
+def test_rank_rule_tie_only_extends_over_equal_values():
+    # a near-tie (1 ulp apart) is not a tie
+    s = np.array([1.0, 0.5, np.nextafter(0.5, 0.0), 0.1])
+    assert tt.rank_rule(s, math.sqrt(0.5 ** 2 + 0.01) + 1e-12, 0) == 2
+    # a tie at the very end keeps everything
+    s = np.array([1.0, 0.25, 0.25])
+    assert tt.rank_rule(s, 0.3, 0) == 3
+    # r >= 1 even for delta >= ||s|| and the empty spectrum
+    assert tt.rank_rule(np.array([0.3, 0.2]), 10.0, 0) == 1
+    assert tt.rank_rule(np.array([]), 1.0, 0) == 1
+
+
+@pytest.mark.parametrize("rmax", [0, 2, 3])
+def test_round_tie_spectrum_through_round_tt(rng, rmax):
+    """round_tt on a TT whose unfoldings have EXACTLY repeated singular values.  Computed
+    repeated values are equal only up to rounding, so the space rank is pinned up to the tie
+    (3 or 4 without rmax, exactly rmax when it binds); the bond-1 discarded norm is the
+    closed-form tail of the chosen rank, and the PAPER.md:252-258 bound holds when rmax does
+    not bind (which vectors of a tied subspace are kept is not unique)."""
+    sig = np.array([1.0, 0.5, 0.5, 0.5, 0.1])
+    x = _diag_tt(rng, 30, 12, 9, sig)
+    nrm = np.linalg.norm(sig)
+    tol = 0.6 * math.sqrt(2) / nrm          # delta = 0.6 -> rank 4 (tie rule), or 3 if capped
+    xr, info = tt.round_tt(x, tol, rmax=rmax, return_info=True)
+    r = tt.ranks(xr)[0]
+    assert r in ({3, 4} if rmax == 0 else {min(4, rmax)})
+    assert info["discarded"][0] == pytest.approx(np.linalg.norm(sig[r:]), abs=1e-14)
+    assert np.max(np.abs(info["sigma1"][:5] - sig)) <= 1e-14
+    if rmax == 0:
+        assert np.linalg.norm(tt.full(xr) - tt.full(x)) <= tol * nrm * (1 + 1e-12)

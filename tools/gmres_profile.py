@@ -1,4 +1,4 @@
-"""Per-phase device time and host-side gaps of one c5 low-rank GMRES cycle (TTK_TIMELINE=1):
+"""Per-phase device time and host-side gaps of one c5 low-rank GMRES cycle (tk_ctx_profile(ctx, 3)):
 where a Krylov step's time goes.  usage: python tools/gmres_profile.py"""
 import collections
 import ctypes
@@ -6,7 +6,6 @@ import os
 import sys
 import time
 
-os.environ["TTK_TIMELINE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -25,7 +24,7 @@ bg = ttk.TT.from_cores(*b)
 ttk.gmres_cycle(gop, bg, 4, cfg.tol)
 torch.cuda.synchronize()
 L = ttkmod.lib()
-L.tk_ctx_profile(ctx._h, 1)
+L.tk_ctx_profile(ctx._h, 3)
 t0 = time.perf_counter()
 res = ttk.gmres_cycle(gop, bg, cfg.gmres_steps, cfg.tol)
 torch.cuda.synchronize()

@@ -1,11 +1,10 @@
-"""Print the library's per-kernel timeline of ONE c4 apply+round (TTK_TIMELINE=1 profiling dump):
+"""Print the library's per-kernel timeline of ONE c4 apply+round (tk_ctx_profile(ctx, 3) profiling dump):
 start offset, duration and phase of every profiled launch, to see what overlaps and where the
 GPU idles on the latency-bound chain.  usage: python tools/timeline.py [config] > out.txt"""
 import ctypes
 import os
 import sys
 
-os.environ["TTK_TIMELINE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -25,7 +24,7 @@ ycap = ttk.TT(op.n_x, op.n_xi, op.n_t, op.T * xg.r1, op.T * xg.r2)
 L = ttkmod.lib()
 for i in range(3):
     if i == 2:
-        L.tk_ctx_profile(ctx._h, 1)
+        L.tk_ctx_profile(ctx._h, 3)
     ttk.tt_apply_round(gop, xg, cfg.tol, cfg.rmax, out=ycap)
     torch.cuda.synchronize()
 buf = ctypes.create_string_buffer(1 << 24)
