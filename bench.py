@@ -114,24 +114,32 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# DRAM traffic of the largest dgemm launch from one `ncu --set full` capture (the per-launch
-# average over all dgemm launches is not captured, so `traffic` stays null and the capture is
-# quoted beside it): profiles/r01/ncu_dgemm_formW.txt
-DGEMM_TRAFFIC = {
-    "note": "DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) of the dominant "
-            "dgemm launches of one c4 step vs their algorithmic bytes; the roofline's 'traffic' "
-            "stays null because 'achieved' averages ~45 heavy launches of mixed shapes",
-    "form_W (786432 x 640 x 896)": {"dram_bytes": 9.64e9, "algorithmic_bytes": 9.67e9, "ms": 26.98},
-    "gram_W (640 x 640 x 786432, sym, split-K 32)": {"dram_bytes": 6.61e9,
-                                                     "algorithmic_bytes": 4.03e9, "ms": 10.89},
-    "form_U1 (786432 x 160 x 640)": {"dram_bytes": 5.03e9, "algorithmic_bytes": 5.03e9, "ms": 5.07},
-    "source": "profiles/r01/dgemm_traffic_h.csv (+ .json), profiles/r01/ncu_d_formW.txt"}
+# FP64 tensor-pipe (DMMA) ceiling MEASURED on this pool's B200: tools/ubench/dmma_peak.cu
+# (register-only mma.sync m8n8k4 f64 chains, 296 CTAs, >= 16 warps/SM; 37.07-37.15 TF/s at
+# 1965 MHz with no throttle reason; profiles/r02/dmma_peak.txt).  tcgen05 has no f64 kind, so
+# this is the fp64 tensor roofline of every DMMA GEMM of the rounding.
+DMMA_PEAK = {"tflops": 37.15,
+             "source": "measured DMMA ubench (tools/ubench/dmma_peak.cu, register-only "
+                       "mma.sync m8n8k4 f64, 1965 MHz; profiles/r02/dmma_peak.txt)"}
 
 
-# FP64 tensor-pipe ceiling measured on this pool's B200 (register-only DMMA m8n8k4 chains,
-# >= 8 warps/SM, 1965 MHz): tools/ubench/dmma_peak.cu.  Stricter than the rule-derived peak
-# (bf16 measured x 45/2250 = 32.5), so both fractions are reported.
-DMMA_PEAK_MEASURED = 37.1
+def dgemm_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant
+    kernel's heavy launches from one ncu capture of one c4 step (profiles/r02/)."""
+    p = os.path.join(ROOT, "profiles", "r02", "dgemm_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def algorithmic_round_flops(op, cfg, ranks_out):
+    """SURVEY.md 8(d) algorithmic FLOPs of one apply+round on the Gram path: the Gram of the
+    grown space core (n_x R1^2), its reconstruction (2 n_x R1 r1'), the Gram of the middle
+    unfolding (R1^2 n_xi min(R2, n_t)) and of the time core (R2^2 n_t)."""
+    R1, R2 = op.T * cfg.ranks[0], op.T * cfg.ranks[1]
+    return (op.n_x * R1 * R1 + 2.0 * op.n_x * R1 * ranks_out[0]
+            + R1 * R1 * op.n_xi * min(R2, op.n_t) + R2 * R2 * op.n_t)
 
 
 def load_peaks():
@@ -161,66 +169,114 @@ def time_oracle_op(op, x, cfg):
     return t2 - t0, t1 - t0, t2 - t1
 
 
-ROW_SAMPLE = {"c4": 8}  # configs whose full oracle op exceeds the ~30 s CPU budget
+# configs whose full oracle op is too long for one --impl reference STEP (c4: ~100 s on 16
+# cores): each reference step is then a bounded sample (oracle_sample_step)
+SAMPLED = {"c4": (16, 8)}
 
 
-def oracle_sample_op(op, x, cfg):
-    """One bounded CPU-oracle sample of the config's op.  Full op for c1..c3.  For c4 (a full
-    oracle op is ~4 minutes on 8 cores): the full apply, then the full rounding algorithm on the
-    applied TT restricted to the first n_x/8 spatial rows; the round time is scaled by 8 (its
-    dominant cost, the Householder QR of the n_x x 896 core, is linear in n_x; the small-core
-    work does not shrink, so the estimate is conservative).  Returns (seconds_per_op, text)."""
+def _round_input_sample(y, f_inv):
+    """The applied TT restricted to its first n_x/f_inv spatial rows and first n_xi/f_inv
+    chaos indices: the same rounding algorithm on a proportionally smaller middle and space
+    core (every n_x- or n_xi-proportional cost of the oracle round shrinks by f_inv; the
+    O(R^3) small SVDs do not)."""
+    rows = y[0].shape[0] // f_inv
+    nxi = max(1, y[1].shape[1] // f_inv)
+    return (np.ascontiguousarray(y[0][:rows]), np.ascontiguousarray(y[1][:, :nxi, :]), y[2])
+
+
+def oracle_sample_step(op, x, cfg, y_cache, f_inv):
+    """One --impl reference step of a SAMPLED config: the full oracle apply (timed), then the
+    full rounding algorithm on the 1/f_inv row+chaos sample of its output.  Returns
+    (measured seconds, apply seconds, round-sample seconds)."""
     from oracle import tt as otT
-    f = ROW_SAMPLE.get(cfg.name)
-    if not f:
-        dt, _, _ = time_oracle_op(op, x, cfg)
-        return dt, f"1 full {cfg.name} apply+round op"
     t0 = time.perf_counter()
     y = otT.apply_op(op, x)
     ta = time.perf_counter() - t0
-    rows = op.n_x // f
-    ys = (np.ascontiguousarray(y[0][:rows]), y[1], y[2])
+    ys = _round_input_sample(y, f_inv)
+    del y
     t0 = time.perf_counter()
     otT.round_tt(ys, cfg.tol, cfg.rmax)
     tr = time.perf_counter() - t0
-    return ta + f * tr, (f"full {cfg.name} oracle apply ({ta:.1f} s) + oracle round on the first "
-                         f"n_x/{f} = {rows} spatial rows ({tr:.1f} s) scaled x{f}")
+    return ta + tr, ta, tr
 
 
 def cpu_baseline(cfg, op, x):
+    """The oracle as it stands on ONE full op of the workload (no sampling, no extrapolation:
+    ~100 s on 16 cores at c4), plus a single-thread figure on the reference arm's bounded
+    sample (1/16 of n_x and n_xi; the time of that sample, not an op rate)."""
     cores = cpu_cores_used()
-    dt, what = oracle_sample_op(op, x, cfg)
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{what}; NumPy/SciPy OpenBLAS, {cores} threads; {dt:.1f} s/op"}
+    dt, ta, tr = time_oracle_op(op, x, cfg)
+    out = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"1 full {cfg.name} oracle apply ({ta:.1f} s) + round ({tr:.1f} s), "
+                     f"NumPy/SciPy OpenBLAS, {cores} threads: {dt:.1f} s/op, measured "
+                     f"(not extrapolated)"}
+    if cfg.name in SAMPLED:
+        try:
+            from threadpoolctl import threadpool_limits
+            f_inv = SAMPLED[cfg.name][0]
+            with threadpool_limits(limits=1):
+                t1, a1, r1 = oracle_sample_step(op, x, cfg, None, f_inv)
+            out["single_thread"] = {
+                "seconds": t1, "cores": 1,
+                "sample": f"full {cfg.name} oracle apply ({a1:.1f} s) + round of the first "
+                          f"1/{f_inv} of n_x and n_xi ({r1:.1f} s), BLAS limited to 1 thread"}
+        except Exception as e:  # pragma: no cover
+            out["single_thread"] = {"error": str(e)}
+    return out
 
 
 def run_reference(args, cfg, op, x):
+    """--impl reference: the oracle on this host's cores, W warm-up + K timed steps.  Configs
+    whose full op fits a step run it in full; c4 (SAMPLED) alternates the 1/16 and 1/8
+    row+chaos samples of the round (oracle_sample_step).  Its op time is then EXTRAPOLATED
+    with the affine model t_round(f) = a + b f fitted to the two sample sizes of this run
+    (t_op = t_apply + t_round(f) + b (1 - f) per step), which ignores the oracle's slowdown on
+    the full-size arrays and so OVERSTATES its rate (a measured full op is the main arm's
+    cpu_baseline).  ms_per_step is the measured sample time."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    budget = 150.0
-    # one untimed warm-up sample (page-in, BLAS thread pool), then bounded timed samples: every
-    # step is one oracle sample of the workload (oracle_sample_op); steps stop at ~150 s
-    oracle_sample_op(op, x, cfg)
-    times = []
-    what = ""
-    t_start = time.perf_counter()
-    for k in range(args.steps):
-        dt, what = oracle_sample_op(op, x, cfg)
-        times.append(dt)
-        if time.perf_counter() - t_start > budget:
-            break
-    total = sum(times)
-    v = len(times) / total
+    oop = op.oracle_op()
     cores = cpu_cores_used()
+    samp = SAMPLED.get(cfg.name)
+    meas, ext, what = [], [], ""
+    if not samp:
+        for _ in range(args.warmup):
+            time_oracle_op(oop, x, cfg)
+        for _ in range(args.steps):
+            dt, _, _ = time_oracle_op(oop, x, cfg)
+            meas.append(dt)
+        ext = list(meas)
+        what = f"1 full {cfg.name} oracle apply+round op per step (measured)"
+    else:
+        f_lo, f_hi = samp
+        for _ in range(args.warmup):
+            oracle_sample_step(oop, x, cfg, None, f_hi)
+        rec = []
+        for k in range(args.steps):
+            f_inv = f_lo if k % 2 == 0 else f_hi
+            dt, ta, tr = oracle_sample_step(oop, x, cfg, None, f_inv)
+            meas.append(dt)
+            rec.append((1.0 / f_inv, ta, tr))
+        lo = [r for f, _, r in rec if f == 1.0 / f_lo]
+        hi = [r for f, _, r in rec if f == 1.0 / f_hi]
+        b = 0.0
+        if lo and hi:
+            b = max(0.0, (statistics.mean(hi) - statistics.mean(lo)) / (1.0 / f_hi - 1.0 / f_lo))
+        ext = [ta + tr + b * (1.0 - f) for f, ta, tr in rec]
+        what = (f"per step: the full {cfg.name} oracle apply + the oracle round of the first "
+                f"1/{f_lo} (even steps) or 1/{f_hi} (odd steps) of n_x and n_xi; op time "
+                f"extrapolated as t_apply + t_round(f) + b (1 - f), b = {b:.1f} s fitted to "
+                f"the two sample sizes (affine model, overstates the oracle's rate)")
+    v = len(ext) / sum(ext)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(meas),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(cfg, op),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{len(times)} x [{what}], NumPy/SciPy OpenBLAS, {cores} "
-                                   f"threads; capped at ~{budget:.0f}s"},
+                         "sample": f"{what}; NumPy/SciPy OpenBLAS, {cores} threads; "
+                                   f"measured {statistics.mean(meas):.1f} s per step"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -264,7 +320,7 @@ def run_ours(args, cfg, op, x):
 
     stream = torch.cuda.current_stream()
     ctx = ttk.default_context()
-    gop = ttk.Operator.from_kronsum(op, ctx)
+    gop = op.gpu_op(ctx)
     groups = gop.group_space(True) if args.group_space else None
     xg = ttk.TT.from_cores(*x)
     T = op.T
@@ -337,7 +393,7 @@ def run_ours(args, cfg, op, x):
         d[2] += float(fl)
         d[3] += float(by)
     peaks, peak_kind = load_peaks()
-    fp64_peak = peaks["bf16_tflops"] * (45.0 / 2250.0)  # bf16 measured x nominal fp64/bf16 ratio
+    fp64_peak = DMMA_PEAK["tflops"]
     # group the phase records by KERNEL FUNCTION: every phase tag that is not one of the
     # named kernels below is a launch of the DMMA GEMM (dgemm_kernel + its split-K reduce)
     named = {"jacobi": "jacobi_persistent_k", "qr_panel": "qr_panel_warp_k",
@@ -362,17 +418,22 @@ def run_ours(args, cfg, op, x):
         avg_ms = ms / cnt
         if fl > 0 and (fl / by) > 6.0:
             ach = fl / cnt / (avg_ms * 1e-3) / 1e12
+            alg = algorithmic_round_flops(op, cfg, ranks_out)
+            tr = dgemm_traffic() if cfg.name == "c4" and not args.group_space else None
             roofline = {"kernel": cat, "bound": "tensor", "achieved": ach, "peak": fp64_peak,
-                        "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
-                        "traffic_capture": DGEMM_TRAFFIC,
-                        "peak_dmma_measured": DMMA_PEAK_MEASURED,
-                        "frac_vs_measured_dmma": ach / DMMA_PEAK_MEASURED,
-                        "peak_source": f"bf16 {peak_kind} {peaks['bf16_tflops']} x 45/2250 (fp64 DMMA nominal ratio)",
+                        "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                        "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                        "traffic_capture": tr,
+                        "peak_source": DMMA_PEAK["source"],
                         "launches": cnt, "avg_ms": avg_ms, "share_of_step": ms / total_ms,
                         "launches_recorded": "timed region, launches >= 1e8 flops or bytes",
                         "achieved_all_launches": dom[1][2] / (dom[1][1] * 1e-3) / 1e12,
                         "launches_all_per_step": dom[1][0] / full_steps,
-                        "share_of_step_all_launches": ms_all / (total_ms / args.steps)}
+                        "share_of_step_all_launches": ms_all / (total_ms / args.steps),
+                        # SURVEY 8(d) algorithmic FLOPs of the whole op (Gram path) over the
+                        # whole step time: what the method needs vs what the step delivers
+                        "algorithmic_flops_per_op": alg,
+                        "frac_algorithmic": alg / (total_ms / args.steps * 1e-3) / 1e12 / fp64_peak}
         elif by > 0:
             ach = by / cnt / (avg_ms * 1e-3) / 1e9
             roofline = {"kernel": cat, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
@@ -453,7 +514,7 @@ def run_ours(args, cfg, op, x):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, op, x)
+        cpu = cpu_baseline(cfg, op.oracle_op(), x)
 
     if args.breakdown and rank == 0:
         for cat, (cnt, ms, fl, by) in sorted(phases.items(), key=lambda kv: -kv[1][1]):
@@ -526,7 +587,7 @@ def run_gmres(args, cfg, op):
     b = make_rhs_tt(cfg, op.n_xi)
     if args.impl == "reference":
         if rank == 0:
-            v, what = oracle_sample_gmres(op, b, cfg, budget=120.0)
+            v, what = oracle_sample_gmres(op.oracle_op(), b, cfg, budget=120.0)
             cores = cpu_cores_used()
             print(json.dumps({
                 "impl": "reference", "metric": GMRES_METRIC, "value": v, "unit": GMRES_UNIT,
@@ -540,7 +601,7 @@ def run_gmres(args, cfg, op):
         return
     stream = torch.cuda.current_stream()
     ctx = ttk.default_context()
-    gop = ttk.Operator.from_kronsum(op, ctx)
+    gop = op.gpu_op(ctx)
     bg = ttk.TT.from_cores(*b)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
@@ -597,7 +658,7 @@ def run_gmres(args, cfg, op):
            "steps": 1}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, what = oracle_sample_gmres(op, b, cfg)
+        v, what = oracle_sample_gmres(op.oracle_op(), b, cfg)
         cores = cpu_cores_used()
         cpu = {"value": v, "unit": GMRES_UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{what}; NumPy/SciPy OpenBLAS, {cores} threads"}
@@ -623,13 +684,53 @@ def run_gmres(args, cfg, op):
         tdist.destroy_process_group()
 
 
+class Workload:
+    """The config's operator: a host descriptor (c1..c5, built by synth) or, for the NEXT-1
+    convection config c6, the discretisation + velocity TT from which the LIBRARY builds N(u)
+    on the device (tk_op_convection) and the oracle builds its own eq:N_kron operator."""
+
+    def __init__(self, cfg):
+        from synth import gpc
+        from synth.operator import build_operator, convection_stencils
+        from synth.tt import make_velocity_tt
+        self.cfg = cfg
+        self._oracle = None
+        if cfg.operator == "convection":
+            self.H = gpc.h_matrices(cfg.m, cfg.p)
+            self.D, self.n_v = convection_stencils(cfg.grid)
+            self.u = make_velocity_tt(cfg, len(self.H))
+            self.host = None
+            self.n_x, self.n_xi, self.n_t = cfg.n_x, len(self.H), cfg.n_t
+            self.T = cfg.n_terms
+        else:
+            self.host = build_operator(cfg)
+            self.n_x, self.n_xi, self.n_t, self.T = (self.host.n_x, self.host.n_xi,
+                                                     self.host.n_t, self.host.T)
+
+    def gpu_op(self, ctx):
+        import paper_1906_06785_b200 as ttk
+        if self.host is not None:
+            return ttk.Operator.from_kronsum(self.host, ctx)
+        self._conv = ttk.Convection(self.n_x, self.n_xi, self.n_t, self.D, self.n_v,
+                                    np.stack(self.H), ctx)
+        self._u_dev = ttk.TT.from_cores(*self.u)
+        return self._conv.operator(self._u_dev)   # N(u) built on the device
+
+    def oracle_op(self):
+        if self.host is not None:
+            return self.host
+        if self._oracle is None:
+            from oracle.convection import convection_operator
+            self._oracle = convection_operator(*self.u, self.H, self.D, self.n_v)
+        return self._oracle
+
+
 def main():
     args = parse()
     from synth.configs import CONFIGS
-    from synth.operator import build_operator
     from synth.tt import make_input_tt
     cfg = CONFIGS[args.config]
-    op = build_operator(cfg)
+    op = Workload(cfg)
     if cfg.name == "c5":
         run_gmres(args, cfg, op)
         return

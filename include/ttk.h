@@ -49,6 +49,7 @@ enum {
 
 typedef struct tk_ctx tk_ctx;
 typedef struct tk_op tk_op;
+typedef struct tk_conv tk_conv;
 
 typedef struct {
   int64_t n_x, n_xi, n_t; /* mode sizes (space, stochastic, time)                          */
@@ -110,6 +111,37 @@ int tk_op_set_spmm_kernel(tk_op* op, int kernel);
  * rounding order, fewer flops.  tk_apply_op and tk_round are unaffected.  Returns G (== T when
  * nothing groups; enabling is then a no-op) or TK_EARG. */
 int tk_op_group_space(tk_op* op, int enable);
+
+/* Concatenation A = sum_i A_i of n >= 1 operators with equal mode sizes: the terms of
+ * ops[0], then ops[1], ... (e.g. the Picard matrix F(u) + C = fixed terms + N(u),
+ * PAPER.md:157-161).  Device arrays are copied (the inputs may be destroyed afterwards).
+ * TK_ESHAPE if the mode sizes differ.  Synchronous (setup). */
+int tk_op_concat(tk_ctx* ctx, int n, const tk_op* const* ops, tk_op** out);
+
+/* NEXT-1: the TT-format convection operator of eq:N_kron, built on the
+ * device from a device-resident velocity TT.
+ *
+ * tk_conv_create fixes the discretisation once: the spatial mode is [v_1; ...; v_d; rest]
+ * with d velocity components of n_v dofs each (d n_v <= n_x; rows >= d n_v, e.g. the
+ * pressure, do not convect), D_c (c < d) are the n_v x n_v difference operators of the
+ * convective derivative (HOST CSR, int32, 0-based; every row of their union pattern has
+ * <= 32 distinct columns), and H (HOST, n_xi^3 doubles, H[(l n_xi + r) n_xi + s] =
+ * <psi_l psi_r psi_s>) the chaos triple products.  Copied to the device.
+ *
+ * tk_op_convection builds, for the velocity TT u (DEVICE cores, modes (n_x, n_xi, n_t)),
+ *   N(u) = sum_{a < u.r1, b < u.r2} diag(U3[b, :]) (x) (sum_l U2[a, l, b] H_l) (x) N(U1[:, a])
+ *   N(w) = blkdiag_{s < d}( sum_c diag(w_c) D_c ),  w_c = w[c n_v : (c+1) n_v]
+ * (this repo's core order, R18): u.r1 u.r2 terms, term k = a u.r2 + b, the
+ * kappa -> kappa^2 growth of PAPER.md:331.  Values are computed by kernels from u's device
+ * cores (no host round trip of u); the result is an ordinary operator (tk_apply_op,
+ * tk_apply_round, tk_op_concat, tk_op_destroy), whose SpMM computes each N(U1[:, a]) U1
+ * product once and writes it to the u.r2 blocks of its terms.  It has no per-term CSR
+ * (tk_op_set_spmm_kernel(op, 1) returns TK_EARG).  Asynchronous except for the allocations. */
+int tk_conv_create(tk_ctx* ctx, tk_conv** conv, int64_t n_x, int64_t n_xi, int64_t n_t, int d,
+                   int64_t n_v, const int32_t* const* D_rowptr, const int32_t* const* D_col,
+                   const double* const* D_val, const double* H);
+int tk_conv_destroy(tk_conv* conv);
+int tk_op_convection(tk_ctx* ctx, const tk_conv* conv, const tk_tt* u, tk_op** op);
 
 /* y = A x   (PAPER.md:239-244 eq:Xz).  Per term k: K_k U1, G_k x_2 U2,
  * U3 T_k^T; terms are concatenated: y ranks = (T*x.r1, T*x.r2), y.U1 = [K_0 U1 | ... ],

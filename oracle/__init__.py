@@ -19,5 +19,5 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   * gmres.gmres_cycle at tol 1e-6: parity unpinned beyond GPU-vs-oracle agreement
   * gpc_quadrature.h_by_quadrature vs the closed-form H_l (synth.gpc), H_1 = I, H_{e_i} = G_i
   * convection.dense_convection (the definition) vs the Kronecker-sum N(u)
-                     of eq:N_kron built by synth.operator.convection_operator        — exact
+                     of eq:N_kron (convection.convection_operator); n_of vs w.grad f  — exact
 """

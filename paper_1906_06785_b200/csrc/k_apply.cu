@@ -171,12 +171,23 @@ __global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm
 // computed, the record of the warp's next row (RW words per lane, one coalesced load) and the
 // record pointer of the row after it are already in flight, so the dependent global loads
 // (pointer -> record) leave the critical path; only the U1 row gathers (L2) remain on it.
-template <int TM, bool V2>
-__global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int r,
+//
+// Output map.  The records merge the op's spatial GROUPS (terms with bitwise-proportional K_k
+// share a group, and so do the r2 terms of the convection operator that share N(u_a)), at
+// most TM per launch (a chunk of the op's groups).  MAP == false: the chunk's groups ARE
+// terms k0 .. k0+nout-1 (coefficient 1).  MAP == true: the per-group products are staged in
+// shared memory and every term t < nout of the chunk's term list is written as
+// Y1[:, tk[t] r : (tk[t]+1) r] = tc[t] * (K_{group tg[t]} U1): the products are computed once
+// per group, the T r outputs (the HBM-bound part) are still all written.  R = row stride of Y1.
+template <int TM, bool V2, bool MAP>
+__global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int nout, int r, int64_t R,
                                                        const int64_t* __restrict__ recptr,
                                                        const long long* __restrict__ rec,
                                                        const double* __restrict__ U1,
-                                                       double* __restrict__ Y1) {
+                                                       double* __restrict__ Y1, int k0,
+                                                       const int* __restrict__ tk,
+                                                       const int* __restrict__ tg,
+                                                       const double* __restrict__ tc) {
   static_assert(TM % 2 == 0, "TM even (16-byte value loads)");
   constexpr int RPL = V2 ? 2 : 1;
   constexpr int CW = 32 * RPL;
@@ -186,7 +197,6 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t R = (int64_t)T * r;
   // per warp: the staged record, dense values [distinct column][term pair] and the distinct
   // columns (<= 32 per row: the host routes longer merged rows to the per-term kernel)
   __shared__ long long rec_all[256 / 32][32 * RW];
@@ -241,7 +251,10 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
     }
     off -= cnt;
     const int gp = (gn + UNR - 1) / UNR * UNR;  // padded to the unroll: pad slots hold zeros
-    if (lane < gp) {  // lane j: dense, zero-padded values of distinct column j
+    double* yrow = Y1 + row * R;
+    for (int c0 = 0; c0 < r; c0 += CW) {
+    // (MAP: vd doubles as the staging buffer of the products, so it is re-expanded per chunk)
+    if ((MAP || c0 == 0) && lane < gp) {  // lane j: dense, zero-padded values of distinct column j
       const int64_t v0 = 1 + gn + off;
       // staged record, or (rows longer than 32 RW words) straight from global
       const long long* src = (p1 - p0 <= 32 * RW) ? rs + v0 : rec + p0 + v0;
@@ -256,8 +269,6 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
       cols[lane] = lane < gn ? (int)(w & 0xffffffffLL) : 0;
     }
     __syncwarp();
-    double* yrow = Y1 + row * R;
-    for (int c0 = 0; c0 < r; c0 += CW) {
       const int cc = c0 + (V2 ? 2 * lane : lane);
       const bool okc = cc < r;
       const double* ub = U1 + (okc ? cc : 0);
@@ -292,11 +303,22 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int T, int 
           }
         }
       }
-      if (okc) {
-        double* dst = yrow + cc;
+      if (MAP) {
+        static_assert(!MAP || !V2, "MAP: scalar lanes");
+        __syncwarp();  // every lane is done reading vd: reuse it as [TM][32] staging
+        double(*st)[32] = reinterpret_cast<double(*)[32]>(&vd[0][0]);
+#pragma unroll
+        for (int k = 0; k < TM; k++) st[k][lane] = acc[k][0];
+        __syncwarp();
+        if (okc)
+          for (int t = 0; t < nout; t++)
+            __stcs(yrow + (int64_t)__ldg(tk + t) * r + cc, __ldg(tc + t) * st[__ldg(tg + t)][lane]);
+        __syncwarp();
+      } else if (okc) {
+        double* dst = yrow + (int64_t)k0 * r + cc;
 #pragma unroll
         for (int k = 0; k < TM; k++) {
-          if (k < T) {
+          if (k < nout) {
             if (V2)
               __stcs((double2*)dst, make_double2(acc[k][0], acc[k][RPL - 1]));
             else
@@ -365,52 +387,55 @@ __global__ void time_apply_k(int T, int r2, int n_t, const int* __restrict__ kl,
 int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, double* Y1,
                          bool grouped) {
   const int64_t n_x = op->n_x;
-  if (grouped) {
-    // the representatives of the spatial groups only (tk_op_group_space): Y1' = [K_g U1]_g
-    tk_op g = *op;
-    g.T = op->n_groups;
-    g.recptr = op->g_recptr;
-    g.rec = op->g_rec;
-    g.spmm_perterm = false;
-    g.n_groups = 0;
-    g.g_recptr = nullptr;
-    g.g_rec = nullptr;
-    const int st = tk_launch_spmm_multi(ctx, &g, r, U1, Y1, false);
-    // g's vectors are copies; nothing to free (the device arrays belong to op)
-    return st;
-  }
   const int threads = 256;
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
-
-  if (op->rec && !op->spmm_perterm) {
+  if (grouped && op->chunks.empty()) {
+    ctx->err = "spmm: group-space output needs the merged kernel";
+    return TK_EARG;
+  }
+  if (!op->chunks.empty() && (grouped || !op->spmm_perterm)) {
+    // column-merged kernel, one launch per chunk of <= 16 groups.  grouped: the group
+    // representatives only (tk_op_group_space), Y1' = [K_g U1]_g with row stride G r.
     blocks = std::min<int64_t>((n_x * 32 + threads - 1) / threads, 16LL * ctx->num_sms);
-    // scalar lanes (two 32-column chunks at r = 64) measured faster than 16-byte lanes: the
-    // 2x accumulators of the 16-byte variant halve the resident warps
-    const bool v2m = false;
-#define TK_SPMM_M(TM, V)                                                                    \
-  spmm_merged_k<TM, V><<<(unsigned)blocks, threads, 0, ctx->stream>>>(                      \
-      n_x, op->T, r, op->recptr, (const long long*)op->rec, U1, Y1)
-    if (op->T <= 2) {
-      if (v2m) TK_SPMM_M(2, true); else TK_SPMM_M(2, false);
-    } else if (op->T <= 4) {
-      if (v2m) TK_SPMM_M(4, true); else TK_SPMM_M(4, false);
-    } else if (op->T <= 6) {
-      if (v2m) TK_SPMM_M(6, true); else TK_SPMM_M(6, false);
-    } else if (op->T <= 8) {
-      if (v2m) TK_SPMM_M(8, true); else TK_SPMM_M(8, false);
-    } else if (op->T <= 10) {
-      if (v2m) TK_SPMM_M(10, true); else TK_SPMM_M(10, false);
-    } else if (op->T <= 12) {
-      if (v2m) TK_SPMM_M(12, true); else TK_SPMM_M(12, false);
-    } else if (op->T <= 14) {
-      if (v2m) TK_SPMM_M(14, true); else TK_SPMM_M(14, false);
-    } else {
-      if (v2m) TK_SPMM_M(16, true); else TK_SPMM_M(16, false);
-    }
+    const int64_t R = (int64_t)(grouped ? op->n_groups : op->T) * r;
+    for (const SpmmChunk& c : op->chunks) {
+      const bool map = !grouped && !c.ident;
+      const int nout = grouped ? c.ng : (c.ident ? c.ng : c.nterm);
+      const int k0 = c.g0;
+      const int tm = c.ng;
+#define TK_SPMM_M(TM, MP)                                                                   \
+  spmm_merged_k<TM, false, MP><<<(unsigned)blocks, threads, 0, ctx->stream>>>(              \
+      n_x, nout, r, R, c.recptr, (const long long*)c.rec, U1, Y1, k0, c.tk, c.tg, c.tc)
+#define TK_SPMM_T(TM)            \
+  if (map) TK_SPMM_M(TM, true);  \
+  else TK_SPMM_M(TM, false);
+      if (tm <= 2) {
+        TK_SPMM_T(2)
+      } else if (tm <= 4) {
+        TK_SPMM_T(4)
+      } else if (tm <= 6) {
+        TK_SPMM_T(6)
+      } else if (tm <= 8) {
+        TK_SPMM_T(8)
+      } else if (tm <= 10) {
+        TK_SPMM_T(10)
+      } else if (tm <= 12) {
+        TK_SPMM_T(12)
+      } else if (tm <= 14) {
+        TK_SPMM_T(14)
+      } else {
+        TK_SPMM_T(16)
+      }
+#undef TK_SPMM_T
 #undef TK_SPMM_M
-    TK_LAUNCH_CHECK(ctx);
+      TK_LAUNCH_CHECK(ctx);
+    }
     return TK_OK;
+  }
+  if (!op->rowptr) {
+    ctx->err = "spmm: this operator has no per-term CSR (merged kernel only)";
+    return TK_EARG;
   }
   const int rpl = (r + 31) / 32;
 #define TK_SPMM(R, V)                                                                       \

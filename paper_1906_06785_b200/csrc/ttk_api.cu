@@ -240,14 +240,14 @@ static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
 }
 
 // ============================================================================ operator
-// Column-merged copy of the T spatial factors for spmm_merged_k (k_apply.cu): per row, the
-// distinct columns over all terms in ascending order, each as col | (term mask << 32), and the
-// values in (column, term) order.  Duplicate (column, term) entries are summed.  Not built (the
-// per-term kernel runs) when a row has more than 32 distinct columns.
-static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K_rowptr,
-                        const int32_t* const* K_col, const double* const* K_val,
-                        int64_t** out_recptr, int64_t** out_rec) {
-  if (n_x >= ((int64_t)1 << 31)) return TK_OK;
+// Column-merged records of T spatial factors for spmm_merged_k (k_apply.cu): per row, the
+// distinct columns over all T in ascending order, each as col | (mask << 32), and the values
+// in (column, factor) order.  Duplicate (column, factor) entries are summed.  Returns false
+// (no records) when a row has more than 32 distinct columns (then the per-term kernel runs).
+static bool merge_records(int T, int64_t n_x, const int32_t* const* K_rowptr,
+                          const int32_t* const* K_col, const double* const* K_val,
+                          std::vector<int64_t>& recptr, std::vector<int64_t>& rec) {
+  if (n_x >= ((int64_t)1 << 31) || T > 32) return false;
   // merged per-row lists (distinct columns with term masks, values in (column, term) order)
   std::vector<int64_t> wptr(n_x + 1, 0), vptr(n_x + 1, 0), words, vals_all;
   int64_t tot = 0;
@@ -286,7 +286,7 @@ static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K
     wptr[i + 1] = (int64_t)words.size();
     vptr[i + 1] = (int64_t)vals_all.size();
     // the merged kernel keeps one row's distinct columns in one warp's lanes
-    if (wptr[i + 1] - wptr[i] > 32) return TK_OK;  // per-term kernel for this operator
+    if (wptr[i + 1] - wptr[i] > 32) return false;
   }
   // processing order: breadth-first over the symmetrised merged pattern (Cuthill-McKee, no
   // reversal), each component from its lowest unvisited row
@@ -323,7 +323,8 @@ static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K
       }
     }
   }
-  std::vector<int64_t> recptr(n_x + 1, 0), rec;
+  recptr.assign(n_x + 1, 0);
+  rec.clear();
   rec.reserve(words.size() + vals_all.size() + n_x + 16);
   for (int64_t pos = 0; pos < n_x; pos++) {
     const int64_t i = order[pos];
@@ -333,13 +334,77 @@ static int build_merged(tk_ctx* ctx, int T, int64_t n_x, const int32_t* const* K
     rec.insert(rec.end(), vals_all.begin() + vptr[i], vals_all.begin() + vptr[i + 1]);
     recptr[pos + 1] = (int64_t)rec.size();
   }
+  return true;
+}
+
+void tk_free_chunks(std::vector<SpmmChunk>& cs) {
+  for (auto& c : cs) {
+    cudaFree(c.recptr);
+    cudaFree(c.rec);
+    cudaFree(c.tk);
+    cudaFree(c.tg);
+    cudaFree(c.tc);
+  }
+  cs.clear();
+}
+
+// Device copy of one chunk: its records and its term list (terms k with group in the chunk).
+int tk_upload_chunk(tk_ctx* ctx, SpmmChunk& c, const std::vector<int64_t>& recptr,
+                    const std::vector<int64_t>& rec, const std::vector<int>& tk,
+                    const std::vector<int>& tg, const std::vector<double>& tc) {
   auto up = [&](void** d, const void* h, size_t b) -> int {
     TK_CUDA_TRY(ctx, cudaMalloc(d, b ? b : 8));
     if (b) TK_CUDA_TRY(ctx, cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice));
     return TK_OK;
   };
-  TK_TRY(up((void**)out_recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
-  TK_TRY(up((void**)out_rec, rec.data(), sizeof(int64_t) * rec.size()));
+  c.nterm = (int)tk.size();
+  TK_TRY(up((void**)&c.recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
+  TK_TRY(up((void**)&c.rec, rec.data(), sizeof(int64_t) * rec.size()));
+  TK_TRY(up((void**)&c.tk, tk.data(), sizeof(int) * tk.size()));
+  TK_TRY(up((void**)&c.tg, tg.data(), sizeof(int) * tg.size()));
+  TK_TRY(up((void**)&c.tc, tc.data(), sizeof(double) * tc.size()));
+  return TK_OK;
+}
+
+// The merged-SpMM chunks of an operator: groups in chunks of <= 16 (reps[g] = the term whose
+// CSR represents group g; group[k], coef[k]: K_k = coef[k] K_reps[group[k]]).  Leaves
+// op->chunks empty when some merged row exceeds 32 distinct columns.
+static int build_chunks(tk_ctx* ctx, tk_op* op, int64_t n_x, const int32_t* const* K_rowptr,
+                        const int32_t* const* K_col, const double* const* K_val,
+                        const std::vector<int>& reps, const std::vector<int>& group,
+                        const std::vector<double>& coef) {
+  const int G = (int)reps.size(), T = (int)group.size();
+  bool ident = G == T;
+  for (int k = 0; k < T && ident; k++) ident = group[k] == k && coef[k] == 1.0;
+  for (int g0 = 0; g0 < G; g0 += 16) {
+    const int ng = std::min(16, G - g0);
+    std::vector<const int32_t*> rp, cl;
+    std::vector<const double*> vl;
+    for (int g = g0; g < g0 + ng; g++) {
+      rp.push_back(K_rowptr[reps[g]]);
+      cl.push_back(K_col[reps[g]]);
+      vl.push_back(K_val[reps[g]]);
+    }
+    std::vector<int64_t> recptr, rec;
+    if (!merge_records(ng, n_x, rp.data(), cl.data(), vl.data(), recptr, rec)) {
+      tk_free_chunks(op->chunks);
+      return TK_OK;
+    }
+    std::vector<int> tk, tg;
+    std::vector<double> tc;
+    for (int k = 0; k < T; k++)
+      if (group[k] >= g0 && group[k] < g0 + ng) {
+        tk.push_back(k);
+        tg.push_back(group[k] - g0);
+        tc.push_back(coef[k]);
+      }
+    SpmmChunk c;
+    c.g0 = g0;
+    c.ng = ng;
+    c.ident = ident;
+    op->chunks.push_back(c);
+    TK_TRY(tk_upload_chunk(ctx, op->chunks.back(), recptr, rec, tk, tg, tc));
+  }
   return TK_OK;
 }
 
@@ -464,32 +529,19 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
   }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
                               cudaMemcpyHostToDevice));
-  if (T <= 16) TK_TRY(build_merged(ctx, T, n_x, K_rowptr, K_col, K_val, &op->recptr, &op->rec));
   {
+    // spatial groups (bitwise-proportional K_k) and the merged-SpMM chunks over them
     std::vector<int> group, reps;
     std::vector<double> coef;
     find_groups(T, n_x, K_rowptr, K_col, K_val, group, coef, reps);
     op->n_groups = (int)reps.size();
-    if (op->n_groups < T && op->n_groups <= 16) {
-      std::vector<const int32_t*> grp, gcl;
-      std::vector<const double*> gvl;
-      for (int j : reps) {
-        grp.push_back(K_rowptr[j]);
-        gcl.push_back(K_col[j]);
-        gvl.push_back(K_val[j]);
-      }
-      TK_TRY(build_merged(ctx, op->n_groups, n_x, grp.data(), gcl.data(), gvl.data(),
-                          &op->g_recptr, &op->g_rec));
-      TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_group, sizeof(int) * T));
-      TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_coef, sizeof(double) * T));
-      TK_CUDA_TRY(ctx, cudaMemcpy(op->d_group, group.data(), sizeof(int) * T,
-                                  cudaMemcpyHostToDevice));
-      TK_CUDA_TRY(ctx, cudaMemcpy(op->d_coef, coef.data(), sizeof(double) * T,
-                                  cudaMemcpyHostToDevice));
-      if (!op->g_rec) op->n_groups = T;  // (a group row with > 32 distinct columns: no grouping)
-    } else {
-      op->n_groups = T;
-    }
+    TK_TRY(build_chunks(ctx, op.get(), n_x, K_rowptr, K_col, K_val, reps, group, coef));
+    TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_group, sizeof(int) * T));
+    TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_coef, sizeof(double) * T));
+    TK_CUDA_TRY(ctx, cudaMemcpy(op->d_group, group.data(), sizeof(int) * T,
+                                cudaMemcpyHostToDevice));
+    TK_CUDA_TRY(ctx, cudaMemcpy(op->d_coef, coef.data(), sizeof(double) * T,
+                                cudaMemcpyHostToDevice));
   }
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_kl, T_kl, sizeof(int) * T, cudaMemcpyHostToDevice));
   TK_CUDA_TRY(ctx, cudaMemcpy(op->band_ku, T_ku, sizeof(int) * T, cudaMemcpyHostToDevice));
@@ -510,10 +562,7 @@ extern "C" int tk_op_destroy(tk_op* op) {
   cudaFree(op->band_ku);
   cudaFree(op->band_off);
   cudaFree(op->band);
-  cudaFree(op->recptr);
-  cudaFree(op->rec);
-  cudaFree(op->g_recptr);
-  cudaFree(op->g_rec);
+  tk_free_chunks(op->chunks);
   cudaFree(op->d_group);
   cudaFree(op->d_coef);
   delete op;
@@ -522,12 +571,14 @@ extern "C" int tk_op_destroy(tk_op* op) {
 extern "C" int tk_op_terms(const tk_op* op) { return op ? op->T : 0; }
 extern "C" int tk_op_set_spmm_kernel(tk_op* op, int kernel) {
   if (!op || kernel < 0 || kernel > 1) return TK_EARG;
+  if (kernel == 1 && !op->rowptr) return TK_EARG;  // (no per-term CSR: merged only)
+  if (kernel == 0 && op->chunks.empty()) return 0;
   op->spmm_perterm = kernel == 1;
-  return op->recptr ? 1 - (int)op->spmm_perterm : 0;
+  return op->chunks.empty() ? 0 : 1 - (int)op->spmm_perterm;
 }
 extern "C" int tk_op_group_space(tk_op* op, int enable) {
   if (!op) return TK_EARG;
-  op->group_space = enable != 0 && op->n_groups < op->T;
+  op->group_space = enable != 0 && op->n_groups < op->T && !op->chunks.empty();
   return op->n_groups;
 }
 

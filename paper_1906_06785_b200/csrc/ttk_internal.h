@@ -96,6 +96,19 @@ struct TagScope {
 int tk_prof_begin(tk_ctx* ctx, const char* cat, double flops, double bytes);
 void tk_prof_end(tk_ctx* ctx, int id);
 
+// One launch of the column-merged SpMM: merged records over groups [g0, g0 + ng) of the op and
+// the terms those groups produce.
+struct SpmmChunk {
+  int g0 = 0, ng = 0;          // groups of this chunk
+  int nterm = 0;               // terms written (full output)
+  bool ident = false;          // the chunk's groups are terms g0 .. g0+ng-1 with coefficient 1
+  int64_t* recptr = nullptr;   // n_x + 1 (device): record i at rec + recptr[i]
+  int64_t* rec = nullptr;      // [row | gn << 32][gn words col | mask << 32][values]
+  int* tk = nullptr;           // nterm (device): term index
+  int* tg = nullptr;           // nterm (device): group index within the chunk
+  double* tc = nullptr;        // nterm (device): coefficient
+};
+
 struct tk_op {
   tk_ctx* ctx = nullptr;
   int T = 0;
@@ -110,23 +123,24 @@ struct tk_op {
   int* band_ku = nullptr;      // T
   int64_t* band_off = nullptr; // T+1 prefix offsets into band
   double* band = nullptr;      // concatenated LAPACK band arrays
-  // column-merged copy of all T terms (T <= 16, <= 32 distinct columns per row; k_apply.cu
-  // spmm_merged_k): row i's record at rec + recptr[i] is [gn][gn words col | term-mask << 32]
-  // [values (as doubles) in (column, term) order]
-  int64_t* recptr = nullptr;   // n_x + 1
-  int64_t* rec = nullptr;
+  // column-merged copy of the spatial factors (k_apply.cu spmm_merged_k), in chunks of <= 16
+  // spatial GROUPS (terms whose K_k is bitwise proportional to a representative share a
+  // group; K_k = coef[k] K_group(k)).  Empty when a merged row would exceed 32 distinct columns
+  // (then only the per-term kernel runs).
+  std::vector<SpmmChunk> chunks;
   bool spmm_perterm = false;   // tk_op_set_spmm_kernel(op, 1): use the per-term kernel
-  // spatial groups (tk_op_group_space, SURVEY.md 8d "optional exact factor grouping"): terms
-  // whose K_k is bitwise proportional to a representative share its group; K_k = coef[k] K_g.
   int n_groups = 0;            // number of groups (== T when nothing groups)
   bool group_space = false;    // opt-in: the fused apply+round stores Y1 as Y1' = [K_g U1]_g
   int* d_group = nullptr;      // T (device): group of term k
   double* d_coef = nullptr;    // T (device)
-  int64_t* g_recptr = nullptr; // merged SpMM records of the group representatives
-  int64_t* g_rec = nullptr;
   std::vector<int64_t> h_nnz;  // host copy of per-term nnz
   int max_kl = 0, max_ku = 0;
 };
+
+void tk_free_chunks(std::vector<SpmmChunk>& cs);
+int tk_upload_chunk(tk_ctx* ctx, SpmmChunk& c, const std::vector<int64_t>& recptr,
+                    const std::vector<int64_t>& rec, const std::vector<int>& tk,
+                    const std::vector<int>& tg, const std::vector<double>& tc);
 
 // ----------------------------------------------------------------------------- errors
 #define TK_CUDA_TRY(ctx, call)                                                      \

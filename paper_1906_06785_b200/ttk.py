@@ -23,7 +23,8 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_op_create", "tk_op_destroy", "tk_op_terms", "tk_apply_op", "tk_round",
             "tk_apply_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle",
-            "tk_gmres_solve", "tk_op_group_space", "tk_op_set_spmm_kernel"]
+            "tk_gmres_solve", "tk_op_group_space", "tk_op_set_spmm_kernel", "tk_op_concat",
+            "tk_conv_create", "tk_conv_destroy", "tk_op_convection"]
 
 
 class TkError(RuntimeError):
@@ -66,6 +67,10 @@ def lib():
     L.tk_op_group_space.argtypes = [P, I]
     L.tk_op_set_spmm_kernel.argtypes = [P, I]
     TTP = ctypes.POINTER(tk_tt)
+    L.tk_op_concat.argtypes = [P, I, PP, ctypes.POINTER(P)]
+    L.tk_conv_create.argtypes = [P, ctypes.POINTER(P), I64, I64, I64, I, I64, PP, PP, PP, P]
+    L.tk_conv_destroy.argtypes = [P]
+    L.tk_op_convection.argtypes = [P, P, TTP, ctypes.POINTER(P)]
     DP = ctypes.POINTER(D)
     L.tk_apply_op.argtypes = [P, P, TTP, TTP]
     L.tk_round.argtypes = [P, TTP, D, I64, DP, DP, DP, DP]
@@ -216,6 +221,25 @@ class Operator:
     def from_kronsum(cls, op, ctx=None):
         return cls(op.n_x, op.n_xi, op.n_t, op.terms, ctx)
 
+    @classmethod
+    def _from_handle(cls, h, n_x, n_xi, n_t, ctx) -> "Operator":
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.n_x, self.n_xi, self.n_t = int(n_x), int(n_xi), int(n_t)
+        self._h = h
+        self.T = int(lib().tk_op_terms(h))
+        return self
+
+    @classmethod
+    def concat(cls, ops) -> "Operator":
+        """A = sum_i A_i: the terms of ops[0], ops[1], ... (tk_op_concat)."""
+        ctx = ops[0].ctx
+        arr = (ctypes.c_void_p * len(ops))(*[o._h.value for o in ops])
+        h = ctypes.c_void_p()
+        ctx.check(lib().tk_op_concat(ctx._h, len(ops), arr, ctypes.byref(h)))
+        o = ops[0]
+        return cls._from_handle(h, o.n_x, o.n_xi, o.n_t, ctx)
+
     def group_space(self, enable: bool = True) -> int:
         """Opt-in exact factor grouping of the space core in tt_apply_round
         (tk_op_group_space); returns the number of spatial groups G (T: nothing groups)."""
@@ -236,6 +260,47 @@ class Operator:
         try:
             if self._h:
                 lib().tk_op_destroy(self._h)
+        except Exception:
+            pass
+
+
+class Convection:
+    """The discretisation of the TT convection operator N(u) of eq:N_kron (tk_conv_create):
+    d velocity components of n_v dofs at the start of the spatial mode, the n_v x n_v
+    difference operators D_c (scipy CSR) of the convective derivative, and the chaos triple
+    products H (n_xi x n_xi x n_xi, H[l, r, s] = <psi_l psi_r psi_s>).  operator(u) builds
+    N(u) on the device from the velocity TT u (tk_op_convection)."""
+
+    def __init__(self, n_x, n_xi, n_t, D, n_v, H, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.n_x, self.n_xi, self.n_t = int(n_x), int(n_xi), int(n_t)
+        d = len(D)
+        rp, cl, vl = [(ctypes.c_void_p * d)() for _ in range(3)]
+        keep = []
+        for c, m in enumerate(D):
+            a_rp = np.ascontiguousarray(m.indptr, dtype=np.int32)
+            a_cl = np.ascontiguousarray(m.indices, dtype=np.int32)
+            a_vl = np.ascontiguousarray(m.data, dtype=np.float64)
+            keep += [a_rp, a_cl, a_vl]
+            rp[c], cl[c], vl[c] = a_rp.ctypes.data, a_cl.ctypes.data, a_vl.ctypes.data
+        h = np.ascontiguousarray(np.asarray(H, dtype=np.float64).reshape(-1))
+        assert h.size == self.n_xi ** 3
+        self._h = ctypes.c_void_p()
+        self.ctx.check(lib().tk_conv_create(self.ctx._h, ctypes.byref(self._h), self.n_x,
+                                            self.n_xi, self.n_t, d, int(n_v), rp, cl, vl,
+                                            h.ctypes.data))
+
+    def operator(self, u: "TT") -> Operator:
+        us = u.struct()
+        h = ctypes.c_void_p()
+        self.ctx.check(lib().tk_op_convection(self.ctx._h, self._h, ctypes.byref(us),
+                                              ctypes.byref(h)))
+        return Operator._from_handle(h, self.n_x, self.n_xi, self.n_t, self.ctx)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().tk_conv_destroy(self._h)
         except Exception:
             pass
 

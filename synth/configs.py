@@ -55,9 +55,9 @@ CONFIGS = {
                  gmres_steps=20, rhs_ranks=(8, 8)),
     # NEXT-1, not a BASELINE.json config: apply + round of the TT convection
     # operator N(u~) of eq:N_kron on the c2 sizes, u~ a seeded decaying
-    # velocity TT of ranks (4, 4) -> 16 terms, x the c2-style input (20, 20) -> (320, 320)
+    # velocity TT of ranks (8, 8) -> 64 terms, x the c2-style input (20, 20) -> (1280, 1280)
     "c6": Config("c6", 5, 64, 4, 3, 64, 1.0 / 64, _nus(4), 1, (20, 20), 1e-8, 80, "decay",
-                 operator="convection", velocity_ranks=(4, 4)),
+                 operator="convection", velocity_ranks=(8, 8)),
 }
 
 

@@ -78,11 +78,8 @@ def _csr32(k: sp.csr_matrix) -> sp.csr_matrix:
 
 def build_operator(cfg: Config) -> KronSumOp:
     if cfg.operator == "convection":
-        from .tt import make_velocity_tt
-        H = gpc.h_matrices(cfg.m, cfg.p)
-        op = convection_operator(cfg.grid, len(H), cfg.n_t, H, *make_velocity_tt(cfg, len(H)))
-        assert op.T == cfg.n_terms
-        return op
+        raise ValueError("the convection operator is built by the library (tk_op_convection) "
+                         "or by oracle.convection from synth.operator.convection_stencils")
     rng = np.random.default_rng([cfg.index, 0])
     n = cfg.grid
     winds = [fd.sinusoid_wind(n, rng, scale=0.5 ** j) for j in range(cfg.wind_rank)]
@@ -119,28 +116,9 @@ def random_operator(rng: np.random.Generator, n_x: int, n_xi: int, n_t: int, T: 
     return KronSumOp(n_x, n_xi, n_t, terms)
 
 
-def convection_operator(n: int, n_xi: int, n_t: int, H: list, U1: np.ndarray, U2: np.ndarray,
-                        U3: np.ndarray) -> KronSumOp:
-    """The TT-format convection operator N(u) of eq:N_kron for a velocity
-    field u given as a TT in this repo's core order (R1, R18):
-
-        N(u) = sum_{a < r1, b < r2} diag(U3[b, :]) (x) (sum_l U2[a, l, b] H_l) (x) N(u_a)
-
-    with the paper's u^(1)(k, alpha_1) = U3[alpha_1, k] (time), u^(2)(alpha_1, l, alpha_2) =
-    U2[alpha_2, l, alpha_1], u^(3)(alpha_2, j) = U1[j, alpha_2] (space); N(u_a) is the FD
-    convection blkdiag(N(w), N(w), 0) of the wind w = (U1[:N^2, a], U1[N^2:2N^2, a]) (the
-    velocity components of the spatial basis vector; its pressure part does not convect, R10).
-    T_k = diag(U3[b, :]) is a band of width 0.  r1 r2 terms (the kappa -> kappa^2 growth,
-    PAPER.md:331)."""
-    n2 = n * n
-    r1, r2 = U1.shape[1], U3.shape[0]
-    assert U1.shape[0] == 3 * n2 and U2.shape == (r1, n_xi, r2) and U3.shape == (r2, n_t)
-    Hs = np.stack(H)  # (n_xi, n_xi, n_xi): Hs[l]
-    terms = []
-    for a in range(r1):
-        K = _csr32(fd.wind_block(n, (U1[:n2, a], U1[n2:2 * n2, a])))
-        for b in range(r2):
-            G = np.tensordot(U2[a, :, b], Hs, axes=(0, 0))
-            band = U3[b, :].reshape(1, n_t).copy()
-            terms.append(Term(f"conv{a}_{b}", 0, 0, band, G, K))
-    return KronSumOp(3 * n2, n_xi, n_t, terms)
+def convection_stencils(n: int):
+    """The discretisation data of the convection operator (input data, no method arithmetic):
+    the central-difference operators (D_x, D_y) on the N x N velocity grid and n_v = N^2 dofs
+    per velocity component; the spatial mode is [u1; u2; p] (R10).  N(w) itself is
+    formed by the library (tk_conv_create / tk_op_convection) and by oracle.convection."""
+    return [_csr32(fd.central_dx(n)), _csr32(fd.central_dy(n))], n * n

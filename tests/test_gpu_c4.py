@@ -45,7 +45,7 @@ def c4():
 
 def test_c4_apply_round_full_oracle_parity(c4):
     """North-star parity at the headline size: GPU apply+round vs the oracle on all of c4."""
-    from tests.test_gpu_parity import ranks_excused, tt_diff_rel
+    from parity_util import ranks_excused, tt_diff_rel
     cfg, op, x, gop, _ = c4
     y_o = otT.apply_op(op, x)
     o, info = otT.round_tt(y_o, cfg.tol, cfg.rmax, return_info=True)
