@@ -12,6 +12,7 @@ Readings (R15):
   * breakdown when h_{k+1,k} <= 1e-14 ||T(L v_k)||
   * z = sum_i y_i v_i accumulated as z <- T(z + y_i v_i); explicit residual ||T(b - L z)||.
 gmres_solve: the complete, restarted Alg. 3 (NEXT-2; reading R19 in its docstring).
+Both take an optional right preconditioner (NEXT-3, oracle/precond.py): flexible GMRES.
 """
 from __future__ import annotations
 
@@ -30,10 +31,12 @@ def givens(a: float, b: float):
 
 
 def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6, stop_abs: float = 0.0,
-                explicit: bool = True):
+                explicit: bool = True, prec=None):
     """One cycle.  stop_abs > 0: stop once the least-squares residual |g_{k+1}| <= stop_abs
     (Alg. 3 line 2 with the Givens estimate, R19).  explicit=False skips the explicit
-    residual T(b - L z) (the restarted solver forms its own)."""
+    residual T(b - L z) (the restarted solver forms its own).  prec (callable TT -> TT): the
+    right preconditioner of Alg. 3 line 4, v^_k = P^{-1} v_k; the flexible variant keeps the
+    v^_k and forms z = z_0 + V^_k y_k (lines 11, 13)."""
     s0 = tt.round_tt(b, tol)
     beta = tt.norm(s0)
     v = [tt.scale(1.0 / beta, s0)]
@@ -44,8 +47,11 @@ def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6, stop_abs: float = 0.0
     hist = [beta]
     ranks = [tt.ranks(v[0])]
     k_done = 0
+    vhat = []
     for k in range(steps):
-        x = tt.round_tt(tt.apply_op(op, v[k]), tol)
+        vh = prec(v[k]) if prec is not None else v[k]                # line 4
+        vhat.append(vh)
+        x = tt.round_tt(tt.apply_op(op, vh), tol)                     # line 5
         nav = tt.norm(x)
         for i in range(k + 1):
             h = tt.dot(x, v[i])
@@ -76,9 +82,9 @@ def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6, stop_abs: float = 0.0
     # least squares solve: H[:k,:k] y = g[:k] (upper triangular after rotations)
     R = H[:k_done, :k_done]
     y = np.linalg.solve(np.triu(R), g[:k_done])
-    z = tt.scale(y[0], v[0])
+    z = tt.scale(y[0], vhat[0])
     for i in range(1, k_done):
-        z = tt.round_tt(tt.axpby(1.0, z, y[i], v[i]), tol)
+        z = tt.round_tt(tt.axpby(1.0, z, y[i], vhat[i]), tol)
     if not explicit:
         return dict(history=np.array(hist), explicit=None, y=y, z=z, ranks=ranks, steps=k_done)
     r = tt.round_tt(tt.axpby(1.0, b, -1.0, tt.apply_op(op, z)), tol)
@@ -86,7 +92,7 @@ def gmres_cycle(op, b, steps: int = 20, tol: float = 1e-6, stop_abs: float = 0.0
 
 
 def gmres_solve(op, b, restart: int = 20, max_cycles: int = 5, tol: float = 1e-6,
-                tol_gmres: float = 1e-8, eps_soln: float | None = None):
+                tol_gmres: float = 1e-8, eps_soln: float | None = None, prec=None):
     """Complete low-rank GMRES (NEXT-2): Alg. 3 with P = I,
     restarted every `restart` steps (z_0 <- z), the stopping test ||s_k|| <= tol_gmres ||b||
     (line 2) and the truncated solution update of eq:eps_soln.  Reading
@@ -103,7 +109,8 @@ def gmres_solve(op, b, restart: int = 20, max_cycles: int = 5, tol: float = 1e-6
     for _cycle in range(max_cycles):
         if explicit[-1] <= tol_gmres * bnorm:
             break
-        res = gmres_cycle(op, s, restart, tol, stop_abs=tol_gmres * bnorm, explicit=False)
+        res = gmres_cycle(op, s, restart, tol, stop_abs=tol_gmres * bnorm, explicit=False,
+                          prec=prec)
         ls.append(res["history"])
         dz = res["z"]
         z = tt.round_tt(dz if z is None else tt.axpby(1.0, z, 1.0, dz), eps_soln)

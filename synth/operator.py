@@ -122,3 +122,16 @@ def convection_stencils(n: int):
     per velocity component; the spatial mode is [u1; u2; p] (R10).  N(w) itself is
     formed by the library (tk_conv_create / tk_op_convection) and by oracle.convection."""
     return [_csr32(fd.central_dx(n)), _csr32(fd.central_dy(n))], n * n
+
+
+def mean_blocks(cfg: Config):
+    """Input data of the mean-based preconditioner (NEXT-3, section 5) for an Oseen
+    config: the mean convection-diffusion block F0s = nu_0 L + N(w_0) of ONE velocity component
+    (the same w_0 as build_operator's mean Oseen term) and the divergence B = [B1 B2]
+    (n_p x 2 n_v).  Returns (F0s, B) as CSR; no preconditioner arithmetic."""
+    rng = np.random.default_rng([cfg.index, 0])
+    n = cfg.grid
+    winds = [fd.sinusoid_wind(n, rng, scale=0.5 ** j) for j in range(cfg.wind_rank)]
+    f0 = _csr32(cfg.nus[0] * fd.laplacian(n) + fd.convection(n, *winds[0]))
+    b = _csr32(sp.hstack([fd.forward_dx(n), fd.forward_dy(n)]))
+    return f0, b
