@@ -416,7 +416,7 @@ def run_ours(args, cfg, op, x):
         cnt, ms, fl, by = heavy.get(cat, dom[1])
         ms_all = dom[1][1] / full_steps
         avg_ms = ms / cnt
-        if fl > 0 and (fl / by) > 6.0:
+        if fl > 0 and (by <= 0 or fl / by > 6.0):
             ach = fl / cnt / (avg_ms * 1e-3) / 1e12
             alg = algorithmic_round_flops(op, cfg, ranks_out)
             tr = dgemm_traffic() if cfg.name == "c4" and not args.group_space else None

@@ -175,10 +175,10 @@ __global__ void __launch_bounds__(256, (RPL <= 2 ? 4 : (RPL <= 3 ? 3 : 1))) spmm
 // Output map.  The records merge the op's spatial GROUPS (terms with bitwise-proportional K_k
 // share a group, and so do the r2 terms of the convection operator that share N(u_a)), at
 // most TM per launch (a chunk of the op's groups).  MAP == false: the chunk's groups ARE
-// terms k0 .. k0+nout-1 (coefficient 1).  MAP == true: the per-group products are staged in
-// shared memory and every term t < nout of the chunk's term list is written as
-// Y1[:, tk[t] r : (tk[t]+1) r] = tc[t] * (K_{group tg[t]} U1): the products are computed once
-// per group, the T r outputs (the HBM-bound part) are still all written.  R = row stride of Y1.
+// terms k0 .. k0+nout-1 (coefficient 1).  MAP == true: group g < nout writes its terms
+// tk[tg[g] .. tg[g+1]) as Y1[:, tk[t] r : (tk[t]+1) r] = tc[t] * (K_g U1) straight from its
+// register accumulator: each product is computed once per group, the T r outputs (the
+// HBM-bound part) are all written.  R = row stride of Y1.
 template <int TM, bool V2, bool MAP>
 __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int nout, int r, int64_t R,
                                                        const int64_t* __restrict__ recptr,
@@ -253,8 +253,7 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int nout, i
     const int gp = (gn + UNR - 1) / UNR * UNR;  // padded to the unroll: pad slots hold zeros
     double* yrow = Y1 + row * R;
     for (int c0 = 0; c0 < r; c0 += CW) {
-    // (MAP: vd doubles as the staging buffer of the products, so it is re-expanded per chunk)
-    if ((MAP || c0 == 0) && lane < gp) {  // lane j: dense, zero-padded values of distinct column j
+    if (c0 == 0 && lane < gp) {  // lane j: dense, zero-padded values of distinct column j
       const int64_t v0 = 1 + gn + off;
       // staged record, or (rows longer than 32 RW words) straight from global
       const long long* src = (p1 - p0 <= 32 * RW) ? rs + v0 : rec + p0 + v0;
@@ -305,15 +304,17 @@ __global__ void __launch_bounds__(256, 2) spmm_merged_k(int64_t n_x, int nout, i
       }
       if (MAP) {
         static_assert(!MAP || !V2, "MAP: scalar lanes");
-        __syncwarp();  // every lane is done reading vd: reuse it as [TM][32] staging
-        double(*st)[32] = reinterpret_cast<double(*)[32]>(&vd[0][0]);
+        // group g's product goes to its terms tk[tg[g] .. tg[g+1]) (warp-uniform loads)
+        if (okc) {
 #pragma unroll
-        for (int k = 0; k < TM; k++) st[k][lane] = acc[k][0];
-        __syncwarp();
-        if (okc)
-          for (int t = 0; t < nout; t++)
-            __stcs(yrow + (int64_t)__ldg(tk + t) * r + cc, __ldg(tc + t) * st[__ldg(tg + t)][lane]);
-        __syncwarp();
+          for (int g = 0; g < TM; g++) {
+            if (g < nout) {
+              const int t1 = __ldg(tg + g + 1);
+              for (int t = __ldg(tg + g); t < t1; t++)
+                __stcs(yrow + (int64_t)__ldg(tk + t) * r + cc, __ldg(tc + t) * acc[g][0]);
+            }
+          }
+        }
       } else if (okc) {
         double* dst = yrow + (int64_t)k0 * r + cc;
 #pragma unroll
@@ -390,19 +391,19 @@ int tk_launch_spmm_multi(tk_ctx* ctx, const tk_op* op, int r, const double* U1, 
   const int threads = 256;
   int64_t blocks = (n_x * 32 + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, 32LL * ctx->num_sms);
-  if (grouped && op->chunks.empty()) {
-    ctx->err = "spmm: group-space output needs the merged kernel";
+  if (grouped && op->gchunks.empty()) {
+    ctx->err = "spmm: this operator has no group-space records";
     return TK_EARG;
   }
-  if (!op->chunks.empty() && (grouped || !op->spmm_perterm)) {
+  if (grouped || (!op->chunks.empty() && !op->spmm_perterm)) {
     // column-merged kernel, one launch per chunk of <= 16 groups.  grouped: the group
     // representatives only (tk_op_group_space), Y1' = [K_g U1]_g with row stride G r.
     blocks = std::min<int64_t>((n_x * 32 + threads - 1) / threads, 16LL * ctx->num_sms);
     const int64_t R = (int64_t)(grouped ? op->n_groups : op->T) * r;
-    for (const SpmmChunk& c : op->chunks) {
+    for (const SpmmChunk& c : (grouped ? op->gchunks : op->chunks)) {
       const bool map = !grouped && !c.ident;
-      const int nout = grouped ? c.ng : (c.ident ? c.ng : c.nterm);
-      const int k0 = c.g0;
+      const int nout = c.ng;  // (MAP: the chunk's groups; their terms come from c.tg / c.tk)
+      const int k0 = grouped ? c.g0 : c.k0;
       const int tm = c.ng;
 #define TK_SPMM_M(TM, MP)                                                                   \
   spmm_merged_k<TM, false, MP><<<(unsigned)blocks, threads, 0, ctx->stream>>>(              \

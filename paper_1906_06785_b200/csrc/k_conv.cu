@@ -314,6 +314,7 @@ extern "C" int tk_op_convection(tk_ctx* ctx, const tk_conv* cvc, const tk_tt* u,
     c.g0 = g0;
     c.ng = ng;
     c.ident = r2 == 1;  // then the chunk's groups are terms g0 .. g0+ng-1
+    c.k0 = g0;
     std::vector<int> tk, tg;
     std::vector<double> tc;
     for (int a = g0; a < g0 + ng; a++)
@@ -324,23 +325,24 @@ extern "C" int tk_op_convection(tk_ctx* ctx, const tk_conv* cvc, const tk_tt* u,
       }
     op->chunks.push_back(c);
     SpmmChunk& cc = op->chunks.back();
-    cc.nterm = (int)tk.size();
     TK_TRY(dmal((void**)&cc.recptr, sizeof(int64_t) * (n_x + 1)));
     TK_TRY(dmal((void**)&cc.rec, sizeof(int64_t) * sk->len));
-    TK_TRY(dmal((void**)&cc.tk, sizeof(int) * tk.size()));
-    TK_TRY(dmal((void**)&cc.tg, sizeof(int) * tg.size()));
-    TK_TRY(dmal((void**)&cc.tc, sizeof(double) * tc.size()));
+    TK_TRY(tk_upload_terms(ctx, cc, tk, tg, tc));
     TK_CUDA_TRY(ctx, cudaMemcpyAsync(cc.recptr, sk->recptr, sizeof(int64_t) * (n_x + 1),
                                      cudaMemcpyDeviceToDevice, st));
     TK_CUDA_TRY(ctx, cudaMemcpyAsync(cc.rec, sk->rec, sizeof(int64_t) * sk->len,
                                      cudaMemcpyDeviceToDevice, st));
-    TK_CUDA_TRY(ctx, cudaMemcpy(cc.tk, tk.data(), sizeof(int) * tk.size(), cudaMemcpyHostToDevice));
-    TK_CUDA_TRY(ctx, cudaMemcpy(cc.tg, tg.data(), sizeof(int) * tg.size(), cudaMemcpyHostToDevice));
-    TK_CUDA_TRY(ctx, cudaMemcpy(cc.tc, tc.data(), sizeof(double) * tc.size(),
-                                cudaMemcpyHostToDevice));
     conv_fill_k<<<grid_of(ctx, n_x), 256, 0, st>>>(n_x, cv->n_v, cv->d, ng, g0, r1, cc.recptr,
                                                    cc.rec, cv->pp, cv->coef, cv->nnz, u->U1);
     TK_LAUNCH_CHECK(ctx);
+  }
+  // group-space output: the same records, identity over the groups (aliases, not owned)
+  for (const SpmmChunk& c : op->chunks) {
+    SpmmChunk g = c;
+    g.owns = false;
+    g.ident = true;
+    g.k0 = c.g0;
+    op->gchunks.push_back(g);
   }
   *out = op.release();
   return TK_OK;
@@ -438,38 +440,31 @@ extern "C" int tk_op_concat(tk_ctx* ctx, int n, const tk_op* const* ops, tk_op**
       noff += no.back();
     }
     if (all_chunks) {
-      for (const SpmmChunk& sc : s->chunks) {
-        // term list of the source chunk (device) -> offset copy
-        std::vector<int> tk(sc.nterm), tg(sc.nterm);
-        std::vector<double> tc(sc.nterm);
-        if (sc.nterm) {
-          TK_CUDA_TRY(ctx, cudaMemcpy(tk.data(), sc.tk, sizeof(int) * sc.nterm, cudaMemcpyDeviceToHost));
-          TK_CUDA_TRY(ctx, cudaMemcpy(tg.data(), sc.tg, sizeof(int) * sc.nterm, cudaMemcpyDeviceToHost));
-          TK_CUDA_TRY(ctx, cudaMemcpy(tc.data(), sc.tc, sizeof(double) * sc.nterm, cudaMemcpyDeviceToHost));
+      // full output: the source's term list shifted by k0; group-space output: the source's
+      // group chunks shifted by gofs (copies of the records)
+      for (int pass = 0; pass < 2; pass++) {
+        const std::vector<SpmmChunk>& src = pass == 0 ? s->chunks : s->gchunks;
+        for (const SpmmChunk& sc : src) {
+          std::vector<int> tk = sc.h_tk, tg(sc.nterm);
+          std::vector<double> tc = sc.h_tc;
+          for (int g = 0; g < sc.ng; g++)
+            for (int t = sc.h_goff[g]; t < sc.h_goff[g + 1]; t++) tg[t] = g;
+          for (auto& v : tk) v += k0;
+          std::vector<int64_t> recptr(n_x + 1);
+          TK_CUDA_TRY(ctx, cudaMemcpy(recptr.data(), sc.recptr, sizeof(int64_t) * (n_x + 1),
+                                      cudaMemcpyDeviceToHost));
+          std::vector<int64_t> rec(recptr.back());
+          TK_CUDA_TRY(ctx, cudaMemcpy(rec.data(), sc.rec, sizeof(int64_t) * rec.size(),
+                                      cudaMemcpyDeviceToHost));
+          SpmmChunk c;
+          c.g0 = sc.g0 + gofs;
+          c.ng = sc.ng;
+          c.ident = sc.ident;
+          c.k0 = pass == 0 ? sc.k0 + k0 : c.g0;
+          std::vector<SpmmChunk>& dst = pass == 0 ? op->chunks : op->gchunks;
+          dst.push_back(c);
+          TK_TRY(tk_upload_chunk(ctx, dst.back(), recptr, rec, tk, tg, tc));
         }
-        if (sc.ident) {  // make the identity map explicit: the concatenation is not an identity
-          tk.clear();
-          tg.clear();
-          tc.clear();
-          for (int g = 0; g < sc.ng; g++) {
-            tk.push_back(sc.g0 + g);
-            tg.push_back(g);
-            tc.push_back(1.0);
-          }
-        }
-        for (auto& v : tk) v += k0;
-        std::vector<int64_t> recptr(n_x + 1);
-        TK_CUDA_TRY(ctx, cudaMemcpy(recptr.data(), sc.recptr, sizeof(int64_t) * (n_x + 1),
-                                    cudaMemcpyDeviceToHost));
-        std::vector<int64_t> rec(recptr.back());
-        TK_CUDA_TRY(ctx, cudaMemcpy(rec.data(), sc.rec, sizeof(int64_t) * rec.size(),
-                                    cudaMemcpyDeviceToHost));
-        SpmmChunk c;
-        c.g0 = sc.g0 + gofs;
-        c.ng = sc.ng;
-        c.ident = false;
-        op->chunks.push_back(c);
-        TK_TRY(tk_upload_chunk(ctx, op->chunks.back(), recptr, rec, tk, tg, tc));
       }
     }
     k0 += Ti;
@@ -485,6 +480,13 @@ extern "C" int tk_op_concat(tk_ctx* ctx, int n, const tk_op* const* ops, tk_op**
     TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
                                 cudaMemcpyHostToDevice));
   op->spmm_perterm = !all_chunks;
+  // group-space output only if every part has one (else groups == terms: no grouping)
+  bool all_g = true;
+  for (int i = 0; i < n; i++) all_g = all_g && (!ops[i]->gchunks.empty() || ops[i]->n_groups == ops[i]->T);
+  if (!all_g || !all_chunks) {
+    tk_free_chunks(op->gchunks);
+    op->n_groups = T;
+  }
   *out = op.release();
   return TK_OK;
 }

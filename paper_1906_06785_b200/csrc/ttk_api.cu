@@ -339,6 +339,7 @@ static bool merge_records(int T, int64_t n_x, const int32_t* const* K_rowptr,
 
 void tk_free_chunks(std::vector<SpmmChunk>& cs) {
   for (auto& c : cs) {
+    if (!c.owns) continue;
     cudaFree(c.recptr);
     cudaFree(c.rec);
     cudaFree(c.tk);
@@ -348,7 +349,37 @@ void tk_free_chunks(std::vector<SpmmChunk>& cs) {
   cs.clear();
 }
 
-// Device copy of one chunk: its records and its term list (terms k with group in the chunk).
+// Device copy of a chunk's term list (terms tk[t] of local group tg[t] with coefficient
+// tc[t]), stored sorted by group with the group offsets goff (ng + 1) in c.tg.
+int tk_upload_terms(tk_ctx* ctx, SpmmChunk& c, const std::vector<int>& tk,
+                    const std::vector<int>& tg, const std::vector<double>& tc) {
+  auto up = [&](void** d, const void* h, size_t b) -> int {
+    TK_CUDA_TRY(ctx, cudaMalloc(d, b ? b : 8));
+    if (b) TK_CUDA_TRY(ctx, cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice));
+    return TK_OK;
+  };
+  c.nterm = (int)tk.size();
+  std::vector<int> ord(tk.size());
+  for (size_t t = 0; t < ord.size(); t++) ord[t] = (int)t;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return tg[a] < tg[b]; });
+  std::vector<int> sk(tk.size()), goff(c.ng + 1, 0);
+  std::vector<double> sc(tk.size());
+  for (size_t t = 0; t < ord.size(); t++) {
+    sk[t] = tk[ord[t]];
+    sc[t] = tc[ord[t]];
+    goff[tg[ord[t]] + 1]++;
+  }
+  for (int g = 0; g < c.ng; g++) goff[g + 1] += goff[g];
+  c.h_tk = sk;
+  c.h_goff = goff;
+  c.h_tc = sc;
+  TK_TRY(up((void**)&c.tk, sk.data(), sizeof(int) * sk.size()));
+  TK_TRY(up((void**)&c.tg, goff.data(), sizeof(int) * goff.size()));
+  TK_TRY(up((void**)&c.tc, sc.data(), sizeof(double) * sc.size()));
+  return TK_OK;
+}
+
+// Device copy of one chunk: its records and its term list (tk_upload_terms).
 int tk_upload_chunk(tk_ctx* ctx, SpmmChunk& c, const std::vector<int64_t>& recptr,
                     const std::vector<int64_t>& rec, const std::vector<int>& tk,
                     const std::vector<int>& tg, const std::vector<double>& tc) {
@@ -357,25 +388,18 @@ int tk_upload_chunk(tk_ctx* ctx, SpmmChunk& c, const std::vector<int64_t>& recpt
     if (b) TK_CUDA_TRY(ctx, cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice));
     return TK_OK;
   };
-  c.nterm = (int)tk.size();
   TK_TRY(up((void**)&c.recptr, recptr.data(), sizeof(int64_t) * recptr.size()));
   TK_TRY(up((void**)&c.rec, rec.data(), sizeof(int64_t) * rec.size()));
-  TK_TRY(up((void**)&c.tk, tk.data(), sizeof(int) * tk.size()));
-  TK_TRY(up((void**)&c.tg, tg.data(), sizeof(int) * tg.size()));
-  TK_TRY(up((void**)&c.tc, tc.data(), sizeof(double) * tc.size()));
-  return TK_OK;
+  return tk_upload_terms(ctx, c, tk, tg, tc);
 }
 
-// The merged-SpMM chunks of an operator: groups in chunks of <= 16 (reps[g] = the term whose
-// CSR represents group g; group[k], coef[k]: K_k = coef[k] K_reps[group[k]]).  Leaves
-// op->chunks empty when some merged row exceeds 32 distinct columns.
-static int build_chunks(tk_ctx* ctx, tk_op* op, int64_t n_x, const int32_t* const* K_rowptr,
-                        const int32_t* const* K_col, const double* const* K_val,
-                        const std::vector<int>& reps, const std::vector<int>& group,
-                        const std::vector<double>& coef) {
-  const int G = (int)reps.size(), T = (int)group.size();
-  bool ident = G == T;
-  for (int k = 0; k < T && ident; k++) ident = group[k] == k && coef[k] == 1.0;
+// Merged-SpMM chunks over the factors reps[0..G) (each the representative CSR of one output
+// column block g, coefficient 1, identity output map: chunk c writes blocks c*16 ..), in chunks
+// of <= 16.  Leaves `out` empty when some merged row exceeds 32 distinct columns.
+static int build_chunks(tk_ctx* ctx, std::vector<SpmmChunk>& out, int64_t n_x,
+                        const int32_t* const* K_rowptr, const int32_t* const* K_col,
+                        const double* const* K_val, const std::vector<int>& reps) {
+  const int G = (int)reps.size();
   for (int g0 = 0; g0 < G; g0 += 16) {
     const int ng = std::min(16, G - g0);
     std::vector<const int32_t*> rp, cl;
@@ -387,23 +411,23 @@ static int build_chunks(tk_ctx* ctx, tk_op* op, int64_t n_x, const int32_t* cons
     }
     std::vector<int64_t> recptr, rec;
     if (!merge_records(ng, n_x, rp.data(), cl.data(), vl.data(), recptr, rec)) {
-      tk_free_chunks(op->chunks);
+      tk_free_chunks(out);
       return TK_OK;
     }
     std::vector<int> tk, tg;
     std::vector<double> tc;
-    for (int k = 0; k < T; k++)
-      if (group[k] >= g0 && group[k] < g0 + ng) {
-        tk.push_back(k);
-        tg.push_back(group[k] - g0);
-        tc.push_back(coef[k]);
-      }
+    for (int g = 0; g < ng; g++) {
+      tk.push_back(g0 + g);
+      tg.push_back(g);
+      tc.push_back(1.0);
+    }
     SpmmChunk c;
     c.g0 = g0;
     c.ng = ng;
-    c.ident = ident;
-    op->chunks.push_back(c);
-    TK_TRY(tk_upload_chunk(ctx, op->chunks.back(), recptr, rec, tk, tg, tc));
+    c.ident = true;
+    c.k0 = g0;
+    out.push_back(c);
+    TK_TRY(tk_upload_chunk(ctx, out.back(), recptr, rec, tk, tg, tc));
   }
   return TK_OK;
 }
@@ -530,12 +554,17 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
   TK_CUDA_TRY(ctx, cudaMemcpy(op->nnz_off, nnz_off.data(), sizeof(int64_t) * (T + 1),
                               cudaMemcpyHostToDevice));
   {
-    // spatial groups (bitwise-proportional K_k) and the merged-SpMM chunks over them
-    std::vector<int> group, reps;
+    // merged-SpMM chunks over the terms (the literal output), and over the spatial groups
+    // (bitwise-proportional K_k) for the optional group-space output
+    std::vector<int> group, reps, all(T);
     std::vector<double> coef;
+    for (int k = 0; k < T; k++) all[k] = k;
+    TK_TRY(build_chunks(ctx, op->chunks, n_x, K_rowptr, K_col, K_val, all));
     find_groups(T, n_x, K_rowptr, K_col, K_val, group, coef, reps);
     op->n_groups = (int)reps.size();
-    TK_TRY(build_chunks(ctx, op.get(), n_x, K_rowptr, K_col, K_val, reps, group, coef));
+    if (op->n_groups < T && !op->chunks.empty())
+      TK_TRY(build_chunks(ctx, op->gchunks, n_x, K_rowptr, K_col, K_val, reps));
+    if (op->gchunks.empty()) op->n_groups = T;  // (no group-space output)
     TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_group, sizeof(int) * T));
     TK_CUDA_TRY(ctx, cudaMalloc((void**)&op->d_coef, sizeof(double) * T));
     TK_CUDA_TRY(ctx, cudaMemcpy(op->d_group, group.data(), sizeof(int) * T,
@@ -562,6 +591,7 @@ extern "C" int tk_op_destroy(tk_op* op) {
   cudaFree(op->band_ku);
   cudaFree(op->band_off);
   cudaFree(op->band);
+  tk_free_chunks(op->gchunks);
   tk_free_chunks(op->chunks);
   cudaFree(op->d_group);
   cudaFree(op->d_coef);
@@ -578,7 +608,7 @@ extern "C" int tk_op_set_spmm_kernel(tk_op* op, int kernel) {
 }
 extern "C" int tk_op_group_space(tk_op* op, int enable) {
   if (!op) return TK_EARG;
-  op->group_space = enable != 0 && op->n_groups < op->T && !op->chunks.empty();
+  op->group_space = enable != 0 && op->n_groups < op->T && !op->gchunks.empty();
   return op->n_groups;
 }
 

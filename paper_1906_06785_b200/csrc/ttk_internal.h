@@ -101,12 +101,16 @@ void tk_prof_end(tk_ctx* ctx, int id);
 struct SpmmChunk {
   int g0 = 0, ng = 0;          // groups of this chunk
   int nterm = 0;               // terms written (full output)
-  bool ident = false;          // the chunk's groups are terms g0 .. g0+ng-1 with coefficient 1
+  bool ident = false;          // the chunk's groups are terms k0 .. k0+ng-1 with coefficient 1
+  int k0 = 0;                  // (ident) first term
+  bool owns = true;            // false: the device arrays belong to another chunk
   int64_t* recptr = nullptr;   // n_x + 1 (device): record i at rec + recptr[i]
   int64_t* rec = nullptr;      // [row | gn << 32][gn words col | mask << 32][values]
-  int* tk = nullptr;           // nterm (device): term index
-  int* tg = nullptr;           // nterm (device): group index within the chunk
+  int* tk = nullptr;           // nterm (device): term index, sorted by group
+  int* tg = nullptr;           // ng + 1 (device): group g's terms are tk[tg[g] .. tg[g+1])
   double* tc = nullptr;        // nterm (device): coefficient
+  std::vector<int> h_tk, h_goff;  // host copies (tk_op_concat)
+  std::vector<double> h_tc;
 };
 
 struct tk_op {
@@ -128,6 +132,9 @@ struct tk_op {
   // group; K_k = coef[k] K_group(k)).  Empty when a merged row would exceed 32 distinct columns
   // (then only the per-term kernel runs).
   std::vector<SpmmChunk> chunks;
+  // the same over the group REPRESENTATIVES only, for the group-space output Y1' = [K_g U1]_g
+  // of tk_op_group_space (identity over groups); empty when nothing groups
+  std::vector<SpmmChunk> gchunks;
   bool spmm_perterm = false;   // tk_op_set_spmm_kernel(op, 1): use the per-term kernel
   int n_groups = 0;            // number of groups (== T when nothing groups)
   bool group_space = false;    // opt-in: the fused apply+round stores Y1 as Y1' = [K_g U1]_g
@@ -138,6 +145,8 @@ struct tk_op {
 };
 
 void tk_free_chunks(std::vector<SpmmChunk>& cs);
+int tk_upload_terms(tk_ctx* ctx, SpmmChunk& c, const std::vector<int>& tk,
+                    const std::vector<int>& tg, const std::vector<double>& tc);
 int tk_upload_chunk(tk_ctx* ctx, SpmmChunk& c, const std::vector<int64_t>& recptr,
                     const std::vector<int64_t>& rec, const std::vector<int>& tk,
                     const std::vector<int>& tg, const std::vector<double>& tc);
