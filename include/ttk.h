@@ -222,6 +222,74 @@ int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart, in
                    double tol, double tol_gmres, double eps_soln, tk_tt* z, double* explicit_out,
                    double* ls_out, int* cycles_done, int* steps_out);
 
+/* ===================================================================================== NEXT-3
+ * The mean-based preconditioner of PAPER.md section 5.
+ *
+ * tk_bt: a direct solver for a sparse spatial matrix K (n x n, n = nb * N) that is BLOCK
+ * TRIDIAGONAL in blocks of N consecutive rows (entries only between block rows i-1, i, i+1 —
+ * the lexicographic 5-point finite-difference structure of the configs, R10, with N
+ * the grid line length).  The factorisation is block LU (block Thomas) on the device:
+ *   S_0 = D_0,  S_i = D_i - L_i S_{i-1}^{-1} U_{i-1};  E_i = S_i^{-1}, F_i = E_i U_i,
+ *   G_i = E_i L_i   (dense N x N blocks; E_i from a Householder QR of S_i: R^{-1} Q^T)
+ * and a solve is  y_i = E_i b_i - G_i y_{i-1}  (forward),  x_i = y_i - F_i x_{i+1}  (back).
+ * Storage 3 nb N^2 doubles.  Singular or badly conditioned blocks are not detected beyond
+ * non-finite results (TK_ENUMERIC from the GMRES / rounding calls that consume them).
+ *
+ * tk_bt_create: K = A + shift * I for the HOST CSR A (int32, 0-based).  TK_EARG if A has an
+ *   entry outside the block-tridiagonal band or n != nb N.  Synchronous (setup).
+ * tk_bt_create_gram: K = B B^T for the HOST CSR B (n x ncols); TK_EARG if a column of B
+ *   couples rows more than one block row apart.  (The pressure Laplacian B M*^{-1} B^T of
+ *   eq:mean_lsc, with M* = I.)  Synchronous (setup).
+ * tk_bt_solve: y = (I (x) I (x) K^{-1}) x restricted to the rows [row0, row0 + reps n) of the
+ *   space core: K^{-1} applied to each of the reps consecutive n-row blocks of U1 (x's r1
+ *   columns), zero elsewhere; y.U2, y.U3 = x's (ranks unchanged, PAPER.md:244 with a single
+ *   spatial factor).  y needs cap >= x's ranks and must not alias x.  Asynchronous. */
+typedef struct tk_bt tk_bt;
+int tk_bt_create(tk_ctx* ctx, tk_bt** bt, int64_t nb, int64_t N, const int32_t* rowptr,
+                 const int32_t* col, const double* val, double shift);
+int tk_bt_create_gram(tk_ctx* ctx, tk_bt** bt, int64_t nb, int64_t N, int64_t ncols,
+                      const int32_t* rowptr, const int32_t* col, const double* val);
+int tk_bt_destroy(tk_bt* bt);
+int tk_bt_solve(tk_ctx* ctx, const tk_bt* bt, const tk_tt* x, int64_t row0, int reps, tk_tt* y);
+
+/* tk_prec: the right preconditioner P^{-1} of eq:prec on the stacked spatial
+ * mode [u1; u2; p] (R8, R20) with the two approximations of section 5:
+ *   S^{-1} ~ S_LSC,0^{-1} = (B B^T)^{-1} B (F0 + C) B^T (B B^T)^{-1}    (eq:mean_lsc, M* = I)
+ *   (F + C)^{-1} ~ inner low-rank GMRES on (F0 + C) u = w to tol_in (eq:11_sys), itself right
+ *   preconditioned by M = (I - C) (x) I (x) (tau^-1 I + F0s) (eq:11_prec; w_avg = w0, R20)
+ * F0 + C = ((I - C)/tau) (x) I (x) blkdiag(I, I, 0) + I (x) I (x) blkdiag(F0s, F0s, 0).
+ * Inputs (HOST CSR, int32): F0s (n_v x n_v, n_v = grid^2) the mean convection-diffusion block
+ * nu_0 L + N(w_0) of one velocity component; B (n_p x 2 n_v, n_p = grid^2) the divergence
+ * [B1 B2]; n_x = 2 n_v + n_p.  tol: truncation eps of every T inside P^{-1}; inner GMRES:
+ * restart_in steps per cycle, max_cycles_in cycles, stop at ||s|| <= tol_in ||w||.
+ * Block size of both spatial solves: grid.  Synchronous (setup).
+ *
+ * tk_prec_apply: part 0 = P^{-1} v (steps 1-7 of DESIGN.md R20); part 1 = M^{-1} v (the
+ * eq:11_prec solve: cumulative sum over time, K_s^{-1} on both velocity blocks, zero pressure
+ * rows); part 2 = S_LSC,0^{-1} v_p on the pressure rows of v (positive sign, velocity rows
+ * ignored).  out: caller TT, TK_ECAP if the result's ranks exceed its capacity.  Blocking
+ * (the inner GMRES reads its Hessenberg entries on the host). */
+typedef struct tk_prec tk_prec;
+int tk_prec_create_lsc(tk_ctx* ctx, tk_prec** P, int64_t n_xi, int64_t n_t, int64_t grid,
+                       const int32_t* F_rowptr, const int32_t* F_col, const double* F_val,
+                       const int32_t* B_rowptr, const int32_t* B_col, const double* B_val,
+                       double tau, double tol, double tol_in, int restart_in, int max_cycles_in);
+int tk_prec_destroy(tk_prec* P);
+int tk_prec_apply(tk_ctx* ctx, const tk_prec* P, int part, const tk_tt* v, tk_tt* out);
+/* The preconditioner's operators (owned by P; valid while P lives): which = 0: F0 + C,
+ * 1: the embedded B^T (pressure rows -> velocity rows), 2: the embedded B. */
+const tk_op* tk_prec_operator(const tk_prec* P, int which);
+
+/* tk_gmres_cycle / tk_gmres_solve with the right preconditioner P (flexible GMRES: Alg. 3 line
+ * 4 v^_k = P^{-1} v_k, z = z_0 + sum_i y_i v^_i).  Same outputs; P must not be NULL. */
+int tk_gmres_cycle_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b, int steps,
+                     double tol, double* history_out, int* steps_done, double* explicit_out,
+                     double* step_ms_out);
+int tk_gmres_solve_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
+                     int restart, int max_cycles, double tol, double tol_gmres, double eps_soln,
+                     tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
+                     int* steps_out);
+
 #ifdef __cplusplus
 }
 #endif

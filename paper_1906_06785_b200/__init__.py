@@ -4,5 +4,7 @@ apply A = sum_k T_k (x) G_k (x) K_k to a 3-core TT, TT-round, TT dot/axpby, one 
 cycle — all in libttk.so (hand-written CUDA, C ABI in include/ttk.h).  This package is the
 thin Python binding; it never imports the CPU oracle and has no CPU fallback.
 """
-from .ttk import (TT, Context, Convection, Operator, RoundInfo, TkError, default_context, gmres_cycle, gmres_solve,  # noqa: F401
-                  lib, tt_apply_op, tt_apply_round, tt_axpby, tt_dot, tt_norm, tt_round)
+from .ttk import (TK_EARG, TK_ECAP, TK_ECUDA, TK_ENUMERIC, TK_ESHAPE, TK_OK, TT,  # noqa: F401
+                  BlockTridiag, Context, Convection, MeanLSC, Operator, RoundInfo, TkError,
+                  default_context, gmres_cycle, gmres_solve, lib, tt_apply_op, tt_apply_round,
+                  tt_axpby, tt_dot, tt_norm, tt_round)

@@ -227,6 +227,10 @@ extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
 extern "C" const char* tk_last_error(const tk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 extern "C" int64_t tk_ctx_launch_count(const tk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes);
+int tk_sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  return sync_read(ctx, host, dev, bytes);
+}
 static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
   if (bytes > ctx->pinned_bytes) {
     TK_CUDA_TRY(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1028,6 +1032,8 @@ int pass2_and_rank(tk_ctx* ctx, int64_t k, const DevBuf& GW, const DevBuf& V,
   return TK_OK;
 }
 
+}  // namespace
+
 int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
   x->r1 = 1;
   x->r2 = 1;
@@ -1037,7 +1043,6 @@ int set_zero_tt(tk_ctx* ctx, tk_tt* x) {
   return TK_OK;
 }
 
-}  // namespace
 
 // y2blk (nullable): the middle core is block diagonal with nb = R1 / rb1 diagonal blocks of
 // size rb1 x n_xi x rb2, packed in y2blk (the fused apply+round); x->U2 is then output only.
@@ -1367,52 +1372,22 @@ extern "C" int tk_scale(tk_ctx* ctx, tk_tt* x, const double* s_dev, int invert) 
   return tk_scale_rows(ctx, x->U3, x->r2 * x->n_t, s_dev, invert);
 }
 
-// ============================================================================ GMRES cycle
-namespace {
-
-// A TT whose buffers are owned by the library (stream-ordered pool).
-struct OwnedTT {
-  tk_tt t{};
-  DevBuf b1, b2, b3;
-  int make(tk_ctx* ctx, int64_t n_x, int64_t n_xi, int64_t n_t, int64_t c1, int64_t c2) {
-    t.n_x = n_x;
-    t.n_xi = n_xi;
-    t.n_t = n_t;
-    t.cap1 = c1;
-    t.cap2 = c2;
-    t.r1 = c1;
-    t.r2 = c2;
-    TK_TRY(b1.get(ctx, n_x * c1));
-    TK_TRY(b2.get(ctx, c1 * n_xi * c2));
-    TK_TRY(b3.get(ctx, c2 * n_t));
-    t.U1 = b1.p;
-    t.U2 = b2.p;
-    t.U3 = b3.p;
-    return TK_OK;
-  }
-};
-
-int clone_tt(tk_ctx* ctx, const tk_tt* src, OwnedTT& dst) {
-  TK_TRY(dst.make(ctx, src->n_x, src->n_xi, src->n_t, src->r1, src->r2));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U1, src->U1, sizeof(double) * src->n_x * src->r1,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U2, src->U2,
-                                   sizeof(double) * src->r1 * src->n_xi * src->r2,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U3, src->U3, sizeof(double) * src->r2 * src->n_t,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  return TK_OK;
+// ============================================================================ GMRES
+int tk_apply_round_owned(tk_ctx* ctx, const tk_op* op, const tk_tt* x, OwnedPtr& y, double tol) {
+  y = std::make_unique<OwnedTT>();
+  TK_TRY(y->make(ctx, x->n_x, x->n_xi, x->n_t, op->T * x->r1, op->T * x->r2));
+  return tk_apply_round(ctx, op, x, &y->t, tol, 0, nullptr, nullptr, nullptr, nullptr);
 }
-
-}  // namespace
 
 // One cycle (tk_gmres_cycle), plus what the restarted solver needs: stop once the Givens
 // least-squares residual is <= stop_abs (Alg. 3 line 2, R19) and hand back the
-// iterate z = sum_i y_i v_i (z_out, nullable) instead of / besides its explicit residual.
+// iterate z = sum_i y_i v^_i (z_out, nullable) instead of / besides its explicit residual.
+// prec (nullable): right preconditioner, v^_k = P^{-1} v_k (line 4); the flexible form keeps
+// the v^_k and forms z from them (lines 11, 13).
 static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps, double tol,
-                            double stop_abs, double* history_out, int* steps_done,
-                            double* explicit_out, double* step_ms_out,
-                            std::unique_ptr<OwnedTT>* z_out) {
+                            double stop_abs, const TkPrecFn* prec, double* history_out,
+                            int* steps_done, double* explicit_out, double* step_ms_out,
+                            OwnedPtr* z_out) {
   if (!ctx || !op || !history_out || !steps_done || steps < 1) return TK_EARG;
   TK_TRY(check_tt(ctx, b, "tk_gmres_cycle(b)"));
   if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t) {
@@ -1431,7 +1406,7 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
   double* d_one = d_negh + (steps + 1);
   TK_TRY(tk_set_scalar(ctx, d_one, 1.0));
 
-  std::vector<std::unique_ptr<OwnedTT>> V;
+  std::vector<OwnedPtr> V, Vhat;
   V.emplace_back(new OwnedTT());
   TK_TRY(clone_tt(ctx, b, *V[0]));
   TK_TRY(tk_round(ctx, &V[0]->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
@@ -1445,18 +1420,22 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
   int k_done = 0;
   for (int k = 0; k < steps; k++) {
     auto t0 = std::chrono::high_resolution_clock::now();
-    const tk_tt& vk = V[k]->t;
-    auto x = std::make_unique<OwnedTT>();
-    TK_TRY(x->make(ctx, n_x, n_xi, n_t, T * vk.r1, T * vk.r2));
-    TK_TRY(tk_apply_round(ctx, op, &vk, &x->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    const tk_tt* vk = &V[k]->t;
+    if (prec) {  // line 4: v^_k = P^{-1} v_k
+      OwnedPtr vh;
+      TK_TRY((*prec)(vk, vh));
+      Vhat.push_back(std::move(vh));
+      vk = &Vhat.back()->t;
+    }
+    OwnedPtr x;
+    TK_TRY(tk_apply_round_owned(ctx, op, vk, x, tol));
     TK_TRY(tk_norm(ctx, &x->t, d_nav));
     for (int i = 0; i <= k; i++) {
       TK_TRY(tk_dot(ctx, &x->t, &V[i]->t, d_h + i));
       TK_TRY(tk_neg_scalar(ctx, d_h + i, d_negh + i));
       auto z = std::make_unique<OwnedTT>();
       TK_TRY(z->make(ctx, n_x, n_xi, n_t, x->t.r1 + V[i]->t.r1, x->t.r2 + V[i]->t.r2));
-      TK_TRY(tk_axpby(ctx, d_one, &x->t, d_negh + i, &V[i]->t,
-                      &z->t));
+      TK_TRY(tk_axpby(ctx, d_one, &x->t, d_negh + i, &V[i]->t, &z->t));
       TK_TRY(tk_round(ctx, &z->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
       x = std::move(z);
     }
@@ -1509,14 +1488,15 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
       for (int j = i + 1; j < k_done; j++) s -= H[(size_t)i * steps + j] * y[j];
       y[i] = s / H[(size_t)i * steps + i];
     }
+    std::vector<OwnedPtr>& B = prec ? Vhat : V;  // the basis z is formed from (line 13)
     auto z = std::make_unique<OwnedTT>();
-    TK_TRY(clone_tt(ctx, &V[0]->t, *z));
+    TK_TRY(clone_tt(ctx, &B[0]->t, *z));
     TK_TRY(tk_set_scalar(ctx, d_h, y[0]));
     TK_TRY(tk_scale(ctx, &z->t, d_h, 0));
     for (int i = 1; i < k_done; i++) {
       auto z2 = std::make_unique<OwnedTT>();
-      TK_TRY(z2->make(ctx, n_x, n_xi, n_t, z->t.r1 + V[i]->t.r1, z->t.r2 + V[i]->t.r2));
-      TK_TRY(tk_axpby_host(ctx, 1.0, &z->t, y[i], &V[i]->t, &z2->t));
+      TK_TRY(z2->make(ctx, n_x, n_xi, n_t, z->t.r1 + B[i]->t.r1, z->t.r2 + B[i]->t.r2));
+      TK_TRY(tk_axpby_host(ctx, 1.0, &z->t, y[i], &B[i]->t, &z2->t));
       TK_TRY(tk_round(ctx, &z2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
       z = std::move(z2);
     }
@@ -1538,54 +1518,63 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
   return TK_OK;
 }
 
+static int gmres_cycle_entry(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
+                             int steps, double tol, double* history_out, int* steps_done,
+                             double* explicit_out, double* step_ms_out) {
+  if (!ctx) return TK_EARG;
+  TkPrecFn fn;
+  if (P) fn = tk_prec_fn(ctx, P, 0);
+  return gmres_cycle_impl(ctx, op, b, steps, tol, 0.0, P ? &fn : nullptr, history_out,
+                          steps_done, explicit_out, step_ms_out, nullptr);
+}
+
 extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps,
                               double tol, double* history_out, int* steps_done,
                               double* explicit_out, double* step_ms_out) {
-  return gmres_cycle_impl(ctx, op, b, steps, tol, 0.0, history_out, steps_done, explicit_out,
-                          step_ms_out, nullptr);
+  return gmres_cycle_entry(ctx, op, nullptr, b, steps, tol, history_out, steps_done,
+                           explicit_out, step_ms_out);
 }
 
-// Complete, restarted low-rank GMRES (NEXT-2; Alg. 3 with P = I, eq:eps_soln; R19).
-extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart,
-                              int max_cycles, double tol, double tol_gmres, double eps_soln,
-                              tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
-                              int* steps_out) {
-  if (!ctx || !op || !z || !explicit_out || !cycles_done || restart < 1 || max_cycles < 0 ||
-      !(tol >= 0.0) || !(tol_gmres >= 0.0))
-    return TK_EARG;
-  TK_TRY(check_tt(ctx, b, "tk_gmres_solve(b)"));
-  if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t || z->n_x != op->n_x ||
-      z->n_xi != op->n_xi || z->n_t != op->n_t) {
-    ctx->err = "tk_gmres_solve: mode sizes differ from the operator's";
-    return TK_ESHAPE;
-  }
+extern "C" int tk_gmres_cycle_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
+                                int steps, double tol, double* history_out, int* steps_done,
+                                double* explicit_out, double* step_ms_out) {
+  if (!P) return TK_EARG;
+  return gmres_cycle_entry(ctx, op, P, b, steps, tol, history_out, steps_done, explicit_out,
+                           step_ms_out);
+}
+
+// Complete, restarted low-rank GMRES (NEXT-2; Alg. 3, eq:eps_soln; R19), flexible
+// with a right preconditioner (NEXT-3).
+int tk_gmres_solve_core(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart,
+                        int max_cycles, double tol, double tol_gmres, double eps_soln,
+                        const TkPrecFn* prec, OwnedPtr& zt, std::vector<double>& explicit_out,
+                        std::vector<double>* ls_out, std::vector<int>* steps_out) {
   if (eps_soln < 0.0) eps_soln = tol;
   const int64_t n_x = b->n_x, n_xi = b->n_xi, n_t = b->n_t;
   const int T = op->T;
   DevBuf sc;
   TK_TRY(sc.get(ctx, 1));
   TK_TRY(tk_norm(ctx, b, sc.p));
-  double bnorm;
+  double bnorm, e;
   TK_TRY(sync_read(ctx, &bnorm, sc.p, sizeof(double)));
   // s_0 = T(b)  (z_0 = 0)
   auto s_ = std::make_unique<OwnedTT>();
   TK_TRY(clone_tt(ctx, b, *s_));
   TK_TRY(tk_round(ctx, &s_->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
   TK_TRY(tk_norm(ctx, &s_->t, sc.p));
-  TK_TRY(sync_read(ctx, explicit_out, sc.p, sizeof(double)));
-  std::unique_ptr<OwnedTT> zt;
-  int cyc = 0;
-  for (; cyc < max_cycles; cyc++) {
+  TK_TRY(sync_read(ctx, &e, sc.p, sizeof(double)));
+  explicit_out.assign(1, e);
+  zt.reset();
+  for (int cyc = 0; cyc < max_cycles; cyc++) {
     if (explicit_out[cyc] <= tol_gmres * bnorm) break;
     std::vector<double> hist(restart + 1, 0.0);
     int done = 0;
-    std::unique_ptr<OwnedTT> dz;
-    TK_TRY(gmres_cycle_impl(ctx, op, &s_->t, restart, tol, tol_gmres * bnorm, hist.data(), &done,
-                            nullptr, nullptr, &dz));
+    OwnedPtr dz;
+    TK_TRY(gmres_cycle_impl(ctx, op, &s_->t, restart, tol, tol_gmres * bnorm, prec, hist.data(),
+                            &done, nullptr, nullptr, &dz));
     if (ls_out)
-      for (int i = 0; i <= restart; i++)
-        ls_out[(size_t)cyc * (restart + 1) + i] = i <= done ? hist[i] : 0.0;
-    if (steps_out) steps_out[cyc] = done;
+      for (int i = 0; i <= restart; i++) ls_out->push_back(i <= done ? hist[i] : 0.0);
+    if (steps_out) steps_out->push_back(done);
     // z <- T_eps_soln(z + dz)   (eq:eps_soln)
     if (!zt) {
       zt = std::move(dz);
@@ -1606,9 +1595,39 @@ extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     TK_TRY(tk_round(ctx, &s2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
     s_ = std::move(s2);
     TK_TRY(tk_norm(ctx, &s_->t, sc.p));
-    TK_TRY(sync_read(ctx, explicit_out + cyc + 1, sc.p, sizeof(double)));
+    TK_TRY(sync_read(ctx, &e, sc.p, sizeof(double)));
+    explicit_out.push_back(e);
   }
+  return TK_OK;
+}
+
+static int gmres_solve_entry(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
+                             int restart, int max_cycles, double tol, double tol_gmres,
+                             double eps_soln, tk_tt* z, double* explicit_out, double* ls_out,
+                             int* cycles_done, int* steps_out) {
+  if (!ctx || !op || !z || !explicit_out || !cycles_done || restart < 1 || max_cycles < 0 ||
+      !(tol >= 0.0) || !(tol_gmres >= 0.0))
+    return TK_EARG;
+  TK_TRY(check_tt(ctx, b, "tk_gmres_solve(b)"));
+  if (b->n_x != op->n_x || b->n_xi != op->n_xi || b->n_t != op->n_t || z->n_x != op->n_x ||
+      z->n_xi != op->n_xi || z->n_t != op->n_t) {
+    ctx->err = "tk_gmres_solve: mode sizes differ from the operator's";
+    return TK_ESHAPE;
+  }
+  TkPrecFn fn;
+  if (P) fn = tk_prec_fn(ctx, P, 0);
+  OwnedPtr zt;
+  std::vector<double> expl, ls;
+  std::vector<int> steps;
+  TK_TRY(tk_gmres_solve_core(ctx, op, b, restart, max_cycles, tol, tol_gmres, eps_soln,
+                             P ? &fn : nullptr, zt, expl, &ls, &steps));
+  const int cyc = (int)steps.size();
   *cycles_done = cyc;
+  for (size_t i = 0; i < expl.size(); i++) explicit_out[i] = expl[i];
+  if (ls_out)
+    for (size_t i = 0; i < ls.size(); i++) ls_out[i] = ls[i];
+  if (steps_out)
+    for (int i = 0; i < cyc; i++) steps_out[i] = steps[i];
   if (!zt) {  // b rounded to (numerically) zero or max_cycles == 0: z = 0
     TK_TRY(set_zero_tt(ctx, z));
     return TK_OK;
@@ -1617,6 +1636,7 @@ extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
     ctx->err = "tk_gmres_solve: solution ranks exceed z's capacity";
     return TK_ECAP;
   }
+  const int64_t n_x = b->n_x, n_xi = b->n_xi, n_t = b->n_t;
   z->r1 = zt->t.r1;
   z->r2 = zt->t.r2;
   TK_TRY(tk_copy2d(ctx, n_x, z->r1, zt->t.U1, z->r1, z->U1, z->r1));
@@ -1624,4 +1644,21 @@ extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
   TK_TRY(tk_copy2d(ctx, z->r2, n_t, zt->t.U3, n_t, z->U3, n_t));
   TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return TK_OK;
+}
+
+extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart,
+                              int max_cycles, double tol, double tol_gmres, double eps_soln,
+                              tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
+                              int* steps_out) {
+  return gmres_solve_entry(ctx, op, nullptr, b, restart, max_cycles, tol, tol_gmres, eps_soln,
+                           z, explicit_out, ls_out, cycles_done, steps_out);
+}
+
+extern "C" int tk_gmres_solve_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
+                                int restart, int max_cycles, double tol, double tol_gmres,
+                                double eps_soln, tk_tt* z, double* explicit_out, double* ls_out,
+                                int* cycles_done, int* steps_out) {
+  if (!P) return TK_EARG;
+  return gmres_solve_entry(ctx, op, P, b, restart, max_cycles, tol, tol_gmres, eps_soln, z,
+                           explicit_out, ls_out, cycles_done, steps_out);
 }

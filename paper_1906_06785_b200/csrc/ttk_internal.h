@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -199,6 +201,58 @@ struct DevBuf {
     p = nullptr;
   }
 };
+
+
+// A TT whose buffers are owned by the library (stream-ordered pool).
+struct OwnedTT {
+  tk_tt t{};
+  DevBuf b1, b2, b3;
+  int make(tk_ctx* ctx, int64_t n_x, int64_t n_xi, int64_t n_t, int64_t c1, int64_t c2) {
+    t.n_x = n_x;
+    t.n_xi = n_xi;
+    t.n_t = n_t;
+    t.cap1 = c1;
+    t.cap2 = c2;
+    t.r1 = c1;
+    t.r2 = c2;
+    TK_TRY(b1.get(ctx, n_x * c1));
+    TK_TRY(b2.get(ctx, c1 * n_xi * c2));
+    TK_TRY(b3.get(ctx, c2 * n_t));
+    t.U1 = b1.p;
+    t.U2 = b2.p;
+    t.U3 = b3.p;
+    return TK_OK;
+  }
+};
+using OwnedPtr = std::unique_ptr<OwnedTT>;
+
+inline int clone_tt(tk_ctx* ctx, const tk_tt* src, OwnedTT& dst) {
+  TK_TRY(dst.make(ctx, src->n_x, src->n_xi, src->n_t, src->r1, src->r2));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U1, src->U1, sizeof(double) * src->n_x * src->r1,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U2, src->U2,
+                                   sizeof(double) * src->r1 * src->n_xi * src->r2,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U3, src->U3, sizeof(double) * src->r2 * src->n_t,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  return TK_OK;
+}
+
+// A right preconditioner v -> P^{-1} v (Alg. 3 line 4) as the GMRES drivers see it: writes a
+// new library-owned TT.
+using TkPrecFn = std::function<int(const tk_tt* v, OwnedPtr& out)>;
+// The restarted low-rank GMRES core (tk_gmres_solve / tk_gmres_solve_p and the inner solve of
+// the LSC preconditioner): flexible when prec != nullptr.  z_out is null when b rounds to zero
+// or max_cycles == 0.  explicit_out gets ||s_0||, then ||s|| per cycle; ls_out (nullable) per
+// cycle the least-squares history (restart + 1 entries, zero padded); steps_out per cycle.
+int tk_gmres_solve_core(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restart,
+                        int max_cycles, double tol, double tol_gmres, double eps_soln,
+                        const TkPrecFn* prec, OwnedPtr& z_out, std::vector<double>& explicit_out,
+                        std::vector<double>* ls_out, std::vector<int>* steps_out);
+TkPrecFn tk_prec_fn(tk_ctx* ctx, const tk_prec* P, int part);
+int tk_apply_round_owned(tk_ctx* ctx, const tk_op* op, const tk_tt* x, OwnedPtr& y, double tol);
+int set_zero_tt(tk_ctx* ctx, tk_tt* x);
+int tk_sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes);
 
 // ----------------------------------------------------------------------------- kernels (host wrappers)
 // Row-major fp64 GEMM on DMMA (mma.sync m8n8k4 f64):

@@ -24,7 +24,10 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_apply_round", "tk_dot",
             "tk_norm", "tk_axpby", "tk_axpby_host", "tk_scale", "tk_gmres_cycle",
             "tk_gmres_solve", "tk_op_group_space", "tk_op_set_spmm_kernel", "tk_op_concat",
-            "tk_conv_create", "tk_conv_destroy", "tk_op_convection"]
+            "tk_conv_create", "tk_conv_destroy", "tk_op_convection",
+            "tk_bt_create", "tk_bt_create_gram", "tk_bt_destroy", "tk_bt_solve",
+            "tk_prec_create_lsc", "tk_prec_destroy", "tk_prec_apply", "tk_prec_operator",
+            "tk_gmres_cycle_p", "tk_gmres_solve_p"]
 
 
 class TkError(RuntimeError):
@@ -83,10 +86,25 @@ def lib():
     L.tk_gmres_cycle.argtypes = [P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
     L.tk_gmres_solve.argtypes = [P, P, TTP, I, I, D, D, D, TTP, DP, DP, ctypes.POINTER(I),
                                  ctypes.POINTER(I)]
+    IP = ctypes.POINTER(ctypes.c_int32)
+    L.tk_bt_create.argtypes = [P, ctypes.POINTER(P), I64, I64, P, P, P, D]
+    L.tk_bt_create_gram.argtypes = [P, ctypes.POINTER(P), I64, I64, I64, P, P, P]
+    L.tk_bt_destroy.argtypes = [P]
+    L.tk_bt_solve.argtypes = [P, P, TTP, I64, I, TTP]
+    L.tk_prec_create_lsc.argtypes = [P, ctypes.POINTER(P), I64, I64, I64, P, P, P, P, P, P, D, D,
+                                     D, I, I]
+    L.tk_prec_destroy.argtypes = [P]
+    L.tk_prec_apply.argtypes = [P, P, I, TTP, TTP]
+    L.tk_prec_operator.argtypes = [P, I]
+    L.tk_prec_operator.restype = P
+    L.tk_gmres_cycle_p.argtypes = [P, P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
+    L.tk_gmres_solve_p.argtypes = [P, P, P, TTP, I, I, D, D, D, TTP, DP, DP, ctypes.POINTER(I),
+                                   ctypes.POINTER(I)]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
-        if name not in ("tk_version", "tk_last_error", "tk_ctx_launch_count"):
+        if name not in ("tk_version", "tk_last_error", "tk_ctx_launch_count",
+                        "tk_prec_operator"):
             getattr(L, name).restype = I
     _lib = L
     return L
@@ -408,8 +426,9 @@ def tt_axpby(a, x: TT, b, y: TT, ctx: Context | None = None, out: TT | None = No
     return z
 
 
-def gmres_cycle(op: Operator, b: TT, steps: int = 20, tol: float = 1e-6):
-    """One low-rank GMRES cycle (tk_gmres_cycle).  Returns dict(history, steps, explicit, step_ms)."""
+def gmres_cycle(op: Operator, b: TT, steps: int = 20, tol: float = 1e-6, prec=None):
+    """One low-rank GMRES cycle (tk_gmres_cycle; tk_gmres_cycle_p with a MeanLSC prec: flexible
+    right preconditioning).  Returns dict(history, steps, explicit, step_ms)."""
     ctx = op.ctx
     D = ctypes.c_double
     hist = (D * (steps + 1))()
@@ -417,15 +436,21 @@ def gmres_cycle(op: Operator, b: TT, steps: int = 20, tol: float = 1e-6):
     done = ctypes.c_int()
     expl = D()
     bs = b.struct()
-    ctx.check(lib().tk_gmres_cycle(ctx._h, op._h, ctypes.byref(bs), int(steps), float(tol), hist,
-                                   ctypes.byref(done), ctypes.byref(expl), ms))
+    if prec is None:
+        ctx.check(lib().tk_gmres_cycle(ctx._h, op._h, ctypes.byref(bs), int(steps), float(tol),
+                                       hist, ctypes.byref(done), ctypes.byref(expl), ms))
+    else:
+        ctx.check(lib().tk_gmres_cycle_p(ctx._h, op._h, prec._h, ctypes.byref(bs), int(steps),
+                                         float(tol), hist, ctypes.byref(done), ctypes.byref(expl),
+                                         ms))
     k = done.value
     return dict(history=np.array(hist[: k + 1]), steps=k, explicit=expl.value,
                 step_ms=np.array(ms[:k]))
 
 
 def gmres_solve(op: Operator, b: TT, restart: int = 20, max_cycles: int = 5, tol: float = 1e-6,
-                tol_gmres: float = 1e-8, eps_soln: float = -1.0, cap: tuple | None = None):
+                tol_gmres: float = 1e-8, eps_soln: float = -1.0, cap: tuple | None = None,
+                prec=None):
     """Complete restarted low-rank GMRES (tk_gmres_solve; Alg. 3 + eq:eps_soln, P = I).
     Returns dict(z, explicit, ls, cycles, steps).  cap: rank capacity of z (default bounded by
     the mode sizes and 512)."""
@@ -439,11 +464,119 @@ def gmres_solve(op: Operator, b: TT, restart: int = 20, max_cycles: int = 5, tol
     steps = (ctypes.c_int * max(max_cycles, 1))()
     done = ctypes.c_int()
     bs, zs = b.struct(), z.struct()
-    ctx.check(lib().tk_gmres_solve(ctx._h, op._h, ctypes.byref(bs), int(restart), int(max_cycles),
-                                   float(tol), float(tol_gmres), float(eps_soln), ctypes.byref(zs),
-                                   expl, ls, ctypes.byref(done), steps))
+    args = (ctypes.byref(bs), int(restart), int(max_cycles), float(tol), float(tol_gmres),
+            float(eps_soln), ctypes.byref(zs), expl, ls, ctypes.byref(done), steps)
+    if prec is None:
+        ctx.check(lib().tk_gmres_solve(ctx._h, op._h, *args))
+    else:
+        ctx.check(lib().tk_gmres_solve_p(ctx._h, op._h, prec._h, *args))
     z._update(zs)
     c = done.value
     lsv = np.array(ls[: c * (restart + 1)]).reshape(c, restart + 1) if c else np.zeros((0, restart + 1))
     return dict(z=z, explicit=np.array(expl[: c + 1]), cycles=c, steps=list(steps[:c]),
                 ls=[row[: steps[i] + 1] for i, row in enumerate(lsv)])
+
+
+# ----------------------------------------------------------------------------- NEXT-3
+def _csr_arrays(m):
+    rp = np.ascontiguousarray(m.indptr, dtype=np.int32)
+    cl = np.ascontiguousarray(m.indices, dtype=np.int32)
+    vl = np.ascontiguousarray(m.data, dtype=np.float64)
+    return rp, cl, vl
+
+
+def _default_cap(n_x, n_xi, n_t):
+    return (max(1, min(n_x, n_xi * n_t, 1024)), max(1, min(n_t, n_x * n_xi, 1024)))
+
+
+class BlockTridiag:
+    """Block-tridiagonal direct solver of a spatial factor (tk_bt_create / _gram): K = A + shift I
+    (gram=False) or K = A A^T (gram=True) for the scipy CSR A, blocks of N rows."""
+
+    def __init__(self, A, nb: int, N: int, shift: float = 0.0, gram: bool = False,
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.n = int(nb) * int(N)
+        rp, cl, vl = _csr_arrays(A)
+        self._h = ctypes.c_void_p()
+        if gram:
+            rc = lib().tk_bt_create_gram(self.ctx._h, ctypes.byref(self._h), int(nb), int(N),
+                                         int(A.shape[1]), rp.ctypes.data, cl.ctypes.data,
+                                         vl.ctypes.data)
+        else:
+            rc = lib().tk_bt_create(self.ctx._h, ctypes.byref(self._h), int(nb), int(N),
+                                    rp.ctypes.data, cl.ctypes.data, vl.ctypes.data, float(shift))
+        self.ctx.check(rc)
+
+    def solve(self, x: TT, row0: int = 0, reps: int = 1) -> TT:
+        """(I (x) I (x) K^{-1}) x on rows [row0, row0 + reps n) of the space core, zero elsewhere."""
+        y = TT(x.n_x, x.n_xi, x.n_t, x.r1, x.r2)
+        xs, ys = x.struct(), y.struct()
+        self.ctx.check(lib().tk_bt_solve(self.ctx._h, self._h, ctypes.byref(xs), int(row0),
+                                         int(reps), ctypes.byref(ys)))
+        y._update(ys)
+        return y
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().tk_bt_destroy(self._h)
+        except Exception:
+            pass
+
+
+class MeanLSC:
+    """P^{-1} of eq:prec with S_LSC,0 (eq:mean_lsc) and the inner (F0 + C) GMRES preconditioned
+    by M (eq:11_prec), tk_prec_create_lsc.  F0s (n_v x n_v) and B (n_p x 2 n_v) scipy CSR."""
+
+    def __init__(self, F0s, B, tau: float, n_xi: int, n_t: int, tol: float, grid: int,
+                 tol_in: float = 1e-1, restart_in: int = 10, max_cycles_in: int = 3,
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.n_x = 2 * F0s.shape[0] + B.shape[0]
+        self.n_xi, self.n_t = int(n_xi), int(n_t)
+        f = _csr_arrays(F0s)
+        b = _csr_arrays(B)
+        self._h = ctypes.c_void_p()
+        self.ctx.check(lib().tk_prec_create_lsc(
+            self.ctx._h, ctypes.byref(self._h), self.n_xi, self.n_t, int(grid),
+            f[0].ctypes.data, f[1].ctypes.data, f[2].ctypes.data,
+            b[0].ctypes.data, b[1].ctypes.data, b[2].ctypes.data,
+            float(tau), float(tol), float(tol_in), int(restart_in), int(max_cycles_in)))
+
+    def apply(self, v: TT, part: int = 0, cap: tuple | None = None) -> TT:
+        """part 0: P^{-1} v; 1: M^{-1} v (eq:11_prec); 2: S_LSC,0^{-1} v_p (eq:mean_lsc)."""
+        cap = cap or _default_cap(v.n_x, v.n_xi, v.n_t)
+        out = TT(v.n_x, v.n_xi, v.n_t, 1, 1, cap[0], cap[1])
+        vs, os_ = v.struct(), out.struct()
+        self.ctx.check(lib().tk_prec_apply(self.ctx._h, self._h, int(part), ctypes.byref(vs),
+                                           ctypes.byref(os_)))
+        out._update(os_)
+        return out
+
+    def operator(self, which: int) -> Operator:
+        """A borrowed view of the preconditioner's operators: 0 = F0 + C, 1 = B^T, 2 = B."""
+        h = lib().tk_prec_operator(self._h, int(which))
+        if not h:
+            raise TkError(TK_EARG, "tk_prec_operator")
+        return _Borrowed(self, h)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().tk_prec_destroy(self._h)
+        except Exception:
+            pass
+
+
+class _Borrowed(Operator):
+    """An operator handle owned by another object (never destroyed here)."""
+
+    def __init__(self, owner, h):
+        self.owner = owner  # keeps the owner (and so the handle) alive
+        self.ctx, self.n_x, self.n_xi, self.n_t = owner.ctx, owner.n_x, owner.n_xi, owner.n_t
+        self._h = ctypes.c_void_p(h)
+        self.T = int(lib().tk_op_terms(self._h))
+
+    def __del__(self):
+        pass
