@@ -290,6 +290,29 @@ int tk_gmres_solve_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt
                      tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
                      int* steps_out);
 
+/* ===================================================================================== NEXT-4
+ * The inexact Picard iteration of PAPER.md Alg. 1 (alg:picard, :199-213) for the all-at-once
+ * stochastic Galerkin Navier-Stokes system eq:ns_sys_all (:148-156), reading R21 of DESIGN.md:
+ *   line 1: z_0 = GMRES solve of stokes z = f to ||s|| <= tol_gmres ||f|| (:538)
+ *           L = stokes + N(T_eps_conv(z_0)) (eq:N_kron from the iterate's cores on the device,
+ *           eq:eps_conv), r_0 = T(f - L z_0)
+ *   while ||r_i|| > tol_picard ||f|| and i < maxit:                                (line 2)
+ *     dz = GMRES solve of L dz = r_{i-1} to ||s|| <= tol_gmres ||r_{i-1}|| (eq:inexact_solve)
+ *     z_i = T(z_{i-1} + dz); L = stokes + N(T_eps_conv(z_i)); r_i = T(f - L z_i)  (lines 5-7)
+ * Every T at eps_gmres (eps_conv < 0: eps_gmres); GMRES restarted every `restart` steps, at
+ * most max_cycles cycles, right-preconditioned by P when P != NULL (NEXT-3).
+ *   stokes: the fixed part (time-mass + Stokes block + KL viscosity terms, no convection)
+ *   conv:   the discretisation of N(u) (tk_conv_create, d = 2 velocity components)
+ *   f:      the right-hand side [f^u; f^p] (DEVICE TT)
+ *   z_out:  OUT, caller TT (TK_ECAP if the solution's ranks exceed its capacity)
+ *   residuals_out (HOST, maxit + 1): ||r_0||, ||r_1||, ...;  iterations (HOST): i on exit
+ *   ranks_out (HOST, nullable, 2 (maxit + 1)): (r1, r2) of every iterate.
+ * Blocking. */
+int tk_picard(tk_ctx* ctx, const tk_op* stokes, const tk_conv* conv, const tk_prec* P,
+              const tk_tt* f, double tol_picard, int maxit, double tol_gmres, double eps_gmres,
+              double eps_conv, int restart, int max_cycles, tk_tt* z_out, double* residuals_out,
+              int* iterations, int64_t* ranks_out);
+
 #ifdef __cplusplus
 }
 #endif

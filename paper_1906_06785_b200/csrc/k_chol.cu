@@ -612,7 +612,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     constexpr int NBR = 16;
     const size_t rsmem = (size_t)NBR * n * sizeof(double);
     static size_t rattr = 0;
-    if (rsmem > 48 * 1024 && rattr < rsmem) {
+    if (rattr < rsmem) {  // (also at <= 48 KB: the kernel has static shared memory too)
       cudaFuncSetAttribute(pchol_panel_reg_k<1, NBR, 2 * PT>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
       rattr = rsmem;
@@ -641,7 +641,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
     constexpr int NBR = 32;
     const size_t rsmem = (size_t)NBR * n * sizeof(double);
     static size_t rattr = 0;
-    if (rsmem > 48 * 1024 && rattr < rsmem) {
+    if (rattr < rsmem) {  // (also at <= 48 KB: the kernel has static shared memory too)
       cudaFuncSetAttribute(pchol_panel_reg_k<1, NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)rsmem);
       rattr = rsmem;
@@ -668,7 +668,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   const int nb = (int)std::max<int64_t>(4, std::min<int64_t>(32, (200 * 1024 / 8) / n - 1));
   const size_t smem = ((size_t)nb + 1) * n * sizeof(double);
   static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
+  if (attr < smem) {  // (also at <= 48 KB: static shared memory counts too)
     cudaFuncSetAttribute(pchol_panel_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }

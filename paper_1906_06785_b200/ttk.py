@@ -27,7 +27,7 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_conv_create", "tk_conv_destroy", "tk_op_convection",
             "tk_bt_create", "tk_bt_create_gram", "tk_bt_destroy", "tk_bt_solve",
             "tk_prec_create_lsc", "tk_prec_destroy", "tk_prec_apply", "tk_prec_operator",
-            "tk_gmres_cycle_p", "tk_gmres_solve_p"]
+            "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard"]
 
 
 class TkError(RuntimeError):
@@ -100,6 +100,8 @@ def lib():
     L.tk_gmres_cycle_p.argtypes = [P, P, P, TTP, I, D, DP, ctypes.POINTER(I), DP, DP]
     L.tk_gmres_solve_p.argtypes = [P, P, P, TTP, I, I, D, D, D, TTP, DP, DP, ctypes.POINTER(I),
                                    ctypes.POINTER(I)]
+    L.tk_picard.argtypes = [P, P, P, P, TTP, D, I, D, D, D, I, I, TTP, DP, ctypes.POINTER(I),
+                            ctypes.POINTER(I64)]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
@@ -580,3 +582,27 @@ class _Borrowed(Operator):
 
     def __del__(self):
         pass
+
+
+# ----------------------------------------------------------------------------- NEXT-4
+def picard(stokes: Operator, conv: Convection, f: TT, tol_picard: float = 1e-4, maxit: int = 10,
+           tol_gmres: float = 1e-1, eps_gmres: float = 1e-3, eps_conv: float = -1.0,
+           restart: int = 20, max_cycles: int = 5, prec: "MeanLSC | None" = None,
+           cap: tuple | None = None):
+    """Inexact Picard iteration of Alg. 1 (tk_picard).  Returns dict(z, residuals, iterations,
+    ranks)."""
+    ctx = stokes.ctx
+    cap = cap or _default_cap(f.n_x, f.n_xi, f.n_t)
+    z = TT(f.n_x, f.n_xi, f.n_t, 1, 1, cap[0], cap[1])
+    res = (ctypes.c_double * (maxit + 1))()
+    rk = (ctypes.c_int64 * (2 * (maxit + 1)))()
+    it = ctypes.c_int()
+    fs, zs = f.struct(), z.struct()
+    ctx.check(lib().tk_picard(ctx._h, stokes._h, conv._h, prec._h if prec is not None else None,
+                              ctypes.byref(fs), float(tol_picard), int(maxit), float(tol_gmres),
+                              float(eps_gmres), float(eps_conv), int(restart), int(max_cycles),
+                              ctypes.byref(zs), res, ctypes.byref(it), rk))
+    z._update(zs)
+    n = it.value
+    return dict(z=z, residuals=np.array(res[: n + 1]), iterations=n,
+                ranks=[(rk[2 * i], rk[2 * i + 1]) for i in range(n + 1)])

@@ -27,7 +27,8 @@ class Config:
     input_kind: str       # "gauss" (N(0,1) cores) or "decay" (0.7^i spectra)
     gmres_steps: int = 0  # c5 only
     rhs_ranks: tuple = field(default=(0, 0))
-    operator: str = "oseen"  # "convection": the TT convection operator N(u~) (NEXT-1, c6)
+    operator: str = "oseen"  # "convection": the TT convection operator N(u~) (NEXT-1, c6);
+    #                          "picard": the Navier-Stokes Picard problem (NEXT-4, c7)
     velocity_ranks: tuple = field(default=(0, 0))  # ranks of the velocity TT u~ (c6)
 
     @property
@@ -38,6 +39,8 @@ class Config:
     def n_terms(self) -> int:
         if self.operator == "convection":  # one term per (alpha_1, alpha_2), eq:N_kron
             return self.velocity_ranks[0] * self.velocity_ranks[1]
+        if self.operator == "picard":  # time-mass + Stokes block + m KL terms (N(u) is added)
+            return 2 + self.m
         # time-mass + mean Oseen + m KL terms + (R_w - 1) wind terms (R8)
         return 2 + self.m + (self.wind_rank - 1)
 
@@ -58,6 +61,15 @@ CONFIGS = {
     # velocity TT of ranks (8, 8) -> 64 terms, x the c2-style input (20, 20) -> (1280, 1280)
     "c6": Config("c6", 5, 64, 4, 3, 64, 1.0 / 64, _nus(4), 1, (20, 20), 1e-8, 80, "decay",
                  operator="convection", velocity_ranks=(8, 8)),
+    # NEXT-4, not BASELINE.json configs: the inexact Picard iteration of Alg. 1
+    # (eq:inexact_solve :536-538) on the all-at-once stochastic Galerkin
+    # Navier-Stokes system (eq:ns_sys_all) with a seeded body force; nu_0 = 1/50 as in the
+    # paper's Table 1, KL viscosity nu_l = 0.002 / l; tol = eps_gmres.
+    # c7: the oracle-parity size; c8: GPU-scale (checked through properties)
+    "c7": Config("c7", 6, 4, 1, 2, 4, 1.0 / 4, (0.02, 0.002), 1, (1, 1), 1e-5, 0, "gauss",
+                 operator="picard"),
+    "c8": Config("c8", 7, 16, 2, 2, 8, 1.0 / 8, (0.02, 0.002, 0.001), 1, (1, 1), 1e-4, 0,
+                 "gauss", operator="picard"),
 }
 
 

@@ -77,6 +77,8 @@ def _csr32(k: sp.csr_matrix) -> sp.csr_matrix:
 
 
 def build_operator(cfg: Config) -> KronSumOp:
+    if cfg.operator == "picard":
+        return build_stokes_operator(cfg)
     if cfg.operator == "convection":
         raise ValueError("the convection operator is built by the library (tk_op_convection) "
                          "or by oracle.convection from synth.operator.convection_stencils")
@@ -131,7 +133,47 @@ def mean_blocks(cfg: Config):
     (n_p x 2 n_v).  Returns (F0s, B) as CSR; no preconditioner arithmetic."""
     rng = np.random.default_rng([cfg.index, 0])
     n = cfg.grid
+    if cfg.operator == "picard":  # no fixed wind: the Stokes mean block (w_avg = 0, R21)
+        f0 = _csr32(cfg.nus[0] * fd.laplacian(n))
+        b = _csr32(sp.hstack([fd.forward_dx(n), fd.forward_dy(n)]))
+        return f0, b
     winds = [fd.sinusoid_wind(n, rng, scale=0.5 ** j) for j in range(cfg.wind_rank)]
     f0 = _csr32(cfg.nus[0] * fd.laplacian(n) + fd.convection(n, *winds[0]))
     b = _csr32(sp.hstack([fd.forward_dx(n), fd.forward_dy(n)]))
     return f0, b
+
+
+def build_stokes_operator(cfg: Config) -> KronSumOp:
+    """The fixed part of the all-at-once Navier-Stokes matrix (eq:ns_sys_all, eq:F without
+    N(u)): time-mass (I - C)/tau (x) I (x) blkdiag(I, I, 0), the mean Stokes block
+    I (x) G_0 (x) [[nu0 L, 0, B1^T], [0, nu0 L, B2^T], [B1, B2, 0]] and the KL terms
+    I (x) G_l (x) blkdiag(nu_l L, nu_l L, 0) — the Stokes operator of Alg. 1 line 1
+    (PAPER.md:197).  The convection N(u) of the current iterate is added by the Picard driver."""
+    n = cfg.grid
+    gs = gpc.g_matrices(cfg.m, cfg.p)
+    nxi = gs[0].shape[0]
+    zero = np.zeros(n * n)
+    terms = []
+    kl, ku, b = band_backward_euler(cfg.n_t, cfg.tau)
+    terms.append(Term("time-mass", kl, ku, b, gs[0], _csr32(fd.mass_block(n))))
+    kl, ku, b = band_identity(cfg.n_t)
+    terms.append(Term("stokes", kl, ku, b, gs[0],
+                      _csr32(fd.oseen_block(n, cfg.nus[0], (zero, zero)))))
+    for l in range(1, cfg.m + 1):
+        kl, ku, b = band_identity(cfg.n_t)
+        terms.append(Term(f"kl{l}", kl, ku, b, gs[l], _csr32(fd.viscous_block(n, cfg.nus[l]))))
+    return KronSumOp(cfg.n_x, nxi, cfg.n_t, terms)
+
+
+def picard_forcing(cfg: Config, n_xi: int, amp: float = 1.0):
+    """Right-hand side f = [f^u; f^p] of eq:ns_sys_all for the Picard problem (input data):
+    a seeded smooth body force in the mean chaos mode, constant in time, f^p = 0 — rank (1, 1).
+    f^u_c = amp * sum of 3 random sinusoids (the wind recipe of DESIGN.md R11)."""
+    rng = np.random.default_rng([cfg.index, 4])
+    n = cfg.grid
+    f1, f2 = fd.sinusoid_wind(n, rng)
+    u1 = np.concatenate([f1, f2, np.zeros(n * n)])[:, None] * amp
+    u2 = np.zeros((1, n_xi, 1))
+    u2[0, 0, 0] = 1.0
+    u3 = np.ones((1, cfg.n_t))
+    return u1, u2, u3

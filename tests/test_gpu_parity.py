@@ -234,6 +234,16 @@ def test_round_parity_random(seed, ctx):
     check_round(x, tol, 0, ctx)
 
 
+@pytest.mark.parametrize("r2", [128, 160, 192, 200, 256, 520])
+def test_round_wide_time_bond(r2, ctx):
+    """R2 >= 128 runs the rank-revealing orth_rows on the R2 x n_t time core (pivoted Cholesky of
+    an R2 x R2 Gram): every panel-kernel shared-memory size class, including the exact 48 KB
+    edge at R2 = 192 (32 panel rows x 192 doubles) that once failed to launch."""
+    rng = np.random.default_rng(700 + r2)
+    x = random_tt(rng, 40, 3, 6, 5, r2)
+    check_round(x, 1e-8, 0, ctx)
+
+
 def test_round_rank_one_and_zero(ctx):
     rng = np.random.default_rng(9)
     x = random_tt(rng, 5, 4, 3, 1, 1)
