@@ -24,9 +24,12 @@
  * which rounds in place (ranks never grow).
  *
  * Errors: every call returns TK_OK (0) or a negative code; tk_last_error(ctx) returns a
- * message.  No call falls back to the CPU.  All calls are asynchronous on the context stream
- * except where noted (tk_round and tk_gmres_cycle block on the host to read the ranks they
- * choose; tk_*_host variants block to return a host scalar).
+ * message.  No call falls back to the CPU.  Work is enqueued on the context stream.  By
+ * default tk_round / tk_apply_round block the host until the ranks they choose are known (the
+ * launches after a rank decision are sized on the host).  In async mode (tk_ctx_set_async)
+ * they return at once: the rounding runs on a library worker thread, the context stream waits
+ * for it in stream order, and the ranks are published into the caller's tk_tt by
+ * tk_sync_ranks.  The GMRES / preconditioner / Picard drivers and the tk_*_host variants block.
  */
 #ifndef TTK_H
 #define TTK_H
@@ -80,6 +83,29 @@ int64_t tk_ctx_launch_count(const tk_ctx* ctx);
  * records. */
 int tk_ctx_profile(tk_ctx* ctx, int enable);
 int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len);
+
+/* Asynchronous rounding.  on != 0: from now on tk_round and tk_apply_round
+ * only validate their handles and return TK_OK at once; the rounding is queued to a worker
+ * thread of the context that runs the queued roundings in order on a private stream, ordered
+ * after everything enqueued so far on the context stream, and the context stream waits for it
+ * (a device-side wait: later work on that stream runs after the rounding, without a host
+ * synchronisation).  The caller's tk_tt structs (and the optional host outputs) are read and
+ * written by the worker: they must stay valid, and their rank fields are undefined, until
+ * tk_sync_ranks returns.  Every other entry point first waits for the queued roundings.  Errors
+ * of a queued rounding are returned by tk_sync_ranks (or the next call).  Returns 1 if async
+ * mode is on, 0 if the driver has no stream memory operations (the context stays synchronous
+ * and correct), or a negative error.  on == 0 drains the queue and returns to synchronous mode.
+ * tk_sync_ranks: block until every queued rounding has finished and published its ranks (x may
+ * be NULL; all TTs are published).  A no-op in synchronous mode. */
+int tk_ctx_set_async(tk_ctx* ctx, int on);
+int tk_sync_ranks(tk_ctx* ctx, tk_tt* x);
+/* Upper bound (bytes) of the library scratch of one tk_round on ranks (R1, R2), or one
+ * tk_apply_round whose grown ranks are (R1, R2), with these mode sizes; the caller-owned cores
+ * are not included.  tk_ctx_reserve pre-reserves that much of the stream-ordered pool
+ * (synchronous); tk_ctx_scratch_high_water reports the measured peak (reset != 0 restarts it). */
+size_t tk_round_workspace_bytes(int64_t n_x, int64_t n_xi, int64_t n_t, int64_t R1, int64_t R2);
+int tk_ctx_reserve(tk_ctx* ctx, size_t bytes);
+int64_t tk_ctx_scratch_high_water(tk_ctx* ctx, int reset);
 
 /* Operator descriptor  A = sum_{k<T} T_k (x) G_k (x) K_k.
  *   K_k : n_x x n_x CSR, HOST arrays: rowptr[n_x+1] (int32), col[nnz_k] (int32, 0-based),
@@ -159,7 +185,8 @@ int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y);
  * sigma1_out / sigma2_out (nullable HOST arrays of length >= x->r1 and >= x->r2 on entry)
  * receive the singular values of the two bonds (descending; entries past the numerical
  * dimension are 0); discarded_out (nullable HOST, 2 doubles) the discarded tail norms;
- * norm_out (nullable HOST) ||x||_F of the input.  BLOCKS the host (reads the chosen ranks).
+ * norm_out (nullable HOST) ||x||_F of the input.  Blocks the host to read the chosen ranks,
+ * except in async mode (tk_ctx_set_async).
  */
 int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
              double* sigma2_out, double* discarded_out, double* norm_out);
@@ -168,7 +195,8 @@ int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out
  * diagonal middle core of A x is never written densely — its T diagonal blocks G_k x_2 U2 stay
  * in scratch and the right-to-left step U2 x_3 L3 runs block by block (T-fold fewer flops).
  * Same contract, outputs and results as the two calls in sequence; y needs cap1 >= T*x.r1,
- * cap2 >= T*x.r2 and holds the rounded TT on return.  BLOCKS the host. */
+ * cap2 >= T*x.r2 and holds the rounded TT on return (in async mode: after tk_sync_ranks).
+ * Blocks the host except in async mode. */
 int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
                    int64_t rmax, double* sigma1_out, double* sigma2_out, double* discarded_out,
                    double* norm_out);

@@ -6,5 +6,5 @@ thin Python binding; it never imports the CPU oracle and has no CPU fallback.
 """
 from .ttk import (TK_EARG, TK_ECAP, TK_ECUDA, TK_ENUMERIC, TK_ESHAPE, TK_OK, TT,  # noqa: F401
                   BlockTridiag, Context, Convection, MeanLSC, Operator, RoundInfo, TkError,
-                  default_context, gmres_cycle, gmres_solve, lib, picard, tt_apply_op, tt_apply_round,
+                  default_context, gmres_cycle, gmres_solve, lib, picard, round_workspace_bytes, tt_apply_op, tt_apply_round,
                   tt_axpby, tt_dot, tt_norm, tt_round)

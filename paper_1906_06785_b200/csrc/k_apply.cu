@@ -491,3 +491,8 @@ int tk_launch_time_apply(tk_ctx* ctx, const tk_op* op, int r2, const double* U3,
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
+
+// Module anchor: async.cu loads every kernel of this translation unit through it (lazy module
+// loading must not happen while a context stream is gated, see tk_ctx_set_async).
+__global__ void tk_anchor_k_apply_k() {}
+const void* tk_anchor_k_apply() { return (const void*)tk_anchor_k_apply_k; }

@@ -751,3 +751,8 @@ int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
+
+// Module anchor: async.cu loads every kernel of this translation unit through it (lazy module
+// loading must not happen while a context stream is gated, see tk_ctx_set_async).
+__global__ void tk_anchor_k_chol_k() {}
+const void* tk_anchor_k_chol() { return (const void*)tk_anchor_k_chol_k; }

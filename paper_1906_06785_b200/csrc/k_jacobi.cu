@@ -693,3 +693,8 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   }
   return TK_OK;
 }
+
+// Module anchor: async.cu loads every kernel of this translation unit through it (lazy module
+// loading must not happen while a context stream is gated, see tk_ctx_set_async).
+__global__ void tk_anchor_k_jacobi_k() {}
+const void* tk_anchor_k_jacobi() { return (const void*)tk_anchor_k_jacobi_k; }

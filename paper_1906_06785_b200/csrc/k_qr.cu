@@ -989,3 +989,8 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   }
   return TK_OK;
 }
+
+// Module anchor: async.cu loads every kernel of this translation unit through it (lazy module
+// loading must not happen while a context stream is gated, see tk_ctx_set_async).
+__global__ void tk_anchor_k_qr_k() {}
+const void* tk_anchor_k_qr() { return (const void*)tk_anchor_k_qr_k; }

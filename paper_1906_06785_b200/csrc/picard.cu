@@ -23,7 +23,7 @@ int system_operator(tk_ctx* ctx, const tk_op* stokes, const tk_conv* conv, const
                     double eps_conv, OpPtr& L) {
   OwnedTT u;
   TK_TRY(clone_tt(ctx, z, u));
-  TK_TRY(tk_round(ctx, &u.t, eps_conv, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_round_now(ctx, &u.t, eps_conv, 0, nullptr, nullptr, nullptr, nullptr));
   tk_op* N = nullptr;
   TK_TRY(tk_op_convection(ctx, conv, &u.t, &N));
   OpPtr Np(N);
@@ -43,7 +43,7 @@ int residual(tk_ctx* ctx, const tk_op* L, const tk_tt* f, const tk_tt* z, double
   r = std::make_unique<OwnedTT>();
   TK_TRY(r->make(ctx, z->n_x, z->n_xi, z->n_t, f->r1 + lz.t.r1, f->r2 + lz.t.r2));
   TK_TRY(tk_axpby_host(ctx, 1.0, f, -1.0, &lz.t, &r->t));
-  TK_TRY(tk_round(ctx, &r->t, eps, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_round_now(ctx, &r->t, eps, 0, nullptr, nullptr, nullptr, nullptr));
   DevBuf d;
   TK_TRY(d.get(ctx, 1));
   TK_TRY(tk_norm(ctx, &r->t, d.p));
@@ -63,6 +63,7 @@ extern "C" int tk_picard(tk_ctx* ctx, const tk_op* stokes, const tk_conv* conv, 
                          double eps_gmres, double eps_conv, int restart, int max_cycles,
                          tk_tt* z_out, double* residuals_out, int* iterations,
                          int64_t* ranks_out) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !stokes || !conv || !f || !z_out || !residuals_out || !iterations || maxit < 0 ||
       restart < 1 || max_cycles < 1 || !(tol_picard >= 0.0) || !(tol_gmres >= 0.0) ||
       !(eps_gmres >= 0.0))
@@ -115,7 +116,7 @@ extern "C" int tk_picard(tk_ctx* ctx, const tk_op* stokes, const tk_conv* conv, 
       auto z2 = std::make_unique<OwnedTT>();
       TK_TRY(z2->make(ctx, n_x, n_xi, n_t, z->t.r1 + dz->t.r1, z->t.r2 + dz->t.r2));
       TK_TRY(tk_axpby_host(ctx, 1.0, &z->t, 1.0, &dz->t, &z2->t));
-      TK_TRY(tk_round(ctx, &z2->t, eps_gmres, 0, nullptr, nullptr, nullptr, nullptr));
+      TK_TRY(tk_round_now(ctx, &z2->t, eps_gmres, 0, nullptr, nullptr, nullptr, nullptr));
       z = std::move(z2);
     }
     TK_TRY(system_operator(ctx, stokes, conv, &z->t, eps_conv, L));  // line 6

@@ -143,6 +143,7 @@ int tk_side_join(tk_ctx* ctx) {
 
 extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
   if (!ctx) return TK_OK;
+  tk_async_destroy(ctx);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
@@ -188,6 +189,7 @@ void tk_prof_end(tk_ctx* ctx, int id) {
 }
 
 extern "C" int tk_ctx_profile(tk_ctx* ctx, int enable) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx) return TK_EARG;
   ctx->prof = enable != 0;
   ctx->prof_level = enable == 2 ? 1 : 2;  // enable == 2: heavy launches only
@@ -200,6 +202,7 @@ extern "C" int tk_ctx_profile(tk_ctx* ctx, int enable) {
 }
 
 extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx) return TK_EARG;
   TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   std::string out;
@@ -222,6 +225,47 @@ extern "C" int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len) {
     buf[n] = 0;
   }
   return (int)ctx->recs.size();
+}
+
+// Upper bound of the library scratch (stream-ordered pool) of one tk_round on ranks (R1, R2), or
+// of one tk_apply_round whose grown ranks are (R1, R2): every temporary of round_impl,
+// orth_rows, the bond SVDs and the fused apply counted as if live at once (they are not), in
+// doubles, plus 1 MiB for small buffers.  tests/test_gpu_parity.py checks it against the
+// measured high-water mark.
+extern "C" size_t tk_round_workspace_bytes(int64_t n_x, int64_t n_xi, int64_t n_t, int64_t R1,
+                                           int64_t R2) {
+  if (n_x < 1 || n_xi < 1 || n_t < 1 || R1 < 1 || R2 < 1) return 0;
+  const double k3 = (double)std::min(n_t, R2), N2 = (double)n_xi * k3;
+  const double k2 = std::min((double)R1, N2), r1 = R1, r2 = R2, nx = n_x, nt = n_t;
+  const double time_core = 12 * r2 * r2 + 4 * nt * r2 + 2 * nt * nt;
+  const double mid = 3 * r1 * N2 + 12 * r1 * r1 + 4 * N2 * r1;
+  const double bond1 = nx * k2 + r1 * r1 + 3 * r1 * k2 + 14 * k2 * k2 + 2 * k2 * N2;
+  const double bond2 = 3 * k2 * n_xi * k3 + 14 * k3 * k3 + 2 * k2 * k3;
+  const double fused = 2 * r1 * n_xi * r2 + r1 * r1;
+  return (size_t)(8.0 * (time_core + mid + bond1 + bond2 + fused)) + ((size_t)1 << 20);
+}
+
+// Reserve `bytes` of the stream-ordered pool for the context's scratch (the pool keeps freed
+// memory, so later calls up to that size map nothing new; cf. pool_settle).  Synchronous.
+extern "C" int tk_ctx_reserve(tk_ctx* ctx, size_t bytes) {
+  TK_ASYNC_GUARD(ctx);
+  if (!ctx) return TK_EARG;
+  if (bytes <= ctx->reserved_for) return TK_OK;
+  void* p = nullptr;
+  TK_CUDA_TRY(ctx, cudaMallocAsync(&p, bytes, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaFreeAsync(p, ctx->stream));
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->reserved_for = bytes;
+  return TK_OK;
+}
+
+// High-water mark of the library scratch since creation or the last reset (bytes).
+extern "C" int64_t tk_ctx_scratch_high_water(tk_ctx* ctx, int reset) {
+  if (!ctx) return 0;
+  if (ctx->async) tk_async_drain(ctx);
+  const int64_t h = (int64_t)ctx->high_bytes;
+  if (reset) ctx->high_bytes = ctx->live_bytes;
+  return h;
 }
 
 extern "C" const char* tk_last_error(const tk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
@@ -473,6 +517,7 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
                             const int32_t* const* K_col, const double* const* K_val,
                             const double* const* G, const int* T_kl, const int* T_ku,
                             const double* const* T_band) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !out) return TK_EARG;
   if (T < 1 || n_x < 1 || n_xi < 1 || n_t < 1) {
     ctx->err = "tk_op_create: T, n_x, n_xi, n_t must be >= 1";
@@ -585,6 +630,7 @@ extern "C" int tk_op_create(tk_ctx* ctx, tk_op** out, int T, int64_t n_x, int64_
 }
 
 extern "C" int tk_op_destroy(tk_op* op) {
+  { tk_ctx* _gc = op ? op->ctx : nullptr; TK_ASYNC_GUARD(_gc); }
   if (!op) return TK_OK;
   cudaFree(op->rowptr);
   cudaFree(op->col);
@@ -604,6 +650,7 @@ extern "C" int tk_op_destroy(tk_op* op) {
 }
 extern "C" int tk_op_terms(const tk_op* op) { return op ? op->T : 0; }
 extern "C" int tk_op_set_spmm_kernel(tk_op* op, int kernel) {
+  { tk_ctx* _gc = op ? op->ctx : nullptr; TK_ASYNC_GUARD(_gc); }
   if (!op || kernel < 0 || kernel > 1) return TK_EARG;
   if (kernel == 1 && !op->rowptr) return TK_EARG;  // (no per-term CSR: merged only)
   if (kernel == 0 && op->chunks.empty()) return 0;
@@ -611,6 +658,7 @@ extern "C" int tk_op_set_spmm_kernel(tk_op* op, int kernel) {
   return op->chunks.empty() ? 0 : 1 - (int)op->spmm_perterm;
 }
 extern "C" int tk_op_group_space(tk_op* op, int enable) {
+  { tk_ctx* _gc = op ? op->ctx : nullptr; TK_ASYNC_GUARD(_gc); }
   if (!op) return TK_EARG;
   op->group_space = enable != 0 && op->n_groups < op->T && !op->gchunks.empty();
   return op->n_groups;
@@ -664,6 +712,7 @@ static int apply_space_time(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt*
 }
 
 extern "C" int tk_apply_op(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !op) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_apply_op(x)"));
   if (!y || !y->U1 || !y->U2 || !y->U3) {
@@ -1051,8 +1100,8 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
                       const double* y2blk = nullptr, int64_t rb1 = 0, int64_t rb2 = 0,
                       const double* gy_pre = nullptr, const tk_op* gop = nullptr);
 
-extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
-                        double* sigma2_out, double* discarded_out, double* norm_out) {
+int tk_round_now(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                 double* sigma2_out, double* discarded_out, double* norm_out) {
   if (!ctx) return TK_EARG;
   int st;
   {
@@ -1063,9 +1112,46 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
   return st;
 }
 
+extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                        double* sigma2_out, double* discarded_out, double* norm_out) {
+  if (!ctx || !x) return TK_EARG;
+  if (ctx->async && !tk_async_on_worker(ctx))  // queued: *x is read when the job runs
+    return tk_async_submit(ctx, [=]() {
+      tk_tt xc = *x;
+      const int st = tk_round_now(ctx, &xc, tol, rmax, sigma1_out, sigma2_out, discarded_out,
+                                  norm_out);
+      if (st == TK_OK) {  // publish the ranks into the caller's struct
+        x->r1 = xc.r1;
+        x->r2 = xc.r2;
+      }
+      return st;
+    });
+  return tk_round_now(ctx, x, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out);
+}
+
 extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
                               int64_t rmax, double* sigma1_out, double* sigma2_out,
                               double* discarded_out, double* norm_out) {
+  if (!ctx || !op || !x || !y) return TK_EARG;
+  if (ctx->async && !tk_async_on_worker(ctx))
+    return tk_async_submit(ctx, [=]() {
+      const tk_tt xc = *x;
+      tk_tt yc = *y;
+      const int st = tk_apply_round_now(ctx, op, &xc, &yc, tol, rmax, sigma1_out, sigma2_out,
+                                        discarded_out, norm_out);
+      if (st == TK_OK) {
+        y->r1 = yc.r1;
+        y->r2 = yc.r2;
+      }
+      return st;
+    });
+  return tk_apply_round_now(ctx, op, x, y, tol, rmax, sigma1_out, sigma2_out, discarded_out,
+                            norm_out);
+}
+
+int tk_apply_round_now(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
+                       int64_t rmax, double* sigma1_out, double* sigma2_out,
+                       double* discarded_out, double* norm_out) {
   if (!ctx || !op) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_apply_round(x)"));
   if (!y || !y->U1 || !y->U2 || !y->U3) {
@@ -1310,6 +1396,7 @@ static int dot_impl(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out, in
 }
 
 extern "C" int tk_dot(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out_dev) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !out_dev) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_dot(x)"));
   TK_TRY(check_tt(ctx, y, "tk_dot(y)"));
@@ -1318,6 +1405,7 @@ extern "C" int tk_dot(tk_ctx* ctx, const tk_tt* x, const tk_tt* y, double* out_d
 }
 
 extern "C" int tk_norm(tk_ctx* ctx, const tk_tt* x, double* out_dev) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !out_dev) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_norm"));
   return dot_impl(ctx, x, x, out_dev, 1);
@@ -1326,6 +1414,7 @@ extern "C" int tk_norm(tk_ctx* ctx, const tk_tt* x, double* out_dev) {
 // ============================================================================ axpby / scale
 extern "C" int tk_axpby(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const double* b_dev,
                         const tk_tt* y, tk_tt* z) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !a_dev || !b_dev) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_axpby(x)"));
   TK_TRY(check_tt(ctx, y, "tk_axpby(y)"));
@@ -1358,6 +1447,7 @@ extern "C" int tk_axpby(tk_ctx* ctx, const double* a_dev, const tk_tt* x, const 
 
 extern "C" int tk_axpby_host(tk_ctx* ctx, double a, const tk_tt* x, double b, const tk_tt* y,
                              tk_tt* z) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx) return TK_EARG;
   DevBuf s;
   TK_TRY(s.get(ctx, 2));
@@ -1367,6 +1457,7 @@ extern "C" int tk_axpby_host(tk_ctx* ctx, double a, const tk_tt* x, double b, co
 }
 
 extern "C" int tk_scale(tk_ctx* ctx, tk_tt* x, const double* s_dev, int invert) {
+  TK_ASYNC_GUARD(ctx);
   if (!ctx || !s_dev) return TK_EARG;
   TK_TRY(check_tt(ctx, x, "tk_scale"));
   return tk_scale_rows(ctx, x->U3, x->r2 * x->n_t, s_dev, invert);
@@ -1376,7 +1467,7 @@ extern "C" int tk_scale(tk_ctx* ctx, tk_tt* x, const double* s_dev, int invert) 
 int tk_apply_round_owned(tk_ctx* ctx, const tk_op* op, const tk_tt* x, OwnedPtr& y, double tol) {
   y = std::make_unique<OwnedTT>();
   TK_TRY(y->make(ctx, x->n_x, x->n_xi, x->n_t, op->T * x->r1, op->T * x->r2));
-  return tk_apply_round(ctx, op, x, &y->t, tol, 0, nullptr, nullptr, nullptr, nullptr);
+  return tk_apply_round_now(ctx, op, x, &y->t, tol, 0, nullptr, nullptr, nullptr, nullptr);
 }
 
 // One cycle (tk_gmres_cycle), plus what the restarted solver needs: stop once the Givens
@@ -1409,7 +1500,7 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
   std::vector<OwnedPtr> V, Vhat;
   V.emplace_back(new OwnedTT());
   TK_TRY(clone_tt(ctx, b, *V[0]));
-  TK_TRY(tk_round(ctx, &V[0]->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_round_now(ctx, &V[0]->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
   TK_TRY(tk_norm(ctx, &V[0]->t, d_beta));
   double beta;
   TK_TRY(sync_read(ctx, &beta, d_beta, sizeof(double)));
@@ -1436,7 +1527,7 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
       auto z = std::make_unique<OwnedTT>();
       TK_TRY(z->make(ctx, n_x, n_xi, n_t, x->t.r1 + V[i]->t.r1, x->t.r2 + V[i]->t.r2));
       TK_TRY(tk_axpby(ctx, d_one, &x->t, d_negh + i, &V[i]->t, &z->t));
-      TK_TRY(tk_round(ctx, &z->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+      TK_TRY(tk_round_now(ctx, &z->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
       x = std::move(z);
     }
     TK_TRY(tk_norm(ctx, &x->t, d_hn));
@@ -1497,7 +1588,7 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
       auto z2 = std::make_unique<OwnedTT>();
       TK_TRY(z2->make(ctx, n_x, n_xi, n_t, z->t.r1 + B[i]->t.r1, z->t.r2 + B[i]->t.r2));
       TK_TRY(tk_axpby_host(ctx, 1.0, &z->t, y[i], &B[i]->t, &z2->t));
-      TK_TRY(tk_round(ctx, &z2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+      TK_TRY(tk_round_now(ctx, &z2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
       z = std::move(z2);
     }
     if (!explicit_out) {
@@ -1510,7 +1601,7 @@ static int gmres_cycle_impl(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int st
     auto r = std::make_unique<OwnedTT>();
     TK_TRY(r->make(ctx, n_x, n_xi, n_t, b->r1 + az->t.r1, b->r2 + az->t.r2));
     TK_TRY(tk_axpby_host(ctx, 1.0, b, -1.0, &az->t, &r->t));
-    TK_TRY(tk_round(ctx, &r->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_round_now(ctx, &r->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
     TK_TRY(tk_norm(ctx, &r->t, d_hn));
     TK_TRY(sync_read(ctx, explicit_out, d_hn, sizeof(double)));
     if (z_out) *z_out = std::move(z);
@@ -1531,6 +1622,7 @@ static int gmres_cycle_entry(tk_ctx* ctx, const tk_op* op, const tk_prec* P, con
 extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int steps,
                               double tol, double* history_out, int* steps_done,
                               double* explicit_out, double* step_ms_out) {
+  TK_ASYNC_GUARD(ctx);
   return gmres_cycle_entry(ctx, op, nullptr, b, steps, tol, history_out, steps_done,
                            explicit_out, step_ms_out);
 }
@@ -1538,6 +1630,7 @@ extern "C" int tk_gmres_cycle(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
 extern "C" int tk_gmres_cycle_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, const tk_tt* b,
                                 int steps, double tol, double* history_out, int* steps_done,
                                 double* explicit_out, double* step_ms_out) {
+  TK_ASYNC_GUARD(ctx);
   if (!P) return TK_EARG;
   return gmres_cycle_entry(ctx, op, P, b, steps, tol, history_out, steps_done, explicit_out,
                            step_ms_out);
@@ -1560,7 +1653,7 @@ int tk_gmres_solve_core(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restar
   // s_0 = T(b)  (z_0 = 0)
   auto s_ = std::make_unique<OwnedTT>();
   TK_TRY(clone_tt(ctx, b, *s_));
-  TK_TRY(tk_round(ctx, &s_->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+  TK_TRY(tk_round_now(ctx, &s_->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
   TK_TRY(tk_norm(ctx, &s_->t, sc.p));
   TK_TRY(sync_read(ctx, &e, sc.p, sizeof(double)));
   explicit_out.assign(1, e);
@@ -1584,7 +1677,7 @@ int tk_gmres_solve_core(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restar
       TK_TRY(tk_axpby_host(ctx, 1.0, &zt->t, 1.0, &dz->t, &z2->t));
       zt = std::move(z2);
     }
-    TK_TRY(tk_round(ctx, &zt->t, eps_soln, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_round_now(ctx, &zt->t, eps_soln, 0, nullptr, nullptr, nullptr, nullptr));
     // s = T(b - L z)   (line 14)
     auto az = std::make_unique<OwnedTT>();
     TK_TRY(az->make(ctx, n_x, n_xi, n_t, T * zt->t.r1, T * zt->t.r2));
@@ -1592,7 +1685,7 @@ int tk_gmres_solve_core(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int restar
     auto s2 = std::make_unique<OwnedTT>();
     TK_TRY(s2->make(ctx, n_x, n_xi, n_t, b->r1 + az->t.r1, b->r2 + az->t.r2));
     TK_TRY(tk_axpby_host(ctx, 1.0, b, -1.0, &az->t, &s2->t));
-    TK_TRY(tk_round(ctx, &s2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
+    TK_TRY(tk_round_now(ctx, &s2->t, tol, 0, nullptr, nullptr, nullptr, nullptr));
     s_ = std::move(s2);
     TK_TRY(tk_norm(ctx, &s_->t, sc.p));
     TK_TRY(sync_read(ctx, &e, sc.p, sizeof(double)));
@@ -1650,6 +1743,7 @@ extern "C" int tk_gmres_solve(tk_ctx* ctx, const tk_op* op, const tk_tt* b, int 
                               int max_cycles, double tol, double tol_gmres, double eps_soln,
                               tk_tt* z, double* explicit_out, double* ls_out, int* cycles_done,
                               int* steps_out) {
+  TK_ASYNC_GUARD(ctx);
   return gmres_solve_entry(ctx, op, nullptr, b, restart, max_cycles, tol, tol_gmres, eps_soln,
                            z, explicit_out, ls_out, cycles_done, steps_out);
 }
@@ -1658,6 +1752,7 @@ extern "C" int tk_gmres_solve_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, 
                                 int restart, int max_cycles, double tol, double tol_gmres,
                                 double eps_soln, tk_tt* z, double* explicit_out, double* ls_out,
                                 int* cycles_done, int* steps_out) {
+  TK_ASYNC_GUARD(ctx);
   if (!P) return TK_EARG;
   return gmres_solve_entry(ctx, op, P, b, restart, max_cycles, tol, tol_gmres, eps_soln, z,
                            explicit_out, ls_out, cycles_done, steps_out);

@@ -19,6 +19,8 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 
+struct tk_async;
+
 struct tk_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
@@ -52,7 +54,31 @@ struct tk_ctx {
   // SMs to it before the side stream's big kernels (which cannot be preempted)
   cudaStream_t crit = nullptr;
   cudaEvent_t crit_ev[2] = {nullptr, nullptr};
+  // async mode (tk_ctx_set_async, async.cu): the worker that runs queued roundings
+  tk_async* async = nullptr;
 };
+// Async mode (async.cu).  drain: wait until the queued jobs ran (returns their first error);
+// submit: queue body() for the worker, ordered after (and gating) the caller's stream.
+int tk_async_drain(tk_ctx* ctx);
+int tk_async_submit(tk_ctx* ctx, std::function<int()> body);
+bool tk_async_on_worker(const tk_ctx* ctx);
+void tk_async_destroy(tk_ctx* ctx);
+// First statement of every entry point that reads ranks or enqueues work: wait for the queued
+// asynchronous roundings (a no-op on the worker thread and in synchronous mode).
+#define TK_ASYNC_GUARD(c)                         \
+  do {                                             \
+    if ((c) && (c)->async) {                       \
+      int _g = tk_async_drain(c);                  \
+      if (_g != TK_OK) return _g;                  \
+    }                                              \
+  } while (0)
+// The synchronous rounding entry points (what tk_round / tk_apply_round run, on the calling
+// thread or on the async worker).  Library-internal callers use these.
+int tk_round_now(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
+                 double* sigma2_out, double* discarded_out, double* norm_out);
+int tk_apply_round_now(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_tt* y, double tol,
+                       int64_t rmax, double* sigma1_out, double* sigma2_out,
+                       double* discarded_out, double* norm_out);
 // Scoped move of a whole library call onto ctx->crit (fork from the caller's stream on entry,
 // join back on exit).
 struct CritScope {

@@ -27,7 +27,9 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_conv_create", "tk_conv_destroy", "tk_op_convection",
             "tk_bt_create", "tk_bt_create_gram", "tk_bt_destroy", "tk_bt_solve",
             "tk_prec_create_lsc", "tk_prec_destroy", "tk_prec_apply", "tk_prec_operator",
-            "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard"]
+            "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard",
+            "tk_ctx_set_async", "tk_sync_ranks", "tk_round_workspace_bytes", "tk_ctx_reserve",
+            "tk_ctx_scratch_high_water"]
 
 
 class TkError(RuntimeError):
@@ -102,11 +104,19 @@ def lib():
                                    ctypes.POINTER(I)]
     L.tk_picard.argtypes = [P, P, P, P, TTP, D, I, D, D, D, I, I, TTP, DP, ctypes.POINTER(I),
                             ctypes.POINTER(I64)]
+    L.tk_ctx_set_async.argtypes = [P, I]
+    L.tk_sync_ranks.argtypes = [P, TTP]
+    L.tk_round_workspace_bytes.argtypes = [I64, I64, I64, I64, I64]
+    L.tk_round_workspace_bytes.restype = ctypes.c_size_t
+    L.tk_ctx_reserve.argtypes = [P, ctypes.c_size_t]
+    L.tk_ctx_scratch_high_water.argtypes = [P, I]
+    L.tk_ctx_scratch_high_water.restype = I64
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
         if name not in ("tk_version", "tk_last_error", "tk_ctx_launch_count",
-                        "tk_prec_operator"):
+                        "tk_prec_operator", "tk_round_workspace_bytes",
+                        "tk_ctx_scratch_high_water"):
             getattr(L, name).restype = I
     _lib = L
     return L
@@ -124,9 +134,37 @@ class Context:
         _require_cuda()
         self.stream = stream or torch.cuda.current_stream()
         self._h = ctypes.c_void_p()
+        self.async_on = False
+        self._pending = []  # (TT, tk_tt struct) of queued async roundings
         rc = lib().tk_ctx_create(ctypes.byref(self._h), ctypes.c_void_p(self.stream.cuda_stream))
         if rc != TK_OK:
             raise TkError(rc, "tk_ctx_create failed")
+
+    def set_async(self, on: bool = True) -> bool:
+        """tk_ctx_set_async: queue tk_round / tk_apply_round to the context's worker; the TTs'
+        ranks are valid after sync().  Returns whether async mode is on."""
+        if not on:
+            self.sync()
+        rc = lib().tk_ctx_set_async(self._h, 1 if on else 0)
+        if rc < 0:
+            raise TkError(rc, lib().tk_last_error(self._h).decode())
+        self.async_on = bool(on) and rc == 1
+        return self.async_on
+
+    def sync(self):
+        """tk_sync_ranks: wait for the queued roundings and publish their ranks."""
+        pend, self._pending = self._pending, []
+        rc = lib().tk_sync_ranks(self._h, None) if self._h else TK_OK
+        for t, st in pend:
+            if t is not None:
+                t._update(st)
+        self.check(rc)
+
+    def reserve(self, nbytes: int):
+        self.check(lib().tk_ctx_reserve(self._h, int(nbytes)))
+
+    def scratch_high_water(self, reset: bool = False) -> int:
+        return int(lib().tk_ctx_scratch_high_water(self._h, 1 if reset else 0))
 
     def check(self, rc: int):
         if rc != TK_OK:
@@ -159,7 +197,8 @@ class TT:
 
     def __init__(self, n_x, n_xi, n_t, r1, r2, cap1=None, cap2=None, device="cuda"):
         self.n_x, self.n_xi, self.n_t = int(n_x), int(n_xi), int(n_t)
-        self.r1, self.r2 = int(r1), int(r2)
+        self._pend = None  # (Context, tk_tt) while an async rounding of this TT is queued
+        self._r1, self._r2 = int(r1), int(r2)
         self.cap1 = int(cap1 if cap1 is not None else r1)
         self.cap2 = int(cap2 if cap2 is not None else r2)
         dt = torch.float64
@@ -178,6 +217,19 @@ class TT:
                                     dtype=torch.float64)
             buf[: src_t.numel()].copy_(src_t.reshape(-1), non_blocking=non_blocking)
         return t
+
+    # ranks: reading them waits for a queued asynchronous rounding of this TT (tk_sync_ranks)
+    @property
+    def r1(self):
+        if self._pend is not None:
+            self._pend[0].sync()
+        return self._r1
+
+    @property
+    def r2(self):
+        if self._pend is not None:
+            self._pend[0].sync()
+        return self._r2
 
     @property
     def U1(self):
@@ -200,11 +252,18 @@ class TT:
                 self.U3.cpu().numpy().copy())
 
     def struct(self) -> tk_tt:
-        return tk_tt(self.n_x, self.n_xi, self.n_t, self.r1, self.r2, self.cap1, self.cap2,
+        if self._pend is not None:  # queued: later queued calls share the struct the worker
+            return self._pend[1]    # publishes into
+        return tk_tt(self.n_x, self.n_xi, self.n_t, self._r1, self._r2, self.cap1, self.cap2,
                      self.b1.data_ptr(), self.b2.data_ptr(), self.b3.data_ptr())
 
     def _update(self, s: tk_tt):
-        self.r1, self.r2 = int(s.r1), int(s.r2)
+        self._pend = None
+        self._r1, self._r2 = int(s.r1), int(s.r2)
+
+    def _queue(self, ctx, s: tk_tt):
+        self._pend = (ctx, s)
+        ctx._pending.append((self, s))
 
 
 class Operator:
@@ -351,6 +410,13 @@ def tt_round(x: TT, tol: float, rmax: int = 0, ctx: Context | None = None,
     ctx = ctx or default_context()
     s = x.struct()
     D = ctypes.c_double
+    if ctx.async_on:
+        if want_info:
+            raise ValueError("want_info needs a synchronous context")
+        ctx.check(lib().tk_round(ctx._h, ctypes.byref(s), float(tol), int(rmax), None, None, None,
+                                 None))
+        x._queue(ctx, s)
+        return x
     if want_info:
         s1 = (D * max(x.r1, 1))()
         s2 = (D * max(x.r2, 1))()
@@ -377,6 +443,14 @@ def tt_apply_round(op: "Operator", x: TT, tol: float, rmax: int = 0, out: TT | N
     y = out if out is not None else TT(x.n_x, x.n_xi, x.n_t, T * x.r1, T * x.r2)
     xs, ys = x.struct(), y.struct()
     D = ctypes.c_double
+    if ctx.async_on:
+        if want_info:
+            raise ValueError("want_info needs a synchronous context")
+        ctx.check(lib().tk_apply_round(ctx._h, op._h, ctypes.byref(xs), ctypes.byref(ys),
+                                       float(tol), int(rmax), None, None, None, None))
+        y._queue(ctx, ys)
+        ctx._pending.append((None, xs))  # keeps the input struct alive until sync
+        return y
     if want_info:
         s1 = (D * max(T * x.r1, 1))()
         s2 = (D * max(T * x.r2, 1))()
@@ -606,3 +680,8 @@ def picard(stokes: Operator, conv: Convection, f: TT, tol_picard: float = 1e-4, 
     n = it.value
     return dict(z=z, residuals=np.array(res[: n + 1]), iterations=n,
                 ranks=[(rk[2 * i], rk[2 * i + 1]) for i in range(n + 1)])
+
+
+def round_workspace_bytes(n_x, n_xi, n_t, R1, R2) -> int:
+    """tk_round_workspace_bytes: scratch bound of one rounding on grown ranks (R1, R2)."""
+    return int(lib().tk_round_workspace_bytes(int(n_x), int(n_xi), int(n_t), int(R1), int(R2)))
