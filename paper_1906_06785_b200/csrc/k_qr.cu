@@ -643,6 +643,142 @@ __global__ void __launch_bounds__(32 * QB)
   stamp(4);
 }
 
+// Tall-panel variant of qr_panel_reg_k for 32 * MAXR < m <= BIG_M (the pass-1 QR of the
+// c5 / c6 Grams, k ~ 1300-2300): warp j holds rows [0, 32 MAXR) of column j in registers and the
+// rows beyond in a per-column shared-memory overflow region, so the panel is factored by one
+// CTA without global-memory round trips (the former fallback, qr_panel_k<false> working in
+// global memory, took ~460 us per 16-column panel at m = 2240).  Same contract as
+// qr_panel_k<false>: the panel (m x jb, ld ldg, already updated by the previous reflectors)
+// in, V (m x QB, unit lower trapezoidal, zero padded) and T (QB x QB) out; VT / VT^T are formed
+// by the caller.  Dynamic smem: QB x (BIG_M - 32 MAXR) doubles.
+constexpr int BIG_M = 2256;
+template <int MAXR>
+__global__ void __launch_bounds__(32 * QB)
+    qr_panel_big_k(int m, int jb, const double* __restrict__ Pg, int64_t ldg,
+                   double* __restrict__ Vout, double* __restrict__ Tout) {
+  constexpr int MR = 32 * MAXR;
+  constexpr int OVL = BIG_M - MR;  // overflow rows per column
+  __shared__ double vbuf[2][BIG_M];
+  __shared__ double s_tau[QB], s_z[QB][QB];
+  __shared__ double Ts[QB][QB + 1];
+  extern __shared__ double ov_all[];
+  const int tid = threadIdx.x, lane = tid & 31, j = tid >> 5;
+  double* ov = ov_all + (size_t)j * OVL;  // rows MR.. of column j
+  double c[MAXR];
+#pragma unroll
+  for (int k = 0; k < MAXR; k++) {
+    const int i = lane + 32 * k;
+    c[k] = (i < m && j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
+  }
+  for (int i = MR + lane; i < m; i += 32) ov[i - MR] = j < jb ? Pg[(int64_t)i * ldg + j] : 0.0;
+  for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
+  __syncthreads();
+  auto reflect = [&](int buf) {
+    const int r0 = j;
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXR; k++) {
+      const int i = lane + 32 * k;
+      if (i > r0 && i < m) sq = fma(c[k], c[k], sq);
+    }
+    for (int i = MR + lane; i < m; i += 32) sq = fma(ov[i - MR], ov[i - MR], sq);
+    sq = warp_sum(sq);
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXR; k++)
+      if (lane + 32 * k == r0) a = c[k];
+    const double alpha = __shfl_sync(0xffffffffu, a, r0 & 31);
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (sq > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, sq));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+#pragma unroll
+    for (int k = 0; k < MAXR; k++) {
+      const int i = lane + 32 * k;
+      double v = 0.0;
+      if (i > r0 && i < m) {
+        c[k] *= scale;
+        v = c[k];
+      } else if (i == r0) {
+        c[k] = 1.0;
+        v = 1.0;
+      } else if (i < r0) {
+        c[k] = 0.0;
+      }
+      vbuf[buf][i] = v;
+    }
+    for (int i = MR + lane; i < m; i += 32) {
+      ov[i - MR] *= scale;
+      vbuf[buf][i] = ov[i - MR];
+    }
+    if (lane == 0) s_tau[j] = tau;
+  };
+  if (j == 0 && jb > 0) reflect(0);
+  __syncthreads();
+  for (int cc = 0; cc < jb; cc++) {
+    const int buf = cc & 1;
+    const double tau = s_tau[cc];
+    const int r0 = cc;
+    if (j > cc && j < jb) {
+      double vr[MAXR];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) {
+        const int i = lane + 32 * k;
+        vr[k] = (i >= r0 && i < m) ? vbuf[buf][i] : 0.0;
+        if (k & 1)
+          w1 = fma(vr[k], c[k], w1);
+        else
+          w0 = fma(vr[k], c[k], w0);
+      }
+      for (int i = MR + lane; i < m; i += 32) w0 = fma(vbuf[buf][i], ov[i - MR], w0);
+      const double w = warp_sum(w0 + w1) * tau;
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) c[k] = fma(-w, vr[k], c[k]);
+      for (int i = MR + lane; i < m; i += 32) ov[i - MR] = fma(-w, vbuf[buf][i], ov[i - MR]);
+      if (j == cc + 1) reflect(buf ^ 1);
+    } else if (j < cc) {
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXR; k++) {
+        const int i = lane + 32 * k;
+        const double v = (i >= r0 && i < m) ? vbuf[buf][i] : 0.0;
+        if (k & 1)
+          z1 = fma(v, c[k], z1);
+        else
+          z0 = fma(v, c[k], z0);
+      }
+      for (int i = MR + lane; i < m; i += 32) z0 = fma(vbuf[buf][i], ov[i - MR], z0);
+      const double z = warp_sum(z0 + z1);
+      if (lane == 0) s_z[cc][j] = z;
+    }
+    __syncthreads();
+  }
+  if (j == 0) {
+    for (int cc = 0; cc < jb; cc++) {
+      if (lane < cc) {
+        double t = 0.0;
+        for (int q = lane; q < cc; q++) t = fma(Ts[lane][q], s_z[cc][q], t);
+        Ts[lane][cc] = -s_tau[cc] * t;
+      }
+      if (lane == 0) Ts[cc][cc] = s_tau[cc];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // V out (warp j writes column j; zero columns beyond jb)
+#pragma unroll
+  for (int k = 0; k < MAXR; k++) {
+    const int i = lane + 32 * k;
+    if (i < m) Vout[(int64_t)i * QB + j] = (j < jb) ? c[k] : 0.0;
+  }
+  for (int i = MR + lane; i < m; i += 32) Vout[(int64_t)i * QB + j] = (j < jb) ? ov[i - MR] : 0.0;
+  for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
+}
+
 // C <- C - X (V^T C) for the m x nc block C (leading dimension ldc) and the m x QB panels V, X
 // (row-major, ld QB): the compact-WY application of one panel's block reflector (X = V T^T for
 // the trailing update, X = V T for the accumulation of Q), fused into one kernel.  CTA = a strip
@@ -922,7 +1058,7 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
       return TK_OK;
     }
     const size_t psmem = (size_t)(m + off) * (QB + 1) * sizeof(double);
-    if (psmem <= 200 * 1024) {
+    if (psmem <= 200 * 1024 && m > BIG_M) {  // (never: the big kernel serves 896 < m <= BIG_M)
       const double* Vq = p > 0 ? Vb.p + (size_t)(p - 1) * n * QB : nullptr;
       const double* VTtq = p > 0 ? VTtb.p + (size_t)(p - 1) * n * QB : nullptr;
       qr_panel_warp_k<<<1, 32 * QB, psmem, s0>>>(
@@ -939,7 +1075,20 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
             Aw.p + (int64_t)(j0 - QB) * n + j0, n);
         TK_LAUNCH_CHECK(ctx);
       }
-      qr_panel_k<false><<<1, QT, 0, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+      if (m <= BIG_M) {
+        constexpr int BMR = 26;  // 832 register rows; the rest in shared memory
+        const size_t osmem = sizeof(double) * (size_t)QB * (BIG_M - 32 * BMR);
+        static bool at = false;
+        if (!at) {
+          cudaFuncSetAttribute(qr_panel_big_k<BMR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)osmem);
+          at = true;
+        }
+        qr_panel_big_k<BMR><<<1, 32 * QB, osmem, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp,
+                                                      Tp);
+      } else {
+        qr_panel_k<false><<<1, QT, 0, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
+      }
       TK_LAUNCH_CHECK(ctx);
       tk_prof_end(ctx, pid);
       TK_TRY(tk_dgemm(ctx, false, false, m, QB, QB, 1.0, Vp, QB, Tp, QB, 0.0, VTp, QB));
