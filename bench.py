@@ -43,6 +43,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--breakdown", action="store_true", help="per-phase times to stderr")
+    p.add_argument("--prec", action="store_true",
+                   help="c5 / c7 / c8: right-precondition GMRES with the mean-based LSC "
+                        "preconditioner (NEXT-3)")
     p.add_argument("--group-space", action="store_true",
                    help="optional exact factor grouping of the space core (SURVEY 8d; reported "
                         "separately, the literal T r growth is the primary line)")
@@ -603,9 +606,16 @@ def run_gmres(args, cfg, op):
     ctx = ttk.default_context()
     gop = op.gpu_op(ctx)
     bg = ttk.TT.from_cores(*b)
+    steps_k = cfg.gmres_steps
+    P = None
+    if args.prec:  # NEXT-3: flexible GMRES with the mean-based LSC preconditioner
+        from synth.operator import mean_blocks
+        F0s, Bd = mean_blocks(cfg)
+        P = ttk.MeanLSC(F0s, Bd, cfg.tau, op.n_xi, op.n_t, tol=cfg.tol, grid=cfg.grid, ctx=ctx)
+        steps_k = 3
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
-        ttk.gmres_cycle(gop, bg, cfg.gmres_steps, cfg.tol)
+        ttk.gmres_cycle(gop, bg, steps_k, cfg.tol, prec=P)
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
@@ -623,7 +633,7 @@ def run_gmres(args, cfg, op):
         for i in range(args.steps):
             flush.fill_(float(i))
             evs[i][0].record(stream)
-            res = ttk.gmres_cycle(gop, bg, cfg.gmres_steps, cfg.tol)
+            res = ttk.gmres_cycle(gop, bg, steps_k, cfg.tol, prec=P)
             evs[i][1].record(stream)
             krylov += res["steps"]
         torch.cuda.synchronize()
@@ -650,14 +660,14 @@ def run_gmres(args, cfg, op):
     e0.record(stream)
     for buf_, src in zip((be.b1, be.b2, be.b3), pinned):
         buf_[: src.numel()].copy_(src.reshape(-1), non_blocking=True)
-    re_ = ttk.gmres_cycle(gop, be, cfg.gmres_steps, cfg.tol)
+    re_ = ttk.gmres_cycle(gop, be, steps_k, cfg.tol, prec=P)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e = {"value": world * 1000.0 * re_["steps"] / e0.elapsed_time(e1), "unit": GMRES_UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * (len(re_["history"]) + 1),
            "steps": 1}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and P is None:
         v, what = oracle_sample_gmres(op.oracle_op(), b, cfg)
         cores = cpu_cores_used()
         cpu = {"value": v, "unit": GMRES_UNIT, "cores": cores, "kind": "oracle",
@@ -679,9 +689,99 @@ def run_gmres(args, cfg, op):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "note": "step = one GMRES cycle (the c5 line; the headline bench line is c4)",
         }
+        if P is not None:
+            line["config"]["workload"] = (f"{cfg.name}: one {steps_k}-step flexible low-rank GMRES "
+                                          "cycle, mean-based LSC preconditioner (NEXT-3)")
+            line["note"] = ("NEXT-3 line (not a BASELINE.json config): each Krylov step applies "
+                            "P^{-1} (two pressure solves, B(F0+C)B^T, an inner GMRES with M)")
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- c7/c8: Picard
+def run_picard(args, cfg):
+    """NEXT-4 line (not a BASELINE.json config): one full inexact Picard solve (Alg. 1) per step
+    on the synthetic stochastic Galerkin Navier-Stokes problem of config c7 / c8."""
+    import torch
+    import paper_1906_06785_b200 as ttk
+    from synth import gpc
+    from synth.operator import (build_operator, convection_stencils, mean_blocks,
+                                picard_forcing)
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    op = build_operator(cfg)
+    H = gpc.h_matrices(cfg.m, cfg.p)
+    D, nv = convection_stencils(cfg.grid)
+    f = picard_forcing(cfg, op.n_xi)
+    kw = dict(tol_picard=1e-3, maxit=12, tol_gmres=1e-1, eps_gmres=cfg.tol, restart=20,
+              max_cycles=5)
+    wl = {"workload": f"{cfg.name}: inexact Picard solve (Alg. 1), stochastic Galerkin NS",
+          "n_x": op.n_x, "n_xi": op.n_xi, "n_t": op.n_t, "grid": cfg.grid, **kw,
+          "prec": "mean-based LSC" if args.prec else "none", "parallelism": "replicas"}
+    if args.impl == "reference":
+        if rank == 0:
+            from oracle.precond import MeanLSC as OLSC
+            from oracle.picard import picard as o_picard
+            prec = None
+            if args.prec:
+                F0s, Bd = mean_blocks(cfg)
+                prec = OLSC(F0s, Bd, cfg.tau, op.n_xi, op.n_t, tol=cfg.tol).apply
+            t0 = time.perf_counter()
+            o_picard(op, H, D, nv, f, prec=prec, **kw)
+            dt = time.perf_counter() - t0
+            v = 1.0 / dt
+            print(json.dumps({"impl": "reference", "metric": "Picard solves/s", "value": v,
+                              "unit": "solves/s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+                              "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                              "dtype": "f64", "data": "synthetic", "config": wl,
+                              "cpu_baseline": {"value": v, "unit": "solves/s",
+                                               "cores": cpu_cores_used(), "kind": "oracle",
+                                               "sample": f"1 full oracle Picard solve ({dt:.1f} s)"},
+                              "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                                      "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    ctx = ttk.default_context()
+    g_op = ttk.Operator.from_kronsum(op, ctx)
+    conv = ttk.Convection(op.n_x, op.n_xi, op.n_t, D, nv, np.array(H), ctx=ctx)
+    P = None
+    if args.prec:
+        F0s, Bd = mean_blocks(cfg)
+        P = ttk.MeanLSC(F0s, Bd, cfg.tau, op.n_xi, op.n_t, tol=cfg.tol, grid=cfg.grid, ctx=ctx)
+    fg = ttk.TT.from_cores(*f)
+    for _ in range(args.warmup):
+        ttk.picard(g_op, conv, fg, prec=P, **kw)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = ttk.picard(g_op, conv, fg, prec=P, **kw)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and cfg.name == "c7":
+        from oracle.picard import picard as o_picard
+        t0 = time.perf_counter()
+        o_picard(op, H, D, nv, f, **kw)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 1.0 / dt, "unit": "solves/s", "cores": cpu_cores_used(), "kind": "oracle",
+               "sample": f"1 full oracle Picard solve without P ({dt:.1f} s)"}
+    fn = float(np.linalg.norm(f[0]) * np.linalg.norm(f[1]) * np.linalg.norm(f[2]))
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Picard solves/s", "value": world * 1000.0 / ms, "unit": "solves/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "picard_iterations": res["iterations"],
+            "residuals_rel": (res["residuals"] / fn).tolist(), "ranks": res["ranks"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": wl, "cpu_baseline": cpu,
+            "gpu_launches": ctx.launches - launches0, "clocks": clk.summary(),
+            "note": "NEXT-4 line, not a BASELINE.json config (the headline bench line is c4)"}),
+            flush=True)
 
 
 class Workload:
@@ -730,6 +830,9 @@ def main():
     from synth.configs import CONFIGS
     from synth.tt import make_input_tt
     cfg = CONFIGS[args.config]
+    if cfg.operator == "picard":
+        run_picard(args, cfg)
+        return
     op = Workload(cfg)
     if cfg.name == "c5":
         run_gmres(args, cfg, op)

@@ -69,3 +69,43 @@ def test_new_entry_points_reject_null_arguments(so):
         [ctypes.c_double] * 3 + [ctypes.c_void_p] * 5
     assert so.tk_gmres_solve(None, None, None, 4, 2, 1e-8, 1e-6, -1.0, None, None, None, None,
                              None) == -3
+
+
+def test_round2_entry_points_reject_null_arguments(so):
+    """NEXT-3 / NEXT-4 / async entry points validate their handles before any CUDA call."""
+    P = ctypes.c_void_p
+    so.tk_sync_ranks.argtypes = [P, P]
+    assert so.tk_sync_ranks(None, None) == -3
+    so.tk_ctx_set_async.argtypes = [P, ctypes.c_int]
+    assert so.tk_ctx_set_async(None, 1) == -3
+    so.tk_prec_apply.argtypes = [P, P, ctypes.c_int, P, P]
+    assert so.tk_prec_apply(None, None, 0, None, None) == -3
+    so.tk_bt_solve.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int, P]
+    assert so.tk_bt_solve(None, None, None, 0, 1, None) == -3
+    so.tk_picard.argtypes = [P] * 5 + [ctypes.c_double, ctypes.c_int] + [ctypes.c_double] * 3 + \
+        [ctypes.c_int] * 2 + [P] * 4
+    assert so.tk_picard(None, None, None, None, None, 1e-3, 5, 0.1, 1e-3, -1.0, 10, 3, None, None,
+                        None, None) == -3
+    so.tk_prec_operator.argtypes = [P, ctypes.c_int]
+    so.tk_prec_operator.restype = P
+    assert so.tk_prec_operator(None, 0) is None
+
+
+def test_round_workspace_bound_is_a_host_function(so):
+    """tk_round_workspace_bytes is pure host arithmetic: callable without a GPU, zero for
+    invalid sizes, monotone in every argument, and >= the caller-owned-free minimum (the
+    grown space core's Gram pass needs at least n_x * min(R1, n_xi * min(n_t, R2)) doubles)."""
+    f = so.tk_round_workspace_bytes
+    f.argtypes = [ctypes.c_int64] * 5
+    f.restype = ctypes.c_size_t
+    assert f(0, 1, 1, 1, 1) == 0 and f(10, 1, 1, 1, -1) == 0
+    base = (12288, 35, 64, 120, 120)
+    b0 = f(*base)
+    assert b0 >= 8 * 12288 * min(120, 35 * 64)
+    for i in range(5):
+        bigger = list(base)
+        bigger[i] *= 2
+        assert f(*bigger) >= b0
+    # c4 grown ranks: a few GB of scratch, far inside 180 GB of HBM
+    c4 = f(786432, 165, 512, 896, 896)
+    assert 4e9 < c4 < 3e10
