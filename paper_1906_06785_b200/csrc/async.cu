@@ -75,6 +75,7 @@ const void* tk_anchor_k_chol();
 const void* tk_anchor_k_small();
 const void* tk_anchor_k_conv();
 const void* tk_anchor_prec();
+const void* tk_anchor_ttk_api();
 
 // Load every kernel of the library now.  With CUDA's lazy module loading a kernel is loaded at
 // its first launch, and loading waits for the device — which never idles while a context
@@ -92,7 +93,7 @@ static int preload_kernels(tk_ctx* ctx) {
   }
   const void* anchors[] = {tk_anchor_k_apply(), tk_anchor_k_gemm(),  tk_anchor_k_jacobi(),
                            tk_anchor_k_qr(),    tk_anchor_k_chol(),  tk_anchor_k_small(),
-                           tk_anchor_k_conv(),  tk_anchor_prec()};
+                           tk_anchor_k_conv(),  tk_anchor_prec(),    tk_anchor_ttk_api()};
   for (const void* a : anchors) {
     cudaFunction_t f;
     TK_CUDA_TRY(ctx, cudaGetFuncBySymbol(&f, a));

@@ -470,7 +470,7 @@ int tk_launch_stoch_apply(tk_ctx* ctx, const tk_op* op, int r1, int r2, const do
                           double* Y2, bool compact) {
   const int64_t rows = (int64_t)op->T * r1;
   const int64_t total = rows * op->n_xi * op->T * r2;
-  if (!compact) TK_CUDA_TRY(ctx, cudaMemsetAsync(Y2, 0, sizeof(double) * total, ctx->stream));
+  if (!compact) TK_TRY(tk_zero(ctx, Y2, 1, sizeof(double) * total, sizeof(double) * total));
   const int n = (int)(op->n_xi * r2);
   const int bx = std::max(1, std::min((n + 255) / 256, 8));
   if (rows > 65535) {

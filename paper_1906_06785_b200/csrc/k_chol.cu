@@ -554,10 +554,9 @@ int grid_for(tk_ctx* ctx, int64_t total) {
 // stopped the remaining panel launches and (skipped) updates only cost launch latency.
 constexpr int kCholPoll = 2;
 static int chol_stopped(tk_ctx* ctx, const int* state, bool* stopped) {
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, state + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                                   ctx->stream));
-  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  *stopped = *(int*)ctx->pinned != 0;
+  int st = 0;
+  TK_TRY(tk_read_host(ctx, ctx->stream, &st, state + 1, sizeof(int)));
+  *stopped = st != 0;
   return TK_OK;
 }
 
@@ -574,11 +573,10 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
   DevBuf Hw, tol;
   TK_TRY(Hw.get(ctx, (size_t)n * n));
   TK_TRY(tol.get(ctx, 1));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(Hw.p, H, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(Ro, 0, sizeof(double) * n * n, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(state, 0, (2 + (size_t)n) * sizeof(int), ctx->stream));
-  if (rem_out) TK_CUDA_TRY(ctx, cudaMemsetAsync(rem_out, 0, sizeof(double), ctx->stream));
+  TK_TRY(tk_copy2d(ctx, 1, (int64_t)n * n, H, (int64_t)n * n, Hw.p, (int64_t)n * n));
+  TK_TRY(tk_zero(ctx, Ro, 1, sizeof(double) * n * n, sizeof(double) * n * n));
+  TK_TRY(tk_zero(ctx, state, 1, (2 + (int64_t)n) * sizeof(int), (2 + (int64_t)n) * sizeof(int)));
+  if (rem_out) TK_TRY(tk_zero(ctx, rem_out, 1, sizeof(double), sizeof(double)));
   max_diag_tol_k<<<1, 256, 0, ctx->stream>>>(n, H, tol_rel, tol_abs_dev, tol.p);
   TK_LAUNCH_CHECK(ctx);
   if (!pivot && !rem_out) {
@@ -705,8 +703,7 @@ int tk_pchol(tk_ctx* ctx, int n, const double* H, double tol_rel, const double* 
 int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int64_t ldx) {
   if (k <= 0) return TK_OK;
   TagScope tag(ctx, "tri_inv");
-  TK_CUDA_TRY(ctx, cudaMemset2DAsync(X, sizeof(double) * ldx, 0, sizeof(double) * k, k,
-                                     ctx->stream));
+  TK_TRY(tk_zero(ctx, X, k, sizeof(double) * k, sizeof(double) * ldx));
   const int nbk = (k + TS_H - 1) / TS_H;
   {
     const int pid = tk_prof_begin(ctx, "tri_inv_diag", 0.0, 0.0);
@@ -745,7 +742,7 @@ int tk_gather_cols(tk_ctx* ctx, int64_t rows, int k, const double* Ro, int64_t l
 int tk_scatter_rows(tk_ctx* ctx, int64_t n, int k, int64_t cols, const double* X, const int* piv,
                     double* S) {
   if (n <= 0 || cols <= 0) return TK_OK;
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(S, 0, sizeof(double) * n * cols, ctx->stream));
+  TK_TRY(tk_zero(ctx, S, 1, sizeof(double) * n * cols, sizeof(double) * n * cols));
   if (k <= 0) return TK_OK;
   scatter_rows_k<<<grid_for(ctx, (int64_t)k * cols), 256, 0, ctx->stream>>>(n, k, cols, X, piv, S);
   TK_LAUNCH_CHECK(ctx);

@@ -416,8 +416,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
       ctx->err = "tk_dgemm: K == 0 with beta != 0 is not supported";
       return TK_EARG;
     }
-    TK_CUDA_TRY(ctx, cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * N, M,
-                                       ctx->stream));
+    TK_TRY(tk_zero(ctx, C, M, sizeof(double) * N, sizeof(double) * ldc));
     return TK_OK;
   }
   // tile configuration: large non-symmetric products whose N is a multiple of 80 but not of 64

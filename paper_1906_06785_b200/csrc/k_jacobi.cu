@@ -621,8 +621,8 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   unsigned long long* offmax = (unsigned long long*)(scr.p + 1);
   int* stats = (int*)(scr.p + 1 + max_sweeps);
   int* d_sweeps = stats + max_sweeps;
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(scr.p + 1, 0, sizeof(double) * (1 + 2 * (size_t)max_sweeps),
-                                   ctx->stream));
+  TK_TRY(tk_zero(ctx, scr.p + 1, 1, sizeof(double) * (1 + 2 * (int64_t)max_sweeps),
+                 sizeof(double) * (1 + 2 * (int64_t)max_sweeps)));
   const int prof_id = tk_prof_begin(ctx, "jacobi", 0.0, 0.0);
   max_abs_diag_k<<<1, 256, 0, ctx->stream>>>(n, A, d_maxdiag);
   TK_LAUNCH_CHECK(ctx);
@@ -686,10 +686,7 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   TK_LAUNCH_CHECK(ctx);
   tk_prof_end(ctx, prof_id);
   if (sweeps_out) {
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, d_sweeps, sizeof(int), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    *sweeps_out = *(int*)ctx->pinned;
+    TK_TRY(tk_read_host(ctx, ctx->stream, sweeps_out, d_sweeps, sizeof(int)));
   }
   return TK_OK;
 }

@@ -954,8 +954,7 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   if (n <= 0) return TK_OK;
   DevBuf Aw, Vb, Tb, VTb, VTtb;
   TK_TRY(Aw.get(ctx, (size_t)n * n));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(Aw.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
+  TK_TRY(tk_copy2d(ctx, 1, (int64_t)n * n, A, (int64_t)n * n, Aw.p, (int64_t)n * n));
   const int np = (n + QB - 1) / QB;
   // panel p: V, V T, V T^T as (n - j0) x QB at offset p*n*QB;  T: QB x QB
   TK_TRY(Vb.get(ctx, (size_t)np * n * QB));
@@ -1129,10 +1128,7 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
     // panels of the rank-128 time-core Gram).
     if (!no_stop && (p + 1) % kQrPoll == 0 && p + 2 < np) {
       int st = 0;
-      TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned ? ctx->pinned : &st, stop_at, sizeof(int),
-                                       cudaMemcpyDeviceToHost, s0));
-      TK_CUDA_TRY(ctx, cudaStreamSynchronize(s0));
-      if (ctx->pinned) st = *(int*)ctx->pinned;
+      TK_TRY(tk_read_host(ctx, s0, &st, stop_at, sizeof(int)));
       if (st <= p + 1) break;
     }
   }

@@ -49,6 +49,16 @@ __global__ void copy2d_k(int64_t rows, int64_t cols, const double* __restrict__ 
   }
 }
 
+// zero a rows x cols block (leading dimension ld, in 4-byte words: serves doubles and ints)
+__global__ void zero2d_k(int64_t rows, int64_t cols, uint32_t* __restrict__ dst, int64_t ld) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    dst[r * ld + c] = 0u;
+  }
+}
+
 __global__ void fill_k(double* dst, int64_t n, double v) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
@@ -287,6 +297,16 @@ int tk_copy2d(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_
               double* dst, int64_t ldd) {
   if (rows <= 0 || cols <= 0) return TK_OK;
   copy2d_k<<<grid_for(ctx, rows * cols), 256, 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd);
+  TK_LAUNCH_CHECK(ctx);
+  return TK_OK;
+}
+// Kernel zero-fill / copy (not cudaMemsetAsync / cudaMemcpyAsync): the rounding's critical path
+// must not share the copy engines with a user's concurrent bulk H2D / D2H transfers (measured:
+// a 408 MB H2D beside a c4 op slowed it by ~6 ms).
+int tk_zero(tk_ctx* ctx, void* dst, int64_t rows, int64_t cols_bytes, int64_t ld_bytes) {
+  if (rows <= 0 || cols_bytes <= 0) return TK_OK;
+  const int64_t cw = (cols_bytes + 3) / 4, lw = ld_bytes / 4;
+  zero2d_k<<<grid_for(ctx, rows * cw), 256, 0, ctx->stream>>>(rows, cw, (uint32_t*)dst, lw);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }

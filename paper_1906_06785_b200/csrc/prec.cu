@@ -276,11 +276,12 @@ static int bt_solve_impl(tk_ctx* ctx, const tk_bt* bt, const tk_tt* x, int64_t r
   TagScope tag(ctx, "bt_solve");
   y->r1 = x->r1;
   y->r2 = x->r2;
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(y->U1, 0, sizeof(double) * x->n_x * r, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(y->U2, x->U2, sizeof(double) * x->r1 * x->n_xi * x->r2,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(y->U3, x->U3, sizeof(double) * x->r2 * x->n_t,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_TRY(tk_zero(ctx, y->U1, 1, sizeof(double) * x->n_x * r, sizeof(double) * x->n_x * r));
+  {
+    const int64_t n2 = x->r1 * x->n_xi * x->r2, n3 = x->r2 * x->n_t;
+    TK_TRY(tk_copy2d(ctx, 1, n2, x->U2, n2, y->U2, n2));
+    TK_TRY(tk_copy2d(ctx, 1, n3, x->U3, n3, y->U3, n3));
+  }
   for (int s = 0; s < reps; s++) {
     const double* B = x->U1 + (row0 + s * n) * r;
     double* Y = y->U1 + (row0 + s * n) * r;
@@ -483,13 +484,12 @@ int make_like(tk_ctx* ctx, const tk_tt* x, OwnedPtr& y) {
 int restrict_rows(tk_ctx* ctx, const tk_tt* x, int64_t lo, int64_t hi, OwnedPtr& y) {
   TK_TRY(make_like(ctx, x, y));
   const int64_t r = x->r1;
-  TK_CUDA_TRY(ctx, cudaMemsetAsync(y->t.U1, 0, sizeof(double) * x->n_x * r, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(y->t.U1 + lo * r, x->U1 + lo * r, sizeof(double) * (hi - lo) * r,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(y->t.U2, x->U2, sizeof(double) * x->r1 * x->n_xi * x->r2,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(y->t.U3, x->U3, sizeof(double) * x->r2 * x->n_t,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  TK_TRY(tk_zero(ctx, y->t.U1, 1, sizeof(double) * x->n_x * r, sizeof(double) * x->n_x * r));
+  TK_TRY(tk_copy2d(ctx, 1, (hi - lo) * r, x->U1 + lo * r, (hi - lo) * r, y->t.U1 + lo * r,
+                   (hi - lo) * r));
+  const int64_t n2 = x->r1 * x->n_xi * x->r2, n3 = x->r2 * x->n_t;
+  TK_TRY(tk_copy2d(ctx, 1, n2, x->U2, n2, y->t.U2, n2));
+  TK_TRY(tk_copy2d(ctx, 1, n3, x->U3, n3, y->t.U3, n3));
   return TK_OK;
 }
 
@@ -511,10 +511,11 @@ int axpby_round(tk_ctx* ctx, double a, const tk_tt* x, double b, const tk_tt* y,
 int m_inv(tk_ctx* ctx, const tk_prec* P, const tk_tt* x, OwnedPtr& out) {
   OwnedPtr tc;
   TK_TRY(make_like(ctx, x, tc));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(tc->t.U1, x->U1, sizeof(double) * x->n_x * x->r1,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(tc->t.U2, x->U2, sizeof(double) * x->r1 * x->n_xi * x->r2,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  {
+    const int64_t n1 = x->n_x * x->r1, n2 = x->r1 * x->n_xi * x->r2;
+    TK_TRY(tk_copy2d(ctx, 1, n1, x->U1, n1, tc->t.U1, n1));
+    TK_TRY(tk_copy2d(ctx, 1, n2, x->U2, n2, tc->t.U2, n2));
+  }
   time_cumsum_k<<<grid1(x->r2), 256, 0, ctx->stream>>>(x->r2, x->n_t, x->U3, tc->t.U3);
   TK_LAUNCH_CHECK(ctx);
   TK_TRY(make_like(ctx, x, out));

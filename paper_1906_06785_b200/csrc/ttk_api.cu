@@ -72,7 +72,8 @@ extern "C" int tk_ctx_create(tk_ctx** out, void* stream) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     ctx->pinned_bytes = 1 << 16;
-    e = cudaMallocHost(&ctx->pinned, ctx->pinned_bytes);
+    e = cudaHostAlloc(&ctx->pinned, ctx->pinned_bytes, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->pinned_dev, ctx->pinned, 0);
   }
   if (e != cudaSuccess) {
     delete ctx;
@@ -275,16 +276,38 @@ static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes);
 int tk_sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
   return sync_read(ctx, host, dev, bytes);
 }
-static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
-  if (bytes > ctx->pinned_bytes) {
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+namespace {
+// bytes -> the mapped pinned buffer (8-byte words when aligned)
+__global__ void read_to_host_k(const void* __restrict__ src, void* dst, size_t n) {
+  if ((((uintptr_t)src | (uintptr_t)dst) & 7) == 0) {
+    const size_t w = n / 8;
+    for (size_t i = threadIdx.x; i < w; i += blockDim.x)
+      ((volatile unsigned long long*)dst)[i] = ((const unsigned long long*)src)[i];
+    for (size_t i = 8 * w + threadIdx.x; i < n; i += blockDim.x)
+      ((volatile unsigned char*)dst)[i] = ((const unsigned char*)src)[i];
+  } else {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x)
+      ((volatile unsigned char*)dst)[i] = ((const unsigned char*)src)[i];
+  }
+}
+}  // namespace
+
+int tk_read_host(tk_ctx* ctx, cudaStream_t stream, void* host, const void* dev, size_t bytes) {
+  if (bytes == 0) return TK_OK;
+  if (bytes > ctx->pinned_bytes || !ctx->pinned_dev) {
+    TK_CUDA_TRY(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream));
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(stream));
     return TK_OK;
   }
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  read_to_host_k<<<1, 256, 0, stream>>>(dev, ctx->pinned_dev, bytes);
+  TK_LAUNCH_CHECK(ctx);
+  TK_CUDA_TRY(ctx, cudaStreamSynchronize(stream));
   memcpy(host, ctx->pinned, bytes);
   return TK_OK;
+}
+
+static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  return tk_read_host(ctx, ctx->stream, host, dev, bytes);
 }
 
 // ============================================================================ operator
@@ -1036,11 +1059,9 @@ int pass2_chol(tk_ctx* ctx, int64_t k, const DevBuf& GW, const double* floor, De
                        nullptr, nullptr, 0.0, 0, floor));
   TK_TRY(lam.get(ctx, k));
   TK_TRY(tk_fill(ctx, lam.p, k, 0.0));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(lam.p, lam2.p, sizeof(double) * kc, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
+  TK_TRY(tk_copy2d(ctx, 1, kc, lam2.p, kc, lam.p, kc));
   if (kc < k)
-    TK_CUDA_TRY(ctx, cudaMemcpyAsync(lam.p + kc, rem.p, sizeof(double), cudaMemcpyDeviceToDevice,
-                                     ctx->stream));
+    TK_TRY(tk_copy2d(ctx, 1, 1, rem.p, 1, lam.p + kc, 1));
   TK_TRY(V2.get(ctx, k * k));
   TK_TRY(tk_fill(ctx, V2.p, k * k, 0.0));
   TK_TRY(tk_dgemm(ctx, false, false, k, kc, kc, 1.0, Qv.p, kc, V2p.p, kc, 0.0, V2.p, k));
@@ -1757,3 +1778,8 @@ extern "C" int tk_gmres_solve_p(tk_ctx* ctx, const tk_op* op, const tk_prec* P, 
   return gmres_solve_entry(ctx, op, P, b, restart, max_cycles, tol, tol_gmres, eps_soln, z,
                            explicit_out, ls_out, cycles_done, steps_out);
 }
+
+// Module anchor: async.cu loads every kernel of this translation unit through it (lazy module
+// loading must not happen while a context stream is gated, see tk_ctx_set_async).
+__global__ void tk_anchor_ttk_api_k() {}
+const void* tk_anchor_ttk_api() { return (const void*)tk_anchor_ttk_api_k; }

@@ -30,6 +30,8 @@ struct tk_ctx {
   // pinned host scratch for the few device->host reads (ranks, scalars)
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  void* pinned_dev = nullptr;  // device alias of `pinned` (mapped): small reads are kernel stores
+
   // profiling (tk_ctx_profile): per-launch event pairs, tagged by the current phase
   bool prof = false;
   bool prof_timeline = false;  // tk_ctx_profile(ctx, 3): dump start offsets too
@@ -252,16 +254,15 @@ struct OwnedTT {
 };
 using OwnedPtr = std::unique_ptr<OwnedTT>;
 
+int tk_copy2d(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
+              double* dst, int64_t ldd);
 inline int clone_tt(tk_ctx* ctx, const tk_tt* src, OwnedTT& dst) {
   TK_TRY(dst.make(ctx, src->n_x, src->n_xi, src->n_t, src->r1, src->r2));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U1, src->U1, sizeof(double) * src->n_x * src->r1,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U2, src->U2,
-                                   sizeof(double) * src->r1 * src->n_xi * src->r2,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  TK_CUDA_TRY(ctx, cudaMemcpyAsync(dst.t.U3, src->U3, sizeof(double) * src->r2 * src->n_t,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  return TK_OK;
+  const int64_t n1 = src->n_x * src->r1, n2 = src->r1 * src->n_xi * src->r2,
+                n3 = src->r2 * src->n_t;
+  TK_TRY(tk_copy2d(ctx, 1, n1, src->U1, n1, dst.t.U1, n1));  // kernels, not the copy engines
+  TK_TRY(tk_copy2d(ctx, 1, n2, src->U2, n2, dst.t.U2, n2));
+  return tk_copy2d(ctx, 1, n3, src->U3, n3, dst.t.U3, n3);
 }
 
 // A right preconditioner v -> P^{-1} v (Alg. 3 line 4) as the GMRES drivers see it: writes a
@@ -279,6 +280,10 @@ TkPrecFn tk_prec_fn(tk_ctx* ctx, const tk_prec* P, int part);
 int tk_apply_round_owned(tk_ctx* ctx, const tk_op* op, const tk_tt* x, OwnedPtr& y, double tol);
 int set_zero_tt(tk_ctx* ctx, tk_tt* x);
 int tk_sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes);
+// Small device -> host read on `stream` (synchronises it): a one-CTA kernel stores the bytes into
+// the context's mapped pinned buffer, so the read never queues behind bulk DMA copies that share
+// the device-to-host copy engine (a concurrent 1 GB D2H delayed every rank decision).
+int tk_read_host(tk_ctx* ctx, cudaStream_t stream, void* host, const void* dev, size_t bytes);
 
 // ----------------------------------------------------------------------------- kernels (host wrappers)
 // Row-major fp64 GEMM on DMMA (mma.sync m8n8k4 f64):
@@ -360,6 +365,8 @@ int tk_row_scale(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int
 int tk_copy2d(tk_ctx* ctx, int64_t rows, int64_t cols, const double* src, int64_t lds,
               double* dst, int64_t ldd);
 int tk_fill(tk_ctx* ctx, double* dst, int64_t n, double v);
+// zero rows x cols_bytes bytes at dst with row stride ld_bytes (multiples of 4 bytes), by a kernel
+int tk_zero(tk_ctx* ctx, void* dst, int64_t rows, int64_t cols_bytes, int64_t ld_bytes);
 int tk_eye(tk_ctx* ctx, double* dst, int64_t n);
 // Rank decision on device from eigenvalues lam (descending, n of them):
 //   sigma = sqrt(max(lam,0)) written to sig; info[0] = r (rule), info[1] = k (numerical dim
