@@ -107,6 +107,25 @@ size_t tk_round_workspace_bytes(int64_t n_x, int64_t n_xi, int64_t n_t, int64_t 
 int tk_ctx_reserve(tk_ctx* ctx, size_t bytes);
 int64_t tk_ctx_scratch_high_water(tk_ctx* ctx, int reset);
 
+/* The dense contraction of the path (north star: "Gram/TSQR on FP64 DMMA tensor cores fed via
+ * TMA"; the Grams W = X^T Y of the rounding and of the TT dot):
+ *   C (M x N, ldc) = alpha op(A) op(B) + beta C,  op(A) M x K, op(B) K x N, fp64, DEVICE
+ * pointers, row-major: transA == 0: A is M x K (lda >= K); != 0: A is stored K x M (lda >= M);
+ * transB == 0: B is K x N (ldb >= N); != 0: B is stored N x K (ldb >= K).  sym != 0 (needs
+ * M == N, B^T A == A^T B): only the upper tiles are computed and mirrored (symmetric Gram).
+ * Asynchronous on the context stream; split-K partial sums are reduced in a fixed order, so
+ * results are bitwise reproducible run to run (per feed).  Errors: TK_EARG (null pointer,
+ * sym with M != N, K == 0 with beta != 0), TK_ECUDA.
+ * tk_ctx_set_gemm_feed: how the heavy products (>= 2e8 flops, beta == 0) get their operand
+ * tiles: 1 = TMA tensor tiles (cp.async.bulk.tensor + mbarrier, 128B-swizzled shared memory;
+ * default), 0 = cp.async.  Operands that are not 16-byte aligned or have an odd leading
+ * dimension always take the cp.async kernel.  Both feeds compute the same sums in a different
+ * (fixed) order. */
+int tk_gemm(tk_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+            int64_t ldc, int sym);
+int tk_ctx_set_gemm_feed(tk_ctx* ctx, int mode);
+
 /* Operator descriptor  A = sum_{k<T} T_k (x) G_k (x) K_k.
  *   K_k : n_x x n_x CSR, HOST arrays: rowptr[n_x+1] (int32), col[nnz_k] (int32, 0-based),
  *         val[nnz_k] (float64).

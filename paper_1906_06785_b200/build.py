@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttk.so")
-SOURCES = ["ttk_api.cu", "k_apply.cu", "k_gemm.cu", "k_jacobi.cu", "k_qr.cu", "k_chol.cu", "k_small.cu", "k_conv.cu", "prec.cu", "picard.cu", "async.cu"]
+SOURCES = ["ttk_api.cu", "k_apply.cu", "k_gemm.cu", "k_gemm_tma.cu", "k_jacobi.cu", "k_qr.cu", "k_chol.cu", "k_small.cu", "k_conv.cu", "prec.cu", "picard.cu", "async.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

@@ -69,6 +69,7 @@ bool entry(const char* name, F* out) {
 // One kernel of every translation unit (its module anchor).
 const void* tk_anchor_k_apply();
 const void* tk_anchor_k_gemm();
+const void* tk_anchor_k_gemm_tma();
 const void* tk_anchor_k_jacobi();
 const void* tk_anchor_k_qr();
 const void* tk_anchor_k_chol();
@@ -93,7 +94,8 @@ static int preload_kernels(tk_ctx* ctx) {
   }
   const void* anchors[] = {tk_anchor_k_apply(), tk_anchor_k_gemm(),  tk_anchor_k_jacobi(),
                            tk_anchor_k_qr(),    tk_anchor_k_chol(),  tk_anchor_k_small(),
-                           tk_anchor_k_conv(),  tk_anchor_prec(),    tk_anchor_ttk_api()};
+                           tk_anchor_k_conv(),  tk_anchor_prec(),    tk_anchor_ttk_api(),
+                           tk_anchor_k_gemm_tma()};
   for (const void* a : anchors) {
     cudaFunction_t f;
     TK_CUDA_TRY(ctx, cudaGetFuncBySymbol(&f, a));

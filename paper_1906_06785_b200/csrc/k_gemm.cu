@@ -469,7 +469,14 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   // 16-byte vector path: contiguous dims even and 16-byte aligned bases
   bool v2 = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
             (((uintptr_t)B & 15) == 0);
-  int st;
+  int st = TK_OK;
+  // heavy products with beta == 0: the TMA-fed kernel (same tile, same split-K partials)
+  const bool use_tma = ctx->gemm_tma && cfg == 0 && beta == 0.0 && !triu_b && flops >= 2e8 &&
+                       tk_dgemm_tma_eligible(transA, transB, M, N, K, A, lda, B, ldb);
+  if (use_tma) {
+    st = tk_dgemm_tma_launch(ctx, transA, transB, M, N, K, alpha, A, lda, B, ldb, C, ldc, kchunk,
+                             (int)splits, sym ? 1 : 0, partial, skip);
+  } else {
 #define TK_GEMM_CASE(a, b, v)                                                               \
   if (AK == a && BKm == b && v2 == v) {                                                     \
     const int sf = (sym ? 1 : 0) | (triu_b ? 2 : 0);                                        \
@@ -489,6 +496,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   TK_GEMM_CASE(true, true, false)
   TK_GEMM_CASE(true, true, true)
 #undef TK_GEMM_CASE
+  }
   if (st != TK_OK) return st;
   if (splits > 1) {
     int64_t total = M * N;

@@ -272,6 +272,34 @@ extern "C" int64_t tk_ctx_scratch_high_water(tk_ctx* ctx, int reset) {
 extern "C" const char* tk_last_error(const tk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 extern "C" int64_t tk_ctx_launch_count(const tk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+extern "C" int tk_ctx_set_gemm_feed(tk_ctx* ctx, int mode) {
+  if (!ctx) return TK_EARG;
+  if (mode != 0 && mode != 1) {
+    ctx->err = "tk_ctx_set_gemm_feed: mode must be 0 (cp.async) or 1 (TMA)";
+    return TK_EARG;
+  }
+  TK_ASYNC_GUARD(ctx);
+  ctx->gemm_tma = mode;
+  return TK_OK;
+}
+
+extern "C" int tk_gemm(tk_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K,
+                       double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double beta, double* C, int64_t ldc, int sym) {
+  if (!ctx) return TK_EARG;
+  if (M < 0 || N < 0 || K < 0 || ((!A || !B) && K > 0 && M > 0 && N > 0) || (!C && M > 0 && N > 0)) {
+    ctx->err = "tk_gemm: null pointer or negative size";
+    return TK_EARG;
+  }
+  TK_ASYNC_GUARD(ctx);
+  const char* tag0 = ctx->tag;
+  ctx->tag = "tk_gemm";
+  const int st = tk_dgemm(ctx, transA != 0, transB != 0, M, N, K, alpha, A, lda, B, ldb, beta, C,
+                          ldc, sym != 0);
+  ctx->tag = tag0;
+  return st;
+}
+
 static int sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes);
 int tk_sync_read(tk_ctx* ctx, void* host, const void* dev, size_t bytes) {
   return sync_read(ctx, host, dev, bytes);

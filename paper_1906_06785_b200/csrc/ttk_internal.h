@@ -58,6 +58,9 @@ struct tk_ctx {
   cudaEvent_t crit_ev[2] = {nullptr, nullptr};
   // async mode (tk_ctx_set_async, async.cu): the worker that runs queued roundings
   tk_async* async = nullptr;
+  // operand feed of the big DMMA GEMMs: 1 = TMA tensor tiles (k_gemm_tma.cu, default),
+  // 0 = cp.async (k_gemm.cu); tk_ctx_set_gemm_feed
+  int gemm_tma = 1;
 };
 // Async mode (async.cu).  drain: wait until the queued jobs ran (returns their first error);
 // submit: queue body() for the worker, ordered after (and gating) the caller's stream.
@@ -299,6 +302,15 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
              double beta, double* C, int64_t ldc, bool sym = false, bool triu_b = false,
              const int* skip = nullptr);
+
+// TMA-fed variant of the 64 x 64 DMMA kernel (k_gemm_tma.cu); tk_dgemm picks it for eligible
+// heavy products (beta == 0, no triangular-B mode) when ctx->gemm_tma is set.
+bool tk_dgemm_tma_eligible(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+                           const double* A, int64_t lda, const double* B, int64_t ldb);
+int tk_dgemm_tma_launch(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+                        double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* C, int64_t ldc, int64_t kchunk, int splits, int sym,
+                        double* partial, const int* skip);
 
 // Symmetric eigen-decomposition by parallel cyclic two-sided Jacobi.
 //   A: n x n symmetric (device, row-major, ld = n), destroyed.

@@ -29,7 +29,7 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_prec_create_lsc", "tk_prec_destroy", "tk_prec_apply", "tk_prec_operator",
             "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard",
             "tk_ctx_set_async", "tk_sync_ranks", "tk_round_workspace_bytes", "tk_ctx_reserve",
-            "tk_ctx_scratch_high_water"]
+            "tk_ctx_scratch_high_water", "tk_gemm", "tk_ctx_set_gemm_feed"]
 
 
 class TkError(RuntimeError):
@@ -111,6 +111,8 @@ def lib():
     L.tk_ctx_reserve.argtypes = [P, ctypes.c_size_t]
     L.tk_ctx_scratch_high_water.argtypes = [P, I]
     L.tk_ctx_scratch_high_water.restype = I64
+    L.tk_gemm.argtypes = [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64, I]
+    L.tk_ctx_set_gemm_feed.argtypes = [P, I]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
@@ -159,6 +161,22 @@ class Context:
             if t is not None:
                 t._update(st)
         self.check(rc)
+
+    def set_gemm_feed(self, mode: int):
+        """0 = cp.async, 1 = TMA tensor tiles (default) for the heavy DMMA products."""
+        self.check(lib().tk_ctx_set_gemm_feed(self._h, int(mode)))
+
+    def gemm(self, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, M: int, N: int, K: int,
+             trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,
+             lda: int | None = None, ldb: int | None = None, ldc: int | None = None,
+             sym: bool = False):
+        """C = alpha op(A) op(B) + beta C on device fp64 buffers (tk_gemm; marshalling only)."""
+        lda = lda if lda is not None else (M if trans_a else K)
+        ldb = ldb if ldb is not None else (K if trans_b else N)
+        ldc = ldc if ldc is not None else N
+        self.check(lib().tk_gemm(self._h, int(trans_a), int(trans_b), M, N, K, float(alpha),
+                                 A.data_ptr(), lda, B.data_ptr(), ldb, float(beta), C.data_ptr(),
+                                 ldc, int(sym)))
 
     def reserve(self, nbytes: int):
         self.check(lib().tk_ctx_reserve(self._h, int(nbytes)))
