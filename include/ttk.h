@@ -125,6 +125,12 @@ int tk_gemm(tk_ctx* ctx, int transA, int transB, int64_t M, int64_t N, int64_t K
             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
             int64_t ldc, int sym);
 int tk_ctx_set_gemm_feed(tk_ctx* ctx, int mode);
+/* Schedule of the block-Jacobi eigensolver behind the bond SVDs (the truncated
+ * SVDs of the rounding): 1 = dataflow (default: the CTAs that solve the 64 x 64 pair problems
+ * and the CTAs that apply the tile updates run one round apart, ordered by counters in global
+ * memory), 0 = two grid-wide barriers per round.  Same rotations, same products, same order:
+ * results are bitwise identical.  Errors: TK_EARG. */
+int tk_ctx_set_jacobi_schedule(tk_ctx* ctx, int mode);
 
 /* Operator descriptor  A = sum_{k<T} T_k (x) G_k (x) K_k.
  *   K_k : n_x x n_x CSR, HOST arrays: rowptr[n_x+1] (int32), col[nnz_k] (int32, 0-based),

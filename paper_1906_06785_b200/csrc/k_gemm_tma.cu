@@ -204,6 +204,12 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
 #pragma unroll
         for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
+    // The stage is about to be overwritten by the TMA (async proxy) while it was read through
+    // the generic proxy: the release needs a cross-proxy fence.  Without it a warp's fragment
+    // loads were occasionally overtaken by the refill when the CTA shared its SM with
+    // higher-priority kernels (bond-1 reconstruction on the side stream: a few wrong 32 x 32
+    // warp tiles per run; a CTA barrier instead of the fence did not help).
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(bar0 + 8 * (STAGES + s));
   }

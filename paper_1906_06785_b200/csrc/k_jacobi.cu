@@ -104,8 +104,11 @@ __device__ __forceinline__ bool needs_rot(double app, double aqq, double apq, do
 // computes the 32 disjoint rotations; (b) every thread applies J^T S J to two 2x2 blocks
 // (rows of one pair x columns of another: each element belongs to exactly one block, so the
 // update is in place) and Q <- Q J to four (row, pair) items.  Two barriers per round.
+// staged: S (full symmetric) and Q = I are already in shared memory (the dataflow schedule builds
+// the pair's block itself); Qout / Sout: where this pair's Q and rotated S go.
 __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerShared& sh,
-                            double abs_tol, double lsk) {
+                            double abs_tol, double lsk, bool staged = false,
+                            double* Qout = nullptr, double* Sout = nullptr) {
   double* S = sm;
   double* Q = sm + JS * JLD;
   int I, J;
@@ -113,11 +116,15 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
   const double* G = a.G;
   const int n_pad = a.n_pad;
   const int tid = threadIdx.x;
-  for (int e = tid; e < JS * JS; e += blockDim.x) {
-    int i = e / JS, j = e % JS;
-    int gi = gidx(i, I, J), gj = gidx(j, I, J);
-    S[i * JLD + j] = 0.5 * (G[(int64_t)gi * n_pad + gj] + G[(int64_t)gj * n_pad + gi]);
-    Q[i * JLD + j] = (i == j) ? 1.0 : 0.0;
+  if (!Qout) Qout = a.Qb;
+  if (!Sout) Sout = a.Sb;
+  if (!staged) {
+    for (int e = tid; e < JS * JS; e += blockDim.x) {
+      int i = e / JS, j = e % JS;
+      int gi = gidx(i, I, J), gj = gidx(j, I, J);
+      S[i * JLD + j] = 0.5 * (G[(int64_t)gi * n_pad + gj] + G[(int64_t)gj * n_pad + gi]);
+      Q[i * JLD + j] = (i == j) ? 1.0 : 0.0;
+    }
   }
   __syncthreads();
   {
@@ -129,8 +136,8 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
     }
     any = __syncthreads_or(any);
     if (!any) {
-      double* Qo = a.Qb + (int64_t)t * JS * JS;
-      double* So = a.Sb + (int64_t)t * JS * JS;
+      double* Qo = Qout + (int64_t)t * JS * JS;
+      double* So = Sout + (int64_t)t * JS * JS;
       for (int e = tid; e < JS * JS; e += blockDim.x) {
         Qo[e] = Q[(e / JS) * JLD + e % JS];
         So[e] = S[uidx(e / JS, e % JS)];
@@ -288,8 +295,8 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
     }
     __syncthreads();
   }
-  double* Qo = a.Qb + (int64_t)t * JS * JS;
-  double* So = a.Sb + (int64_t)t * JS * JS;
+  double* Qo = Qout + (int64_t)t * JS * JS;
+  double* So = Sout + (int64_t)t * JS * JS;
   for (int e = tid; e < JS * JS; e += blockDim.x) {
     Qo[e] = Q[(e / JS) * JLD + e % JS];
     So[e] = S[uidx(e / JS, e % JS)];
@@ -556,6 +563,296 @@ __global__ void __launch_bounds__(JT) jacobi_persistent_k(JacArgs a, int coop) {
     for (int k = 0; k < 6; k++) a.tstamp[k] = tsum[k];  // [6], [7]: inner phase cycles
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Dataflow schedule ("flow"): the same rounds, pairs, rotations and tile products as
+// jacobi_persistent_k, without grid-wide barriers.  CTAs 0..npairs-1 only solve pairs, the others
+// only apply tile updates, and the two groups run one round apart:
+//   * G is double buffered: G_R (the state after the tile phase of global round R) lives in
+//     Gbuf[R & 1], the embedded input G_{-1} in Gbuf[1]; tile phase R reads G_{R-1} and writes G_R
+//     (every block belongs to exactly one (t, s) item per round, so all of G_R is written).
+//   * The pair CTA of round R builds its own 64 x 64 input block of G_{R-1} instead of waiting
+//     for tile phase R-1: the two diagonal 32 x 32 blocks come from the rotated S of the pairs
+//     (a, b) that held blocks I and J in round R-1, the coupling block is the (I, J) part of
+//     Q_a^T G_{R-2}[IJ_a, IJ_b] Q_b (the same DMMA products, in the same order, the tile phase
+//     uses: the values are bitwise those of G_{R-1}).  So inner(R) depends on inner(R-1) (all
+//     pairs) and on tile phase R-2 only, and overlaps tile phase R-1.
+//   * Q and S of the pairs are double buffered by round parity (tile phase R-1 still reads
+//     Q_{R-1} while inner(R) writes Q_R).
+// Ordering is by two monotonic counters in global memory (finished inner solves, finished tile
+// items): writers __syncthreads + __threadfence + atomicAdd, readers ld.acquire.gpu spin by one
+// thread + __syncthreads; data shared between CTAs is read with ld.global.cg.  All CTAs must be
+// co-resident (cooperative launch; no grid.sync is used).
+struct FlowArgs {
+  JacArgs a;            // a.G unused; a.Qb / a.Sb: [2][npairs * 64 * 64]
+  double* Gbuf[2];
+  unsigned int* cnt;    // [0] finished inner solves, [1] finished tile items
+  double* diag_out;     // n_pad: diagonal of the final G
+};
+
+__device__ __forceinline__ void flow_wait(const unsigned int* c, unsigned int target) {
+  if (threadIdx.x == 0) {
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void flow_signal(unsigned int* c, unsigned int inc) {
+  __syncthreads();
+  if (threadIdx.x == 0 && inc) {
+    __threadfence();
+    atomicAdd(c, inc);
+  }
+}
+
+// slot and half (0: rows 0..31 of the pair, 1: rows 32..63) of block B in tournament round r
+__device__ __forceinline__ void find_block(int B, int r, int nb, int npairs, int& slot, int& half) {
+  slot = 0;
+  half = 0;
+  for (int t = 0; t < npairs; t++) {
+    int I, J;
+    pair_blocks(t, r, nb, I, J);
+    if (I == B) {
+      slot = t;
+      half = 0;
+    } else if (J == B) {
+      slot = t;
+      half = 1;
+    }
+  }
+}
+
+// Two-sided tile product shared by the tile phase and the pair CTAs' input construction:
+// acc <- (Q_t^T (X Q_s)) fragments, X = Gin[IJ_t, IJ_s]; Qs/Xs/Qt: three 64 x TLD tiles in sm.
+__device__ __forceinline__ void two_sided_tile(const double* __restrict__ Gin, int n_pad,
+                                               const double* __restrict__ Qtg,
+                                               const double* __restrict__ Qsg, int It, int Jt,
+                                               int Is, int Js, double* sm, double acc[2][2][2]) {
+  double* Qs = sm;
+  double* Xs = sm + JS * TLD;
+  double* Qt = sm + 2 * JS * TLD;
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    const int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = __ldcg(Qsg + e);
+    Qt[i * TLD + j] = __ldcg(Qtg + e);
+    Xs[i * TLD + j] = __ldcg(Gin + (int64_t)gidx(i, It, Jt) * n_pad + gidx(j, Is, Js));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+  tile_mma(Xs, false, Qs, acc);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        Xs[(wm + 8 * i + (lane >> 2)) * TLD + wn + 8 * j + 2 * (lane & 3) + h] = acc[i][j][h];
+  __syncthreads();
+  tile_mma(Qt, true, Xs, acc);
+}
+
+__device__ void flow_sym_tile(const FlowArgs& f, int R, int t, int s, int r, double* sm) {
+  const JacArgs& a = f.a;
+  const int n_pad = a.n_pad;
+  const double* Gin = f.Gbuf[(R + 1) & 1];
+  double* Gout = f.Gbuf[R & 1];
+  const int64_t qoff = (int64_t)(R & 1) * a.npairs * JS * JS;
+  int It, Jt, Is, Js;
+  pair_blocks(t, r, a.nb, It, Jt);
+  pair_blocks(s, r, a.nb, Is, Js);
+  if (t == s) {
+    const double* S = a.Sb + qoff + (int64_t)t * JS * JS;
+    for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+      const int i = e / JS, j = e % JS;
+      Gout[(int64_t)gidx(i, It, Jt) * n_pad + gidx(j, It, Jt)] = __ldcg(S + e);
+    }
+    return;
+  }
+  double acc[2][2][2];
+  two_sided_tile(Gin, n_pad, a.Qb + qoff + (int64_t)t * JS * JS, a.Qb + qoff + (int64_t)s * JS * JS,
+                 It, Jt, Is, Js, sm, acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
+        const int gm = gidx(m, It, Jt), gn = gidx(n, Is, Js);
+        Gout[(int64_t)gm * n_pad + gn] = acc[i][j][h];
+        Gout[(int64_t)gn * n_pad + gm] = acc[i][j][h];
+      }
+  __syncthreads();
+}
+
+// 64-row tile of V[:, I u J] <- V[:, I u J] Q_t (in place; Q of global round R)
+__device__ void flow_col_tile(const FlowArgs& f, int R, int row0, int t, int r, double* sm) {
+  const JacArgs& a = f.a;
+  double* Qs = sm;
+  double* Ts = sm + JS * TLD;
+  int I, J;
+  pair_blocks(t, r, a.nb, I, J);
+  const double* Q = a.Qb + (int64_t)(R & 1) * a.npairs * JS * JS + (int64_t)t * JS * JS;
+  double* M = a.V;
+  const int n_pad = a.n_pad;
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = __ldcg(Q + e);
+    Ts[i * TLD + j] = __ldcg(M + (int64_t)(row0 + i) * n_pad + gidx(j, I, J));
+  }
+  __syncthreads();
+  double acc[2][2][2];
+  tile_mma(Ts, false, Qs, acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
+        M[(int64_t)(row0 + m) * n_pad + gidx(n, I, J)] = acc[i][j][h];
+      }
+  __syncthreads();
+}
+
+// Stage the pair's input block S = G_{R-1}[I u J, I u J] and Q = I in shared memory.
+__device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double* sm) {
+  const JacArgs& a = f.a;
+  const int n_pad = a.n_pad, nrounds = a.nb - 1;
+  double* S = sm;
+  double* Q = sm + JS * JLD;
+  int I, J;
+  pair_blocks(t, r, a.nb, I, J);
+  if (R == 0) {
+    const double* G = f.Gbuf[1];
+    for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+      int i = e / JS, j = e % JS;
+      int gi = gidx(i, I, J), gj = gidx(j, I, J);
+      S[i * JLD + j] = 0.5 * (G[(int64_t)gi * n_pad + gj] + G[(int64_t)gj * n_pad + gi]);
+      Q[i * JLD + j] = (i == j) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const int rp = (r + nrounds - 1) % nrounds;
+  int ta, ha, tb, hb;
+  find_block(I, rp, a.nb, a.npairs, ta, ha);
+  find_block(J, rp, a.nb, a.npairs, tb, hb);
+  int Ia, Ja, Ib, Jb;
+  pair_blocks(ta, rp, a.nb, Ia, Ja);
+  pair_blocks(tb, rp, a.nb, Ib, Jb);
+  const int64_t qoff = (int64_t)((R - 1) & 1) * a.npairs * JS * JS;
+  const double* Qa = a.Qb + qoff + (int64_t)ta * JS * JS;
+  const double* Qbb = a.Qb + qoff + (int64_t)tb * JS * JS;
+  const double* Sa = a.Sb + qoff + (int64_t)ta * JS * JS;
+  const double* Sbb = a.Sb + qoff + (int64_t)tb * JS * JS;
+  // coupling block: the tile phase computes item (min, max) of the two slots and mirrors it;
+  // use the same orientation so the values are bitwise the tile phase's
+  double acc[2][2][2];
+  const bool ab = ta < tb;
+  if (ab)
+    two_sided_tile(f.Gbuf[R & 1], n_pad, Qa, Qbb, Ia, Ja, Ib, Jb, sm, acc);
+  else
+    two_sided_tile(f.Gbuf[R & 1], n_pad, Qbb, Qa, Ib, Jb, Ia, Ja, sm, acc);
+  __syncthreads();  // tiles consumed: S / Q alias them
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    const int i = e / JS, j = e % JS;
+    Q[i * JLD + j] = (i == j) ? 1.0 : 0.0;
+    if (i < JB && j < JB)
+      S[i * JLD + j] = __ldcg(Sa + (ha * JB + i) * JS + ha * JB + j);
+    else if (i >= JB && j >= JB)
+      S[i * JLD + j] = __ldcg(Sbb + (hb * JB + i - JB) * JS + hb * JB + j - JB);
+  }
+  // acc holds Y[m][n]: rows = slot min(ta, tb)'s pair, cols = the other's
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+  const int hr = ab ? ha : hb, hc = ab ? hb : ha;  // wanted half of the rows / columns of Y
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
+        if ((m >> 5) != hr || (n >> 5) != hc) continue;
+        // Y rows belong to I when ab, else to J
+        const int li = ab ? (m & 31) : (n & 31), lj = ab ? (n & 31) : (m & 31);
+        S[li * JLD + JB + lj] = acc[i][j][h];
+        S[(JB + lj) * JLD + li] = acc[i][j][h];
+      }
+}
+
+__global__ void __launch_bounds__(JT) jacobi_flow_k(FlowArgs f) {
+  extern __shared__ double sm[];
+  __shared__ InnerShared sh;
+  const JacArgs& a = f.a;
+  const double abs_tol =
+      fmax(fmax(a.abs_scale * a.d_maxdiag[0], a.abs_floor ? a.abs_floor[0] : 0.0), 1e-300);
+  const int nrounds = a.nb - 1, npairs = a.npairs;
+  const int nsym = npairs * (npairs + 1) / 2;
+  const int nitems = nsym + a.v_tiles * npairs;
+  const bool is_inner = (int)blockIdx.x < npairs;
+  const int ntile = (int)gridDim.x - npairs, tile_id = (int)blockIdx.x - npairs;
+  unsigned int* c_inner = f.cnt;
+  unsigned int* c_tile = f.cnt + 1;
+  int R = 0, sweep = 0;
+  for (; sweep < a.max_sweeps; sweep++) {
+    JacArgs as = a;
+    as.stats = a.stats + sweep;
+    as.offmax = a.offmax + sweep;
+    for (int r = 0; r < nrounds; r++, R++) {
+      if (is_inner) {
+        flow_wait(c_inner, (unsigned)(R * npairs));                   // Q, S of round R - 1
+        if (R >= 2) flow_wait(c_tile, (unsigned)((R - 1) * nitems));  // G_{R-2} complete
+        flow_stage_input(f, R, blockIdx.x, r, sm);
+        const int64_t qoff = (int64_t)(R & 1) * npairs * JS * JS;
+        inner_solve(as, blockIdx.x, r, sm, sh, abs_tol, -1.0, true, a.Qb + qoff, a.Sb + qoff);
+        flow_signal(c_inner, 1);
+      } else {
+        flow_wait(c_inner, (unsigned)((R + 1) * npairs));  // Q, S of round R
+        flow_wait(c_tile, (unsigned)(R * nitems));         // G_{R-1}, V complete
+        int done = 0;
+        for (int w = tile_id; w < nitems; w += ntile, done++) {
+          if (w < nsym) {
+            int t = 0, rem = w;
+            while (rem >= npairs - t) {
+              rem -= npairs - t;
+              t++;
+            }
+            flow_sym_tile(f, R, t, t + rem, r, sm);
+          } else {
+            const int v = w - nsym;
+            flow_col_tile(f, R, (v % a.v_tiles) * JS, v / a.v_tiles, r, sm);
+          }
+        }
+        flow_signal(c_tile, (unsigned)done);
+      }
+    }
+    // the sweep's rotation statistics are complete once all of its pair solves are
+    flow_wait(c_inner, (unsigned)(R * npairs));
+    const int rot = __ldcg(a.stats + sweep);
+    const double om = __longlong_as_double((long long)__ldcg(a.offmax + sweep));
+    if (rot == 0 || om <= a.stop_rel) {
+      sweep++;
+      break;
+    }
+  }
+  if (blockIdx.x == 0) {
+    flow_wait(c_tile, (unsigned)(R * nitems));
+    const double* G = f.Gbuf[(R + 1) & 1];  // G_{R-1}
+    for (int i = threadIdx.x; i < a.n_pad; i += blockDim.x)
+      f.diag_out[i] = __ldcg(G + (int64_t)i * a.n_pad + i);
+    if (threadIdx.x == 0) a.sweeps_out[0] = sweep;
+  }
+}
+
 // G <- A zero-padded to n_pad x n_pad; V <- V0 (mv x n, zero-padded to mv_pad x n_pad) or, when
 // V0 is null, the identity.
 __global__ void embed_k(int n, int n_pad, const double* __restrict__ A, double* __restrict__ G,
@@ -571,14 +868,15 @@ __global__ void embed_k(int n, int n_pad, const double* __restrict__ A, double* 
 }
 
 // Sort eigenvalues descending (stable by index) and permute eigenvector columns.
-__global__ void eig_sort_k(int n, int n_pad, int mv, const double* __restrict__ G,
-                           const double* __restrict__ Vp, double* __restrict__ lam,
-                           double* __restrict__ Vout) {
+// (diag[i * dstride]: the eigenvalues — G's diagonal with dstride = n_pad + 1, or a packed copy)
+__global__ void eig_sort_k(int n, int n_pad, int mv, const double* __restrict__ diag,
+                           int64_t dstride, const double* __restrict__ Vp,
+                           double* __restrict__ lam, double* __restrict__ Vout) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double li = G[(int64_t)i * n_pad + i];
+    double li = diag[i * dstride];
     int rank = 0;
     for (int j = 0; j < n; j++) {
-      double lj = G[(int64_t)j * n_pad + j];
+      double lj = diag[j * dstride];
       rank += (lj > li) || (lj == li && j < i);
     }
     lam[rank] = li;
@@ -611,11 +909,18 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   const int mv_pad = ((mv + JS - 1) / JS) * JS;
   const int nb = n_pad / JB;
   const int npairs = nb / 2;
-  DevBuf Gp, Vp, Qb, Sb, scr;
+  // dataflow schedule (jacobi_flow_k): >= 2 pairs, no cluster skip, room for the pair CTAs plus
+  // at least as many tile CTAs
+  const bool flow = ctx->jacobi_flow && npairs >= 2 && !lskip_dev && 2 * npairs <= ctx->num_sms;
+  DevBuf Gp, Vp, Qb, Sb, scr, G2, dg;
   TK_TRY(Gp.get(ctx, (size_t)n_pad * n_pad));
   TK_TRY(Vp.get(ctx, (size_t)std::max(mv_pad, n_pad) * n_pad));
-  TK_TRY(Qb.get(ctx, (size_t)npairs * JS * JS));
-  TK_TRY(Sb.get(ctx, (size_t)npairs * JS * JS));
+  TK_TRY(Qb.get(ctx, (size_t)(flow ? 2 : 1) * npairs * JS * JS));
+  TK_TRY(Sb.get(ctx, (size_t)(flow ? 2 : 1) * npairs * JS * JS));
+  if (flow) {
+    TK_TRY(G2.get(ctx, (size_t)n_pad * n_pad));
+    TK_TRY(dg.get(ctx, (size_t)n_pad + 1));  // diagonal + the two counters
+  }
   TK_TRY(scr.get(ctx, 2 + 2 * (size_t)max_sweeps));
   double* d_maxdiag = scr.p;
   unsigned long long* offmax = (unsigned long long*)(scr.p + 1);
@@ -672,7 +977,28 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
   int grid = std::min(max_grid, std::max(npairs, (rtiles + mv_pad / JS) * npairs));
   grid = std::min(grid, ctx->num_sms);
   int coop = grid > 1 ? 1 : 0;
-  if (coop) {
+  if (flow) {
+    static int flow_grid = -1;
+    if (flow_grid < 0) {
+      cudaFuncSetAttribute(jacobi_flow_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_flow_k, JT, smem);
+      flow_grid = std::max(1, per_sm) * ctx->num_sms;
+    }
+    FlowArgs f;
+    f.a = a;
+    f.Gbuf[0] = G2.p;
+    f.Gbuf[1] = Gp.p;  // embed_k wrote the input here
+    f.cnt = (unsigned int*)(dg.p + n_pad);
+    f.diag_out = dg.p;
+    TK_TRY(tk_zero(ctx, dg.p + n_pad, 1, sizeof(double), sizeof(double)));
+    const int nitems = npairs * (npairs + 1) / 2 + a.v_tiles * npairs;
+    int fgrid = std::min(std::min(flow_grid, ctx->num_sms), npairs + nitems);
+    void* args[] = {&f};
+    TK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)jacobi_flow_k, dim3(fgrid), dim3(JT),
+                                                 args, smem, ctx->stream));
+    ctx->launches++;
+  } else if (coop) {
     void* args[] = {&a, &coop};
     TK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)jacobi_persistent_k, dim3(grid),
                                                  dim3(JT), args, smem, ctx->stream));
@@ -682,7 +1008,8 @@ int tk_jacobi_eig(tk_ctx* ctx, int n, double* A, double* lam, double* V, double 
     TK_LAUNCH_CHECK(ctx);
   }
   int sg = (int)std::min<int64_t>((n + 127) / 128, 4LL * ctx->num_sms);
-  eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, mv, Gp.p, Vp.p, lam, V);
+  eig_sort_k<<<sg, 128, 0, ctx->stream>>>(n, n_pad, mv, flow ? dg.p : Gp.p,
+                                          flow ? 1 : (int64_t)n_pad + 1, Vp.p, lam, V);
   TK_LAUNCH_CHECK(ctx);
   tk_prof_end(ctx, prof_id);
   if (sweeps_out) {

@@ -240,8 +240,8 @@ extern "C" size_t tk_round_workspace_bytes(int64_t n_x, int64_t n_xi, int64_t n_
   const double k2 = std::min((double)R1, N2), r1 = R1, r2 = R2, nx = n_x, nt = n_t;
   const double time_core = 12 * r2 * r2 + 4 * nt * r2 + 2 * nt * nt;
   const double mid = 3 * r1 * N2 + 12 * r1 * r1 + 4 * N2 * r1;
-  const double bond1 = nx * k2 + r1 * r1 + 3 * r1 * k2 + 14 * k2 * k2 + 2 * k2 * N2;
-  const double bond2 = 3 * k2 * n_xi * k3 + 14 * k3 * k3 + 2 * k2 * k3;
+  const double bond1 = nx * k2 + r1 * r1 + 3 * r1 * k2 + 16 * k2 * k2 + 2 * k2 * N2;
+  const double bond2 = 3 * k2 * n_xi * k3 + 16 * k3 * k3 + 2 * k2 * k3;
   const double fused = 2 * r1 * n_xi * r2 + r1 * r1;
   return (size_t)(8.0 * (time_core + mid + bond1 + bond2 + fused)) + ((size_t)1 << 20);
 }
@@ -280,6 +280,17 @@ extern "C" int tk_ctx_set_gemm_feed(tk_ctx* ctx, int mode) {
   }
   TK_ASYNC_GUARD(ctx);
   ctx->gemm_tma = mode;
+  return TK_OK;
+}
+
+extern "C" int tk_ctx_set_jacobi_schedule(tk_ctx* ctx, int mode) {
+  if (!ctx) return TK_EARG;
+  if (mode != 0 && mode != 1) {
+    ctx->err = "tk_ctx_set_jacobi_schedule: mode must be 0 (grid barriers) or 1 (dataflow)";
+    return TK_EARG;
+  }
+  TK_ASYNC_GUARD(ctx);
+  ctx->jacobi_flow = mode;
   return TK_OK;
 }
 

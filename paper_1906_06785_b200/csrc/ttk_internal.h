@@ -61,6 +61,9 @@ struct tk_ctx {
   // operand feed of the big DMMA GEMMs: 1 = TMA tensor tiles (k_gemm_tma.cu, default),
   // 0 = cp.async (k_gemm.cu); tk_ctx_set_gemm_feed
   int gemm_tma = 1;
+  // schedule of the block-Jacobi eigensolver: 1 = dataflow (pair CTAs and tile CTAs one round
+  // apart, no grid barriers; default), 0 = grid barriers (k_jacobi.cu); tk_ctx_set_jacobi_schedule
+  int jacobi_flow = 1;
 };
 // Async mode (async.cu).  drain: wait until the queued jobs ran (returns their first error);
 // submit: queue body() for the worker, ordered after (and gating) the caller's stream.

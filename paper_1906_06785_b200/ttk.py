@@ -29,7 +29,8 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_prec_create_lsc", "tk_prec_destroy", "tk_prec_apply", "tk_prec_operator",
             "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard",
             "tk_ctx_set_async", "tk_sync_ranks", "tk_round_workspace_bytes", "tk_ctx_reserve",
-            "tk_ctx_scratch_high_water", "tk_gemm", "tk_ctx_set_gemm_feed"]
+            "tk_ctx_scratch_high_water", "tk_gemm", "tk_ctx_set_gemm_feed",
+            "tk_ctx_set_jacobi_schedule"]
 
 
 class TkError(RuntimeError):
@@ -113,6 +114,7 @@ def lib():
     L.tk_ctx_scratch_high_water.restype = I64
     L.tk_gemm.argtypes = [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64, I]
     L.tk_ctx_set_gemm_feed.argtypes = [P, I]
+    L.tk_ctx_set_jacobi_schedule.argtypes = [P, I]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
@@ -165,6 +167,10 @@ class Context:
     def set_gemm_feed(self, mode: int):
         """0 = cp.async, 1 = TMA tensor tiles (default) for the heavy DMMA products."""
         self.check(lib().tk_ctx_set_gemm_feed(self._h, int(mode)))
+
+    def set_jacobi_schedule(self, mode: int):
+        """1 = dataflow (default), 0 = grid barriers for the block-Jacobi eigensolver."""
+        self.check(lib().tk_ctx_set_jacobi_schedule(self._h, int(mode)))
 
     def gemm(self, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, M: int, N: int, K: int,
              trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,

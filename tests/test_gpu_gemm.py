@@ -138,3 +138,33 @@ def test_gemm_argument_errors():
         ctx.gemm(A, A, A, 4, 3, 4, sym=True)  # sym needs M == N
     with pytest.raises(ttk.TkError):
         ctx.set_gemm_feed(7)
+
+
+def test_round_bitwise_reproducible_with_tma_feed():
+    """Regression: the TMA-fed reconstruction GEMM runs on the low-priority side stream while the
+    bond-2 chain runs at high priority; without the cross-proxy fence before a stage is released
+    to the TMA a few warp tiles of U1 came out wrong (run-to-run differences of 1e-2).  Rounding
+    the same c3 TT repeatedly must give bitwise identical cores."""
+    from synth.configs import CONFIGS
+    from synth.operator import build_operator
+    from synth.tt import make_input_tt
+
+    cfg = CONFIGS["c3"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    ctx = ttk.Context()
+    ctx.set_gemm_feed(1)
+    gop = ttk.Operator.from_kronsum(op, ctx)
+    y0 = ttk.tt_apply_op(gop, ttk.TT.from_cores(*x))
+    base = [torch.as_tensor(c).clone() for c in (y0.U1, y0.U2, y0.U3)]
+    outs = []
+    for _ in range(6):
+        y = ttk.TT.from_cores(*[b.clone() for b in base])
+        torch.cuda.synchronize()
+        ttk.tt_round(y, cfg.tol, cfg.rmax, ctx=ctx)
+        torch.cuda.synchronize()
+        outs.append((y.ranks, [c.copy() for c in y.cores_numpy()]))
+    for ranks, cores in outs[1:]:
+        assert ranks == outs[0][0]
+        for a, b in zip(cores, outs[0][1]):
+            assert np.array_equal(a, b)
