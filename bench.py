@@ -49,6 +49,11 @@ def parse():
     p.add_argument("--group-space", action="store_true",
                    help="optional exact factor grouping of the space core (SURVEY 8d; reported "
                         "separately, the literal T r growth is the primary line)")
+    p.add_argument("--gemm-feed", type=int, default=1, choices=[0, 1],
+                   help="operand feed of the heavy DMMA products: 1 = TMA tensor tiles (default), "
+                        "0 = cp.async (A/B comparison)")
+    p.add_argument("--jacobi-schedule", type=int, default=1, choices=[0, 1],
+                   help="block-Jacobi schedule: 1 = dataflow (default), 0 = grid barriers")
     return p.parse_args()
 
 
@@ -323,6 +328,8 @@ def run_ours(args, cfg, op, x):
 
     stream = torch.cuda.current_stream()
     ctx = ttk.default_context()
+    ctx.set_gemm_feed(ARGS_GLOBAL.gemm_feed)
+    ctx.set_jacobi_schedule(ARGS_GLOBAL.jacobi_schedule)
     gop = op.gpu_op(ctx)
     groups = gop.group_space(True) if args.group_space else None
     xg = ttk.TT.from_cores(*x)
@@ -644,6 +651,8 @@ def run_gmres(args, cfg, op):
         return
     stream = torch.cuda.current_stream()
     ctx = ttk.default_context()
+    ctx.set_gemm_feed(ARGS_GLOBAL.gemm_feed)
+    ctx.set_jacobi_schedule(ARGS_GLOBAL.jacobi_schedule)
     gop = op.gpu_op(ctx)
     bg = ttk.TT.from_cores(*b)
     steps_k = cfg.gmres_steps
@@ -782,6 +791,8 @@ def run_picard(args, cfg):
                                       "d2h_bytes_per_step": 0}}), flush=True)
         return
     ctx = ttk.default_context()
+    ctx.set_gemm_feed(ARGS_GLOBAL.gemm_feed)
+    ctx.set_jacobi_schedule(ARGS_GLOBAL.jacobi_schedule)
     g_op = ttk.Operator.from_kronsum(op, ctx)
     conv = ttk.Convection(op.n_x, op.n_xi, op.n_t, D, nv, np.array(H), ctx=ctx)
     P = None
@@ -865,8 +876,12 @@ class Workload:
         return self._oracle
 
 
+ARGS_GLOBAL = None
+
+
 def main():
-    args = parse()
+    global ARGS_GLOBAL
+    args = ARGS_GLOBAL = parse()
     from synth.configs import CONFIGS
     from synth.tt import make_input_tt
     cfg = CONFIGS[args.config]

@@ -100,6 +100,115 @@ __device__ __forceinline__ bool needs_rot(double app, double aqq, double apq, do
   return a2 > abs_tol * abs_tol && a2 > rel * rel * fabs(app * aqq);
 }
 
+// Rotation annihilating a_pq: t = sgn(d) e / u with u = |d| + h, h = sqrt(d^2 + e^2),
+// d = a_qq - a_pp, e = 2 a_pq;  c = u / sqrt(u^2 + e^2), s = sgn(d) e / sqrt(u^2 + e^2).
+// Two dependent special functions (h = x rsqrt(x), then rsqrt(u^2 + e^2) with the division
+// e / u in parallel); c^2 + s^2 = 1 to rounding whatever the accuracy of h.
+__device__ __forceinline__ void rot_params(double app, double aqq, double apq, double& c,
+                                           double& sn, double& tt) {
+  const double d = aqq - app, e2 = 2.0 * apq;
+  const double es = d >= 0.0 ? e2 : -e2;
+  const double x = fma(d, d, e2 * e2);
+  const double u = fabs(d) + x * rsqrt(x);
+  const double rn = rsqrt(fma(u, u, e2 * e2));
+  tt = es / u;
+  c = u * rn;
+  sn = es * rn;
+}
+
+// The 32 cross rounds of one pair (p in block I, q in block J): in inner round ir pair k is
+// (p = k, q = 32 + (k + ir) % 32).  Lean version of the generic round below:
+//   * warp 0 computes the 32 rotations and applies them to its own diagonal 2 x 2 blocks at
+//     once (it holds a_pp, a_qq, a_pq, t), so the other threads only see the strictly upper
+//     pair-blocks (P1 < P2): 496 of them, one per thread — warp w owns rows P1 = w (lanes > w)
+//     and P1 = 31 - w (lanes < w) — with fixed p1, p2 and incrementally known q1, q2: no index
+//     loads, and the (p1, p2) element stays in a register for all 32 rounds;
+//   * Q lives in registers: thread (warp w, lane l) holds rows w + 16 m of column l and of
+//     column 32 + (l + ir) % 32; after each round the partner columns move one lane down.
+//   * the largest rotated relative coupling is tracked as a fraction (a_pq^2 / |a_pp a_qq|
+//     compared by cross-multiplication), one division and square root at the end.
+__device__ __forceinline__ void inner_cross(const JacArgs& a, double* S, double* Q, InnerShared& sh,
+                                            double abs_tol, double lsk, int& my_rot,
+                                            double& my_off) {
+  const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+  const bool has_blk = lane != wq;
+  const int P1 = lane > wq ? wq : 31 - wq, P2 = lane > wq ? lane : 31 - lane;
+  double x00 = has_blk ? S[P1 * JLD + P2] : 0.0;
+  double qr_p[4], qr_q[4];
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    qr_p[m] = (wq + 16 * m == lane) ? 1.0 : 0.0;
+    qr_q[m] = (wq + 16 * m == JB + lane) ? 1.0 : 0.0;
+  }
+  double off_num = 0.0, off_den = 1.0;  // warp 0: max of a_pq^2 / |a_pp a_qq| as a fraction
+  for (int ir = 0; ir < JB; ir++) {
+    if (tid < JB) {
+      const int p = tid, q = JB + ((tid + ir) & (JB - 1));
+      const double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
+      double c = 1.0, sn = 0.0;
+      int act = 0;
+      if (needs_rot(app, aqq, apq, abs_tol, a.rel_tol, lsk)) {
+        double tt;
+        rot_params(app, aqq, apq, c, sn, tt);
+        act = 1;
+        S[p * JLD + p] = app - tt * apq;
+        S[q * JLD + q] = aqq + tt * apq;
+        S[p * JLD + q] = 0.0;
+        const double num = apq * apq, den = fmax(fabs(app * aqq), 1e-300);
+        if (num * off_den > off_num * den) {
+          off_num = num;
+          off_den = den;
+        }
+        my_rot++;
+      }
+      sh.rc[tid] = c;
+      sh.rs[tid] = sn;
+      sh.ract[tid] = act;
+    }
+    __syncthreads();
+    {
+      const double c2 = sh.rc[lane], s2 = sh.rs[lane];
+      const int act2 = sh.ract[lane];
+      if (has_blk) {
+        const int actb = sh.ract[P1] | sh.ract[P2];
+        if (actb) {
+          const double c1 = sh.rc[P1], s1 = sh.rs[P1], cb = sh.rc[P2], sb = sh.rs[P2];
+          const int q1 = JB + ((P1 + ir) & (JB - 1)), q2 = JB + ((P2 + ir) & (JB - 1));
+          const int i01 = P1 * JLD + q2, i10 = P2 * JLD + q1;
+          const int i11 = q1 <= q2 ? q1 * JLD + q2 : q2 * JLD + q1;
+          const double x01 = S[i01], x10 = S[i10], x11 = S[i11];
+          const double y00 = cb * x00 - sb * x01, y01 = sb * x00 + cb * x01;
+          const double y10 = cb * x10 - sb * x11, y11 = sb * x10 + cb * x11;
+          x00 = c1 * y00 - s1 * y10;
+          S[i10] = s1 * y00 + c1 * y10;
+          S[i01] = c1 * y01 - s1 * y11;
+          S[i11] = s1 * y01 + c1 * y11;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; m++) {
+        if (act2) {
+          const double qp = qr_p[m], qq = qr_q[m];
+          qr_p[m] = c2 * qp - s2 * qq;
+          qr_q[m] = s2 * qp + c2 * qq;
+        }
+        qr_q[m] = __shfl_sync(0xffffffffu, qr_q[m], (lane + 1) & 31);
+      }
+    }
+    __syncthreads();
+  }
+  if (has_blk) S[P1 * JLD + P2] = x00;
+  // after JB rounds lane l holds column JB + l again
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    const int i = wq + 16 * m;
+    Q[i * JLD + lane] = qr_p[m];
+    Q[i * JLD + JB + lane] = qr_q[m];
+  }
+  if (tid < JB) my_off = fmax(my_off, sqrt(off_num / off_den));
+  __syncthreads();
+}
+
 // One pair's inner problem, by one CTA (JT = 512 threads).  Per inner round: (a) warp 0
 // computes the 32 disjoint rotations; (b) every thread applies J^T S J to two 2x2 blocks
 // (rows of one pair x columns of another: each element belongs to exactly one block, so the
@@ -146,154 +255,102 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
       return;
     }
   }
-  long long pa_sum = 0, pb_sum = 0, t_a = 0;
   int my_rot = 0;          // warp 0 lanes: rotations applied (this call)
   double my_off = 0.0;     // warp 0 lanes: largest relative coupling rotated away
   // The first outer round of a sweep (r == 0, every block appears once) runs the full
   // 63-round inner sweep; later rounds only rotate the 32 x 32 cross pairs (i in I, j in J):
   // 32 inner rounds of 32 disjoint pairs.  Every index pair is still visited once per sweep.
   const bool cross = (r != 0) && (a.npairs > 1);
-  // Cross rounds keep Q in registers: thread (warp w, lane l) holds rows w + 16 m of column
-  // l (qr_p) and of column 32 + (l + ir) % 32 (qr_q), the partner of l in inner round ir; after
-  // each round the partner columns move one lane down (a shuffle), so Q never touches shared
-  // memory until the end (it was half of the update phase's shared-memory traffic).
   const int lane = tid & 31, wq = tid >> 5;
-  double qr_p[4], qr_q[4];
-#pragma unroll
-  for (int m = 0; m < 4; m++) {
-    qr_p[m] = (wq + 16 * m == lane) ? 1.0 : 0.0;
-    qr_q[m] = (wq + 16 * m == JB + lane) ? 1.0 : 0.0;
-  }
-  for (int sweep = 0; sweep < a.max_inner; sweep++) {
-    int sweep_rot = 0;
-    const int nrounds = cross ? JB : JS - 1;
-    for (int ir = 0; ir < nrounds; ir++) {
-      if (tid == 0) t_a = clock64();
-      if (tid < JB) {
-        const int k = tid;
-        int p, q;
-        if (cross) {
-          p = k;
-          q = JB + (k + ir) % JB;
-        } else {
-          const int pa = rr_player(k, ir, JS), pb = rr_player(JS - 1 - k, ir, JS);
-          p = min(pa, pb);
-          q = max(pa, pb);
-        }
-        const double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
-        double c = 1.0, sn = 0.0, tt = 0.0;
-        int act = 0;
-        if (needs_rot(app, aqq, apq, abs_tol, a.rel_tol, lsk)) {
-          // t = sgn(d) e / u with u = |d| + sqrt(d^2 + e^2),  d = a_qq - a_pp, e = 2 a_pq;
-          // c = u / sqrt(u^2 + e^2), s = sgn(d) e / sqrt(u^2 + e^2): two dependent special
-          // functions (sqrt, then rsqrt and the division in parallel)
-          const double d = aqq - app, e2 = 2.0 * apq;
-          const double es = d >= 0.0 ? e2 : -e2;
-          const double u = fabs(d) + sqrt(fma(d, d, e2 * e2));
-          const double rn = rsqrt(fma(u, u, e2 * e2));
-          tt = es / u;
-          c = u * rn;
-          sn = es * rn;
-          act = 1;
-        }
-        sh.rc[k] = c;
-        sh.rs[k] = sn;
-        sh.rt[k] = tt;
-        sh.rapp[k] = app;
-        sh.raqq[k] = aqq;
-        sh.rapq[k] = apq;
-        sh.rp[k] = p;
-        sh.rq[k] = q;
-        sh.ract[k] = act;
-        sweep_rot += act;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        long long now = clock64();
-        pa_sum += now - t_a;
-        t_a = now;
-      }
-      // S <- J^T S J on 2x2 blocks (pair P1 rows, pair P2 cols) and Q <- Q J.  Only the upper
-      // triangle of S is kept (uidx): block (P1, P2) for P1 <= P2 covers each element once, and
-      // half the shared-memory traffic of the full two-sided update goes away.
-      // Thread map: P2 = lane (parameters loaded once), P1 = warp and warp + 16; Q rows
-      // warp + 16 m (m < 4) of pair lane.
-      {
-        const double c2 = sh.rc[lane], s2 = sh.rs[lane];
-        const int p2 = sh.rp[lane], q2 = sh.rq[lane], act2 = sh.ract[lane];
-        // largest relative coupling rotated away (off the parameter phase's critical path)
-        if (wq == 0 && act2)
-          my_off = fmax(my_off, fabs(sh.rapq[lane]) *
-                                    rsqrt(fmax(fabs(sh.rapp[lane] * sh.raqq[lane]), 1e-300)));
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int P1 = wq + 16 * h;
-          if (P1 > lane) continue;
-          const int act1 = sh.ract[P1];
-          if (!act1 && !act2) continue;
-          const int p1 = sh.rp[P1], q1 = sh.rq[P1];
-          if (P1 == lane) {
-            const double t1 = sh.rt[P1], a1 = sh.rapq[P1];
-            S[p1 * JLD + p1] = sh.rapp[P1] - t1 * a1;
-            S[q1 * JLD + q1] = sh.raqq[P1] + t1 * a1;
-            S[p1 * JLD + q1] = 0.0;  // p1 < q1
-            continue;
-          }
-          const double c1 = sh.rc[P1], s1 = sh.rs[P1];
-          const int i00 = uidx(p1, p2), i01 = uidx(p1, q2), i10 = uidx(q1, p2), i11 = uidx(q1, q2);
-          const double x00 = S[i00], x01 = S[i01], x10 = S[i10], x11 = S[i11];
-          const double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
-          const double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
-          S[i00] = c1 * y00 - s1 * y10;
-          S[i10] = s1 * y00 + c1 * y10;
-          S[i01] = c1 * y01 - s1 * y11;
-          S[i11] = s1 * y01 + c1 * y11;
-        }
-        if (cross) {
-#pragma unroll
-          for (int m = 0; m < 4; m++) {
-            if (act2) {
-              const double qp = qr_p[m], qq = qr_q[m];
-              qr_p[m] = c2 * qp - s2 * qq;
-              qr_q[m] = s2 * qp + c2 * qq;
-            }
-            qr_q[m] = __shfl_sync(0xffffffffu, qr_q[m], (lane + 1) & 31);
-          }
-        } else if (act2) {
-#pragma unroll
-          for (int m = 0; m < 4; m++) {
-            const int i = wq + 16 * m;
-            const double qp = Q[i * JLD + p2], qq = Q[i * JLD + q2];
-            Q[i * JLD + p2] = c2 * qp - s2 * qq;
-            Q[i * JLD + q2] = s2 * qp + c2 * qq;
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) pb_sum += clock64() - t_a;
-    }
-    // inner convergence (only matters when max_inner > 1)
-    if (tid < JB) {
-      int v = sweep_rot;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (tid == 0) sh.nrot = v;
-      my_rot += sweep_rot;
-    }
-    __syncthreads();
-    const bool done = (sh.nrot == 0);
-    __syncthreads();
-    if (done) break;
-  }
   if (cross) {
-    // after JB rounds lane l holds column JB + l again
+    inner_cross(a, S, Q, sh, abs_tol, lsk, my_rot, my_off);
+  } else {
+    for (int sweep = 0; sweep < a.max_inner; sweep++) {
+      int sweep_rot = 0;
+      for (int ir = 0; ir < JS - 1; ir++) {
+        if (tid < JB) {
+          const int k = tid;
+          const int pa = rr_player(k, ir, JS), pb = rr_player(JS - 1 - k, ir, JS);
+          const int p = min(pa, pb), q = max(pa, pb);
+          const double app = S[p * JLD + p], aqq = S[q * JLD + q], apq = S[p * JLD + q];
+          double c = 1.0, sn = 0.0, tt = 0.0;
+          int act = 0;
+          if (needs_rot(app, aqq, apq, abs_tol, a.rel_tol, lsk)) {
+            rot_params(app, aqq, apq, c, sn, tt);
+            act = 1;
+          }
+          sh.rc[k] = c;
+          sh.rs[k] = sn;
+          sh.rt[k] = tt;
+          sh.rapp[k] = app;
+          sh.raqq[k] = aqq;
+          sh.rapq[k] = apq;
+          sh.rp[k] = p;
+          sh.rq[k] = q;
+          sh.ract[k] = act;
+          sweep_rot += act;
+        }
+        __syncthreads();
+        // S <- J^T S J on 2x2 blocks (pair P1 rows, pair P2 cols) and Q <- Q J.  Only the upper
+        // triangle of S is kept (uidx): block (P1, P2) for P1 <= P2 covers each element once.
+        // Thread map: P2 = lane (parameters loaded once), P1 = warp and warp + 16; Q rows
+        // warp + 16 m (m < 4) of pair lane.
+        {
+          const double c2 = sh.rc[lane], s2 = sh.rs[lane];
+          const int p2 = sh.rp[lane], q2 = sh.rq[lane], act2 = sh.ract[lane];
+          if (wq == 0 && act2)
+            my_off = fmax(my_off, fabs(sh.rapq[lane]) *
+                                      rsqrt(fmax(fabs(sh.rapp[lane] * sh.raqq[lane]), 1e-300)));
 #pragma unroll
-    for (int m = 0; m < 4; m++) {
-      const int i = wq + 16 * m;
-      Q[i * JLD + lane] = qr_p[m];
-      Q[i * JLD + JB + lane] = qr_q[m];
+          for (int h = 0; h < 2; h++) {
+            const int P1 = wq + 16 * h;
+            if (P1 > lane) continue;
+            const int act1 = sh.ract[P1];
+            if (!act1 && !act2) continue;
+            const int p1 = sh.rp[P1], q1 = sh.rq[P1];
+            if (P1 == lane) {
+              const double t1 = sh.rt[P1], a1 = sh.rapq[P1];
+              S[p1 * JLD + p1] = sh.rapp[P1] - t1 * a1;
+              S[q1 * JLD + q1] = sh.raqq[P1] + t1 * a1;
+              S[p1 * JLD + q1] = 0.0;  // p1 < q1
+              continue;
+            }
+            const double c1 = sh.rc[P1], s1 = sh.rs[P1];
+            const int i00 = uidx(p1, p2), i01 = uidx(p1, q2), i10 = uidx(q1, p2),
+                      i11 = uidx(q1, q2);
+            const double x00 = S[i00], x01 = S[i01], x10 = S[i10], x11 = S[i11];
+            const double y00 = c2 * x00 - s2 * x01, y01 = s2 * x00 + c2 * x01;
+            const double y10 = c2 * x10 - s2 * x11, y11 = s2 * x10 + c2 * x11;
+            S[i00] = c1 * y00 - s1 * y10;
+            S[i10] = s1 * y00 + c1 * y10;
+            S[i01] = c1 * y01 - s1 * y11;
+            S[i11] = s1 * y01 + c1 * y11;
+          }
+          if (act2) {
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+              const int i = wq + 16 * m;
+              const double qp = Q[i * JLD + p2], qq = Q[i * JLD + q2];
+              Q[i * JLD + p2] = c2 * qp - s2 * qq;
+              Q[i * JLD + q2] = s2 * qp + c2 * qq;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      // inner convergence (only matters when max_inner > 1)
+      if (tid < JB) {
+        int v = sweep_rot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tid == 0) sh.nrot = v;
+        my_rot += sweep_rot;
+      }
+      __syncthreads();
+      const bool done = (sh.nrot == 0);
+      __syncthreads();
+      if (done) break;
     }
-    __syncthreads();
   }
   double* Qo = Qout + (int64_t)t * JS * JS;
   double* So = Sout + (int64_t)t * JS * JS;
@@ -308,10 +365,6 @@ __device__ void inner_solve(const JacArgs& a, int t, int r, double* sm, InnerSha
     for (int w = 16; w > 0; w >>= 1) {
       v += __shfl_xor_sync(0xffffffffu, v, w);
       o = fmax(o, __shfl_xor_sync(0xffffffffu, o, w));
-    }
-    if (tid == 0 && a.tstamp && t == 0) {
-      a.tstamp[6] += pa_sum;
-      a.tstamp[7] += pb_sum;
     }
     if (tid == 0 && v) {
       atomicAdd(a.stats, v);
@@ -330,32 +383,40 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
       : "d"(a), "d"(b));
 }
 
-// acc (this warp's 16 x 16 block of C = op(A) B, 64 x 64 x 64, A/B in shared memory with
-// leading dimension TLD; transA: op(A)[m][k] = A[k][m]).  16 warps cover the 64 x 64 C.
-__device__ __forceinline__ void tile_mma(const double* As, bool transA, const double* Bs,
-                                         double acc[2][2][2]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
+// acc <- this warp's (8 FI) x (8 FJ) block at (wm, wn) of C = op(A) B (64 x 64 x 64, A / B in
+// shared memory with leading dimension TLD; transA: op(A)[m][k] = A[k][m]).  An output element is
+// the same chain of k-steps whatever FI, FJ and the warp map: sub-block products are bitwise
+// equal to the corresponding entries of the full product.
+template <int FI, int FJ>
+__device__ __forceinline__ void tile_mma_at(const double* As, bool transA, const double* Bs,
+                                            double acc[FI][FJ][2], int wm, int wn) {
+  const int lane = threadIdx.x & 31;
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < FI; i++)
 #pragma unroll
-    for (int j = 0; j < 2; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll 4
   for (int k = 0; k < JS; k += 4) {
-    double av[2], bv[2];
+    double av[FI], bv[FJ];
 #pragma unroll
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < FI; i++) {
       const int m = wm + 8 * i + lr, kk = k + lc;
       av[i] = transA ? As[kk * TLD + m] : As[m * TLD + kk];
     }
 #pragma unroll
-    for (int j = 0; j < 2; j++) bv[j] = Bs[(k + lc) * TLD + wn + 8 * j + lr];
+    for (int j = 0; j < FJ; j++) bv[j] = Bs[(k + lc) * TLD + wn + 8 * j + lr];
 #pragma unroll
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < FI; i++)
 #pragma unroll
-      for (int j = 0; j < 2; j++) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      for (int j = 0; j < FJ; j++) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
   }
+}
+// the full 64 x 64 product: 16 warps, each a 16 x 16 block
+__device__ __forceinline__ void tile_mma(const double* As, bool transA, const double* Bs,
+                                         double acc[2][2][2]) {
+  const int warp = threadIdx.x >> 5;
+  tile_mma_at<2, 2>(As, transA, Bs, acc, (warp >> 2) * 16, (warp & 3) * 16);
 }
 
 // 64-row tile of M[:, I u J] <- M[:, I u J] Q   (DMMA)
@@ -607,21 +668,19 @@ __device__ __forceinline__ void flow_signal(unsigned int* c, unsigned int inc) {
   }
 }
 
-// slot and half (0: rows 0..31 of the pair, 1: rows 32..63) of block B in tournament round r
-__device__ __forceinline__ void find_block(int B, int r, int nb, int npairs, int& slot, int& half) {
-  slot = 0;
-  half = 0;
-  for (int t = 0; t < npairs; t++) {
-    int I, J;
-    pair_blocks(t, r, nb, I, J);
-    if (I == B) {
-      slot = t;
-      half = 0;
-    } else if (J == B) {
-      slot = t;
-      half = 1;
-    }
+// slot and half (0: rows 0..31 of the pair, 1: rows 32..63) of block B in tournament round r:
+// the inverse of rr_player (position of B), its partner sits at position nb - 1 - pos
+__device__ __forceinline__ void find_block(int B, int r, int nb, int& slot, int& half) {
+  const int ne1 = nb - 1;
+  int pos = 0;
+  if (B != 0) {
+    int d = (B - 1 - r) % ne1;
+    if (d < 0) d += ne1;
+    pos = 1 + d;
   }
+  const int ppos = nb - 1 - pos;
+  slot = min(pos, ppos);
+  half = B < rr_player(ppos, r, nb) ? 0 : 1;
 }
 
 // Two-sided tile product shared by the tile phase and the pair CTAs' input construction:
@@ -743,8 +802,8 @@ __device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double*
   }
   const int rp = (r + nrounds - 1) % nrounds;
   int ta, ha, tb, hb;
-  find_block(I, rp, a.nb, a.npairs, ta, ha);
-  find_block(J, rp, a.nb, a.npairs, tb, hb);
+  find_block(I, rp, a.nb, ta, ha);
+  find_block(J, rp, a.nb, tb, hb);
   int Ia, Ja, Ib, Jb;
   pair_blocks(ta, rp, a.nb, Ia, Ja);
   pair_blocks(tb, rp, a.nb, Ib, Jb);
@@ -753,14 +812,42 @@ __device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double*
   const double* Qbb = a.Qb + qoff + (int64_t)tb * JS * JS;
   const double* Sa = a.Sb + qoff + (int64_t)ta * JS * JS;
   const double* Sbb = a.Sb + qoff + (int64_t)tb * JS * JS;
-  // coupling block: the tile phase computes item (min, max) of the two slots and mirrors it;
-  // use the same orientation so the values are bitwise the tile phase's
-  double acc[2][2][2];
+  // coupling block: the tile phase computes item (min, max) of the two slots, Y = Q_t^T (X Q_s)
+  // with X = G_{R-2}[IJ_t, IJ_s], and mirrors it; only the (hr, hc) quarter of Y is needed —
+  // the 32 columns hc of X Q_s (16 warps x (16 x 8)), then the 32 x 32 quarter of Q_t^T (.)
+  // (16 warps x (8 x 8)): the same k-chains as the tile phase, so the values are bitwise its.
   const bool ab = ta < tb;
-  if (ab)
-    two_sided_tile(f.Gbuf[R & 1], n_pad, Qa, Qbb, Ia, Ja, Ib, Jb, sm, acc);
-  else
-    two_sided_tile(f.Gbuf[R & 1], n_pad, Qbb, Qa, Ib, Jb, Ia, Ja, sm, acc);
+  const int It = ab ? Ia : Ib, Jt = ab ? Ja : Jb, Is = ab ? Ib : Ia, Js = ab ? Jb : Ja;
+  const double* Qtg = ab ? Qa : Qbb;
+  const double* Qsg = ab ? Qbb : Qa;
+  const int hr = ab ? ha : hb, hc = ab ? hb : ha;  // wanted half of the rows / columns of Y
+  const double* Gin = f.Gbuf[R & 1];
+  double* Qs = sm;
+  double* Xs = sm + JS * TLD;
+  double* Qt = sm + 2 * JS * TLD;
+  for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+    const int i = e / JS, j = e % JS;
+    Qs[i * TLD + j] = __ldcg(Qsg + e);
+    Qt[i * TLD + j] = __ldcg(Qtg + e);
+    Xs[i * TLD + j] = __ldcg(Gin + (int64_t)gidx(i, It, Jt) * n_pad + gidx(j, Is, Js));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    double acc1[2][1][2];
+    const int wm = (warp >> 2) * 16, wn = hc * JB + (warp & 3) * 8;
+    tile_mma_at<2, 1>(Xs, false, Qs, acc1, wm, wn);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        Xs[(wm + 8 * i + (lane >> 2)) * TLD + wn + 2 * (lane & 3) + h] = acc1[i][0][h];
+    __syncthreads();
+  }
+  double acc[1][1][2];
+  const int wm = hr * JB + (warp >> 2) * 8, wn = hc * JB + (warp & 3) * 8;
+  tile_mma_at<1, 1>(Qt, true, Xs, acc, wm, wn);
   __syncthreads();  // tiles consumed: S / Q alias them
   for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
     const int i = e / JS, j = e % JS;
@@ -770,23 +857,14 @@ __device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double*
     else if (i >= JB && j >= JB)
       S[i * JLD + j] = __ldcg(Sbb + (hb * JB + i - JB) * JS + hb * JB + j - JB);
   }
-  // acc holds Y[m][n]: rows = slot min(ta, tb)'s pair, cols = the other's
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;
-  const int hr = ab ? ha : hb, hc = ab ? hb : ha;  // wanted half of the rows / columns of Y
+  // Y rows belong to slot min(ta, tb)'s pair: to I when ab, else to J
 #pragma unroll
-  for (int i = 0; i < 2; i++)
-#pragma unroll
-    for (int j = 0; j < 2; j++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int m = wm + 8 * i + (lane >> 2), n = wn + 8 * j + 2 * (lane & 3) + h;
-        if ((m >> 5) != hr || (n >> 5) != hc) continue;
-        // Y rows belong to I when ab, else to J
-        const int li = ab ? (m & 31) : (n & 31), lj = ab ? (n & 31) : (m & 31);
-        S[li * JLD + JB + lj] = acc[i][j][h];
-        S[(JB + lj) * JLD + li] = acc[i][j][h];
-      }
+  for (int h = 0; h < 2; h++) {
+    const int m = wm + (lane >> 2), n = wn + 2 * (lane & 3) + h;
+    const int li = ab ? (m & 31) : (n & 31), lj = ab ? (n & 31) : (m & 31);
+    S[li * JLD + JB + lj] = acc[0][0][h];
+    S[(JB + lj) * JLD + li] = acc[0][0][h];
+  }
 }
 
 __global__ void __launch_bounds__(JT) jacobi_flow_k(FlowArgs f) {
