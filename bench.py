@@ -379,7 +379,8 @@ def run_ours(args, cfg, op, x):
     for ln in buf.value.decode().splitlines():
         cat, ms, fl, by = ln.split()[:4]
         kn = {"spmm_multi": "spmm_merged_k", "stoch_apply": "stoch_apply_k",
-              "time_apply": "time_apply_k"}.get(cat, "dgemm_kernel")
+              "time_apply": "time_apply_k"}.get(
+                  cat, "dgemm_tma_kernel" if args.gemm_feed else "dgemm_kernel")
         d = heavy.setdefault(kn, [0, 0.0, 0.0, 0.0])
         d[0] += 1
         d[1] += float(ms)
@@ -406,13 +407,18 @@ def run_ours(args, cfg, op, x):
     fp64_peak = DMMA_PEAK["tflops"]
     # group the phase records by KERNEL FUNCTION: every phase tag that is not one of the
     # named kernels below is a launch of the DMMA GEMM (dgemm_kernel + its split-K reduce)
-    named = {"jacobi": "jacobi_persistent_k", "qr_panel": "qr_panel_warp_k",
-             "qr_reflector": "apply_reflector_k", "pchol_panel": "pchol_panel_k",
+    # (kernel names as in the ncu launch list, profiles/r02/launches_c4_r2*.csv; the heavy DMMA
+    # products run the TMA-fed dgemm_tma_kernel, the light ones and the 128 x 80 tile of form_U1
+    # the cp.async dgemm_kernel)
+    gemm_name = "dgemm_tma_kernel" if args.gemm_feed else "dgemm_kernel"
+    named = {"jacobi": "jacobi_flow_k" if args.jacobi_schedule else "jacobi_persistent_k",
+             "qr_panel": "qr_panel_reg_k",
+             "qr_reflector": "apply_reflector_k", "pchol_panel": "pchol_panel_reg_k",
              "spmm_multi": "spmm_merged_k", "stoch_apply": "stoch_apply_k",
              "time_apply": "time_apply_k"}
     kernels = {}
     for cat, v in phases.items():
-        kn = named.get(cat, "dgemm_kernel")
+        kn = named.get(cat, gemm_name)
         d = kernels.setdefault(kn, [0, 0.0, 0.0, 0.0])
         for i in range(4):
             d[i] += v[i]

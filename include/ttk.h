@@ -116,7 +116,7 @@ int64_t tk_ctx_scratch_high_water(tk_ctx* ctx, int reset);
  * Asynchronous on the context stream; split-K partial sums are reduced in a fixed order, so
  * results are bitwise reproducible run to run (per feed).  Errors: TK_EARG (null pointer,
  * sym with M != N, K == 0 with beta != 0), TK_ECUDA.
- * tk_ctx_set_gemm_feed: how the heavy products (>= 2e8 flops, beta == 0) get their operand
+ * tk_ctx_set_gemm_feed: how the heavy products (>= 1e8 flops, beta == 0) get their operand
  * tiles: 1 = TMA tensor tiles (cp.async.bulk.tensor + mbarrier, 128B-swizzled shared memory;
  * default), 0 = cp.async.  Operands that are not 16-byte aligned or have an odd leading
  * dimension always take the cp.async kernel.  Both feeds compute the same sums in a different

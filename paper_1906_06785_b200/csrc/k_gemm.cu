@@ -443,12 +443,30 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
         &per_sm, dgemm_kernel<64, 64, 2, 2, true, true, true, false>, NT, smem);
     per_sm = std::max(per_sm, 1);
   }
-  const int mult = 4;
+  // heavy products with beta == 0: the TMA-fed kernel (same tile, same split-K partials)
+  const double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
+  const bool use_tma = ctx->gemm_tma && cfg == 0 && beta == 0.0 && !triu_b && flops >= 1e8 &&
+                       tk_dgemm_tma_eligible(transA, transB, M, N, K, A, lda, B, ldb);
+  // Waves of resident CTAs.  cp.async kernel: 4 (time-optimal, above).  TMA kernel: 12 — shorter
+  // K chunks keep the CTAs that share operand columns (the 10 tiles of a Gram's column block)
+  // within an L2-sized window of each other: gram_W (640 x 640 x 786432) DRAM reads 10.8 GB at
+  // 4 waves, 6.2 at 8, 5.5 at 12, 5.2 at 16 (4.03 algorithmic) and 10.19 / 10.02 / 10.00 / 9.97 ms
+  // including the reduction of the partials, which grows with the split count.
+  const int mult = use_tma ? 12 : 4;
   const int64_t slots = (int64_t)per_sm * ctx->num_sms * mult;
   int64_t splits = 1;
   if (cfg == 0 && tiles < slots && K >= 8 * BK) {
     splits = std::min<int64_t>(std::max<int64_t>(slots / tiles, 1), (K + 8 * BK - 1) / (8 * BK));
     splits = std::max<int64_t>(splits, 1);
+    if (use_tma) {
+      // the partial sums (written and re-read once) stay below 1/8 of the operand bytes (and
+      // 64 MB): bounds the scratch and the extra traffic of the higher split count
+      const double opb = 8.0 * ((double)M * K + (sym ? 0.0 : (double)K * N));
+      const double cap = std::max(64.0 * 1048576.0, opb / 8.0);
+      const int64_t smax = std::max<int64_t>((int64_t)(cap / (8.0 * M * N)), 1);
+      const int64_t s4 = std::max<int64_t>(slots / (3 * tiles), 1);  // the 4-wave count
+      splits = std::max(std::min(splits, smax), std::min(splits, s4));
+    }
   }
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = ((kchunk + BK - 1) / BK) * BK;
@@ -460,19 +478,16 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
     partial = pbuf.p;
   }
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
-  double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
+  double pflops = flops;
   if (triu_b)
-    flops = K >= N ? (double)M * N * (N + 1) : 2.0 * M * (K * (K + 1) / 2.0 + (double)(N - K) * K);
+    pflops = K >= N ? (double)M * N * (N + 1) : 2.0 * M * (K * (K + 1) / 2.0 + (double)(N - K) * K);
   const double bytes = 8.0 * ((double)M * K + (sym ? 0.0 : (double)K * N) + (double)M * N);
-  const int prof_id = tk_prof_begin(ctx, ctx->tag, flops, bytes);
+  const int prof_id = tk_prof_begin(ctx, ctx->tag, pflops, bytes);
   const bool AK = transA, BKm = !transB;
   // 16-byte vector path: contiguous dims even and 16-byte aligned bases
   bool v2 = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
             (((uintptr_t)B & 15) == 0);
   int st = TK_OK;
-  // heavy products with beta == 0: the TMA-fed kernel (same tile, same split-K partials)
-  const bool use_tma = ctx->gemm_tma && cfg == 0 && beta == 0.0 && !triu_b && flops >= 2e8 &&
-                       tk_dgemm_tma_eligible(transA, transB, M, N, K, A, lda, B, ldb);
   if (use_tma) {
     st = tk_dgemm_tma_launch(ctx, transA, transB, M, N, K, alpha, A, lda, B, ldb, C, ldc, kchunk,
                              (int)splits, sym ? 1 : 0, partial, skip);

@@ -782,8 +782,10 @@ __device__ void flow_col_tile(const FlowArgs& f, int R, int row0, int t, int r, 
   __syncthreads();
 }
 
-// Stage the pair's input block S = G_{R-1}[I u J, I u J] and Q = I in shared memory.
-__device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double* sm) {
+// Stage the pair's input block S = G_{R-1}[I u J, I u J] and Q = I in shared memory.  For R >= 1
+// in two parts: part 0 (needs only tile phase R-2) loads the G_{R-2} block — issued before the
+// wait for the pair solves of round R-1, whose imbalance hides its latency; part 1 the rest.
+__device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double* sm, int part) {
   const JacArgs& a = f.a;
   const int n_pad = a.n_pad, nrounds = a.nb - 1;
   double* S = sm;
@@ -791,6 +793,7 @@ __device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double*
   int I, J;
   pair_blocks(t, r, a.nb, I, J);
   if (R == 0) {
+    if (part == 0) return;
     const double* G = f.Gbuf[1];
     for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
       int i = e / JS, j = e % JS;
@@ -825,11 +828,17 @@ __device__ void flow_stage_input(const FlowArgs& f, int R, int t, int r, double*
   double* Qs = sm;
   double* Xs = sm + JS * TLD;
   double* Qt = sm + 2 * JS * TLD;
+  if (part == 0) {
+    for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
+      const int i = e / JS, j = e % JS;
+      Xs[i * TLD + j] = __ldcg(Gin + (int64_t)gidx(i, It, Jt) * n_pad + gidx(j, Is, Js));
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < JS * JS; e += blockDim.x) {
     const int i = e / JS, j = e % JS;
     Qs[i * TLD + j] = __ldcg(Qsg + e);
     Qt[i * TLD + j] = __ldcg(Qtg + e);
-    Xs[i * TLD + j] = __ldcg(Gin + (int64_t)gidx(i, It, Jt) * n_pad + gidx(j, Is, Js));
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -887,9 +896,10 @@ __global__ void __launch_bounds__(JT) jacobi_flow_k(FlowArgs f) {
     as.offmax = a.offmax + sweep;
     for (int r = 0; r < nrounds; r++, R++) {
       if (is_inner) {
-        flow_wait(c_inner, (unsigned)(R * npairs));                   // Q, S of round R - 1
         if (R >= 2) flow_wait(c_tile, (unsigned)((R - 1) * nitems));  // G_{R-2} complete
-        flow_stage_input(f, R, blockIdx.x, r, sm);
+        flow_stage_input(f, R, blockIdx.x, r, sm, 0);
+        flow_wait(c_inner, (unsigned)(R * npairs));                   // Q, S of round R - 1
+        flow_stage_input(f, R, blockIdx.x, r, sm, 1);
         const int64_t qoff = (int64_t)(R & 1) * npairs * JS * JS;
         inner_solve(as, blockIdx.x, r, sm, sh, abs_tol, -1.0, true, a.Qb + qoff, a.Sb + qoff);
         flow_signal(c_inner, 1);

@@ -643,19 +643,23 @@ __global__ void __launch_bounds__(32 * QB)
   stamp(4);
 }
 
-// Tall-panel variant of qr_panel_reg_k for 32 * MAXR < m <= BIG_M (the pass-1 QR of the
-// c5 / c6 Grams, k ~ 1300-2300): warp j holds rows [0, 32 MAXR) of column j in registers and the
-// rows beyond in a per-column shared-memory overflow region, so the panel is factored by one
-// CTA without global-memory round trips (the former fallback, qr_panel_k<false> working in
-// global memory, took ~460 us per 16-column panel at m = 2240).  Same contract as
-// qr_panel_k<false>: the panel (m x jb, ld ldg, already updated by the previous reflectors)
-// in, V (m x QB, unit lower trapezoidal, zero padded) and T (QB x QB) out; VT / VT^T are formed
-// by the caller.  Dynamic smem: QB x (BIG_M - 32 MAXR) doubles.
+// Tall-panel variant of qr_panel_reg_k for m > 32 * MAXR (the pass-1 QR of the c5 / c6 Grams,
+// k ~ 1300-2800): warp j holds rows [0, 32 MAXR) of column j in registers, rows [32 MAXR, BIG_M)
+// in a per-column shared-memory overflow region and — only when m > BIG_M — the rows beyond in
+// a global-memory tail (gtail: QB columns of mt = m - BIG_M rows, column-major, then two
+// reflector tails of mt rows; L2-resident, a fraction of the panel), so the panel is factored by
+// one CTA (the former fallback, qr_panel_k<false> working entirely in global memory, took
+// ~460 us per 16-column panel at m = 2240).  Same contract as qr_panel_k<false>: the panel
+// (m x jb, ld ldg, already updated by the previous reflectors) in, V (m x QB, unit lower
+// trapezoidal, zero padded) and T (QB x QB) out; VT / VT^T are formed by the caller.  Dynamic
+// smem: QB x (BIG_M - 32 MAXR) doubles.
 constexpr int BIG_M = 2256;
+constexpr int kBigTail = 4096;  // rows beyond BIG_M the tall kernel keeps in global memory
 template <int MAXR>
 __global__ void __launch_bounds__(32 * QB)
     qr_panel_big_k(int m, int jb, const double* __restrict__ Pg, int64_t ldg,
-                   double* __restrict__ Vout, double* __restrict__ Tout) {
+                   double* __restrict__ Vout, double* __restrict__ Tout,
+                   double* __restrict__ gtail) {
   constexpr int MR = 32 * MAXR;
   constexpr int OVL = BIG_M - MR;  // overflow rows per column
   __shared__ double vbuf[2][BIG_M];
@@ -663,26 +667,33 @@ __global__ void __launch_bounds__(32 * QB)
   __shared__ double Ts[QB][QB + 1];
   extern __shared__ double ov_all[];
   const int tid = threadIdx.x, lane = tid & 31, j = tid >> 5;
+  const int ms = min(m, BIG_M);        // rows held on chip
+  const int mt = m - ms;               // rows in the global tail (0 unless m > BIG_M)
   double* ov = ov_all + (size_t)j * OVL;  // rows MR.. of column j
+  double* gc = gtail + (size_t)j * mt;    // rows BIG_M.. of column j
+  double* gv0 = gtail + (size_t)QB * mt;  // reflector tails, two buffers
   double c[MAXR];
 #pragma unroll
   for (int k = 0; k < MAXR; k++) {
     const int i = lane + 32 * k;
     c[k] = (i < m && j < jb) ? Pg[(int64_t)i * ldg + j] : 0.0;
   }
-  for (int i = MR + lane; i < m; i += 32) ov[i - MR] = j < jb ? Pg[(int64_t)i * ldg + j] : 0.0;
+  for (int i = MR + lane; i < ms; i += 32) ov[i - MR] = j < jb ? Pg[(int64_t)i * ldg + j] : 0.0;
+  for (int i = lane; i < mt; i += 32) gc[i] = j < jb ? Pg[(int64_t)(BIG_M + i) * ldg + j] : 0.0;
   for (int e = tid; e < QB * QB; e += blockDim.x) Ts[e / QB][e % QB] = 0.0;
   __syncthreads();
   auto reflect = [&](int buf) {
     const int r0 = j;
-    double sq = 0.0;
+    double* gv = gv0 + (size_t)buf * mt;
+    double sq = 0.0, sq2 = 0.0;
 #pragma unroll
     for (int k = 0; k < MAXR; k++) {
       const int i = lane + 32 * k;
       if (i > r0 && i < m) sq = fma(c[k], c[k], sq);
     }
-    for (int i = MR + lane; i < m; i += 32) sq = fma(ov[i - MR], ov[i - MR], sq);
-    sq = warp_sum(sq);
+    for (int i = MR + lane; i < ms; i += 32) sq = fma(ov[i - MR], ov[i - MR], sq);
+    for (int i = lane; i < mt; i += 32) sq2 = fma(gc[i], gc[i], sq2);
+    sq = warp_sum(sq + sq2);
     double a = 0.0;
 #pragma unroll
     for (int k = 0; k < MAXR; k++)
@@ -710,9 +721,14 @@ __global__ void __launch_bounds__(32 * QB)
       }
       vbuf[buf][i] = v;
     }
-    for (int i = MR + lane; i < m; i += 32) {
+    for (int i = MR + lane; i < ms; i += 32) {
       ov[i - MR] *= scale;
       vbuf[buf][i] = ov[i - MR];
+    }
+    for (int i = lane; i < mt; i += 32) {
+      const double v = gc[i] * scale;
+      gc[i] = v;
+      gv[i] = v;
     }
     if (lane == 0) s_tau[j] = tau;
   };
@@ -722,6 +738,7 @@ __global__ void __launch_bounds__(32 * QB)
     const int buf = cc & 1;
     const double tau = s_tau[cc];
     const int r0 = cc;
+    const double* gv = gv0 + (size_t)buf * mt;
     if (j > cc && j < jb) {
       double vr[MAXR];
       double w0 = 0.0, w1 = 0.0;
@@ -734,11 +751,13 @@ __global__ void __launch_bounds__(32 * QB)
         else
           w0 = fma(vr[k], c[k], w0);
       }
-      for (int i = MR + lane; i < m; i += 32) w0 = fma(vbuf[buf][i], ov[i - MR], w0);
+      for (int i = MR + lane; i < ms; i += 32) w0 = fma(vbuf[buf][i], ov[i - MR], w0);
+      for (int i = lane; i < mt; i += 32) w1 = fma(gv[i], gc[i], w1);
       const double w = warp_sum(w0 + w1) * tau;
 #pragma unroll
       for (int k = 0; k < MAXR; k++) c[k] = fma(-w, vr[k], c[k]);
-      for (int i = MR + lane; i < m; i += 32) ov[i - MR] = fma(-w, vbuf[buf][i], ov[i - MR]);
+      for (int i = MR + lane; i < ms; i += 32) ov[i - MR] = fma(-w, vbuf[buf][i], ov[i - MR]);
+      for (int i = lane; i < mt; i += 32) gc[i] = fma(-w, gv[i], gc[i]);
       if (j == cc + 1) reflect(buf ^ 1);
     } else if (j < cc) {
       double z0 = 0.0, z1 = 0.0;
@@ -751,7 +770,8 @@ __global__ void __launch_bounds__(32 * QB)
         else
           z0 = fma(v, c[k], z0);
       }
-      for (int i = MR + lane; i < m; i += 32) z0 = fma(vbuf[buf][i], ov[i - MR], z0);
+      for (int i = MR + lane; i < ms; i += 32) z0 = fma(vbuf[buf][i], ov[i - MR], z0);
+      for (int i = lane; i < mt; i += 32) z1 = fma(gv[i], gc[i], z1);
       const double z = warp_sum(z0 + z1);
       if (lane == 0) s_z[cc][j] = z;
     }
@@ -775,7 +795,8 @@ __global__ void __launch_bounds__(32 * QB)
     const int i = lane + 32 * k;
     if (i < m) Vout[(int64_t)i * QB + j] = (j < jb) ? c[k] : 0.0;
   }
-  for (int i = MR + lane; i < m; i += 32) Vout[(int64_t)i * QB + j] = (j < jb) ? ov[i - MR] : 0.0;
+  for (int i = MR + lane; i < ms; i += 32) Vout[(int64_t)i * QB + j] = (j < jb) ? ov[i - MR] : 0.0;
+  for (int i = lane; i < mt; i += 32) Vout[(int64_t)(BIG_M + i) * QB + j] = (j < jb) ? gc[i] : 0.0;
   for (int e = tid; e < QB * QB; e += blockDim.x) Tout[e] = Ts[e / QB][e % QB];
 }
 
@@ -975,6 +996,10 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   qr_stop_init_k<<<1, 1024, 0, ctx->stream>>>((int64_t)n * n, A, thr2, stop_at);
   TK_LAUNCH_CHECK(ctx);
   DevBuf dbgb;  // (per-panel clock stamps of the panel kernels: not allocated = off)
+  // global tail of the tall panel kernel (rows beyond BIG_M: QB columns + two reflector tails)
+  DevBuf gtail;
+  if (n > BIG_M && n <= BIG_M + kBigTail)
+    TK_TRY(gtail.get(ctx, (size_t)(QB + 2) * (n - BIG_M)));
   // Streams: s0 (ctx->stream) carries the critical path  F_0, U_0', F_1, U_1', ...  where F_p
   // factors panel p and U_p' applies H_p to panel p+1 only; s1 applies H_p to the columns
   // beyond panel p+1 (overlapping F_{p+1}); s2 accumulates Q <- Q H_p forward (overlapping
@@ -1074,8 +1099,9 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
             Aw.p + (int64_t)(j0 - QB) * n + j0, n);
         TK_LAUNCH_CHECK(ctx);
       }
-      if (m <= BIG_M) {
-        constexpr int BMR = 26;  // 832 register rows; the rest in shared memory
+      if (m <= BIG_M + kBigTail) {
+        constexpr int BMR = 26;  // 832 register rows; the rest in shared memory (and, beyond
+                                 // BIG_M rows, in the global tail gtail)
         const size_t osmem = sizeof(double) * (size_t)QB * (BIG_M - 32 * BMR);
         static bool at = false;
         if (!at) {
@@ -1084,7 +1110,7 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
           at = true;
         }
         qr_panel_big_k<BMR><<<1, 32 * QB, osmem, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp,
-                                                      Tp);
+                                                      Tp, gtail.p);
       } else {
         qr_panel_k<false><<<1, QT, 0, s0>>>(m, jb, Aw.p + (int64_t)j0 * n + j0, n, Vp, Tp);
       }

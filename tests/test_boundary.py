@@ -109,3 +109,15 @@ def test_round_workspace_bound_is_a_host_function(so):
     # c4 grown ranks: a few GB of scratch, far inside 180 GB of HBM
     c4 = f(786432, 165, 512, 896, 896)
     assert 4e9 < c4 < 3e10
+
+
+def test_gemm_and_schedule_entry_points_reject_null_arguments(so):
+    """tk_gemm / tk_ctx_set_gemm_feed / tk_ctx_set_jacobi_schedule validate their handles before
+    any CUDA call (no GPU needed)."""
+    P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    so.tk_gemm.argtypes = [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64, I]
+    assert so.tk_gemm(None, 0, 0, 4, 4, 4, 1.0, None, 4, None, 4, 0.0, None, 4, 0) == -3
+    so.tk_ctx_set_gemm_feed.argtypes = [P, I]
+    assert so.tk_ctx_set_gemm_feed(None, 1) == -3
+    so.tk_ctx_set_jacobi_schedule.argtypes = [P, I]
+    assert so.tk_ctx_set_jacobi_schedule(None, 1) == -3

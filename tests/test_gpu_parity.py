@@ -234,11 +234,13 @@ def test_round_parity_random(seed, ctx):
     check_round(x, tol, 0, ctx)
 
 
-@pytest.mark.parametrize("r1,n_xi,n_t", [(1000, 30, 60), (1700, 45, 40), (2100, 44, 50)])
+@pytest.mark.parametrize("r1,n_xi,n_t", [(1000, 30, 60), (1700, 45, 40), (2100, 44, 50),
+                                        (2500, 200, 20)])
 def test_round_parity_tall_panels(r1, n_xi, n_t, ctx):
     """Wide space bonds (R1 > 896 rows in the Householder panels of pass 1 and of the middle
     core's orth_rows): the shared-memory and the register + shared-memory overflow panel kernels
-    (qr_panel_warp_k, qr_panel_big_k) — the c5 / c6 apply rounds reach k = 2240."""
+    (qr_panel_warp_k, qr_panel_big_k) — the c5 / c6 apply rounds reach k = 2240; the last case
+    (k = 2400 > 2256) also uses the big kernel's global-memory tail."""
     rng = np.random.default_rng(800 + r1)
     x = random_tt(rng, 2600, n_xi, n_t, r1, 12, kind="decay")
     check_round(x, 1e-8, 0, ctx, dense=False)
