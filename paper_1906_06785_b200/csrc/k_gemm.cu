@@ -445,7 +445,9 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   }
   // heavy products with beta == 0: the TMA-fed kernel (same tile, same split-K partials)
   const double flops = sym ? (double)M * (M + 1) * K : 2.0 * M * N * K;
-  const bool use_tma = ctx->gemm_tma && cfg == 0 && beta == 0.0 && !triu_b && flops >= 1e8 &&
+  // (cfg 2, the N = 80 j products, runs the TMA kernel's 64 x 80 tile instead of the cp.async
+  // 128 x 80 one)
+  const bool use_tma = ctx->gemm_tma && beta == 0.0 && !triu_b && flops >= 1e8 &&
                        tk_dgemm_tma_eligible(transA, transB, M, N, K, A, lda, B, ldb);
   // Waves of resident CTAs.  cp.async kernel: 4 (time-optimal, above).  TMA kernel: 12 — shorter
   // K chunks keep the CTAs that share operand columns (the 10 tiles of a Gram's column block)
@@ -490,7 +492,7 @@ int tk_dgemm(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_
   int st = TK_OK;
   if (use_tma) {
     st = tk_dgemm_tma_launch(ctx, transA, transB, M, N, K, alpha, A, lda, B, ldb, C, ldc, kchunk,
-                             (int)splits, sym ? 1 : 0, partial, skip);
+                             (int)splits, sym ? 1 : 0, partial, skip, cfg == 2 ? 80 : 64);
   } else {
 #define TK_GEMM_CASE(a, b, v)                                                               \
   if (AK == a && BKm == b && v2 == v) {                                                     \

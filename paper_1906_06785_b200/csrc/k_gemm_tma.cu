@@ -34,9 +34,8 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 128;
-constexpr int TILE_BYTES = BM * BK * 8;            // 8 KB per operand tile
-constexpr int STAGE_BYTES = 2 * TILE_BYTES;        // A + B
+constexpr int BM = 64, BK = 16, STAGES = 3, NT = 128;
+constexpr int TILE_BYTES = BM * BK * 8;            // 8 KB: the A tile (and the B tile for BN = 64)
 
 __device__ __forceinline__ unsigned smaddr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -84,21 +83,24 @@ __device__ __forceinline__ int tile_off(int m, int k) {
   return (m << 7) + (((k >> 1) ^ (m & 7)) << 4) + ((k & 1) << 3);
 }
 
-// One stage's operand tile.  K-contiguous operand (row-major [rows][K]): one 16 x 64 box at
-// (k0, r0); K-major operand ([K][rows]): four 16 x 16 boxes at (r0 + 16 b, k0).
-template <bool KMAJOR>
+// One stage's operand tile of ROWS rows.  K-contiguous operand (row-major [rows][K]): one
+// 16 x ROWS box at (k0, r0); K-major operand ([K][rows]): ROWS / 16 boxes of 16 x 16 at
+// (r0 + 16 b, k0).
+template <bool KMAJOR, int ROWS>
 __device__ __forceinline__ void issue_tile(unsigned dst, const CUtensorMap* map, int r0, int k0,
                                            unsigned bar) {
   if (KMAJOR) {
 #pragma unroll
-    for (int b = 0; b < BM / 16; b++) tma_load_2d(dst + b * 2048, map, r0 + 16 * b, k0, bar);
+    for (int b = 0; b < ROWS / 16; b++) tma_load_2d(dst + b * 2048, map, r0 + 16 * b, k0, bar);
   } else {
     tma_load_2d(dst, map, k0, r0, bar);
   }
 }
 
-template <bool A_KMAJOR, bool B_KMAJOR>
-__global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+// BN_: tile columns, 64 or 80 (N = 80 j products such as the c4 reconstruction, N = 160: warp
+// tiles 32 x 40, no ragged tile column).
+template <bool A_KMAJOR, bool B_KMAJOR, int BN_>
+__global__ void __launch_bounds__(NT, 4) dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        int64_t M, int64_t N, int64_t K,
                                                        double* __restrict__ C, int64_t ldc,
@@ -110,12 +112,15 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
   if (sym && tile_n < tile_m) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long bars[2 * STAGES];  // full[s], empty[s]
-  const unsigned sbase = (smaddr(smem_raw) + 1023u) & ~1023u;
+  constexpr int FN = BN_ / 16, WN_COLS = BN_ / 2;
+  constexpr int TILE_BYTES_B = BN_ * BK * 8, STAGE_BYTES = TILE_BYTES + TILE_BYTES_B;
+  const unsigned sbase = smaddr(smem_raw);
+  if (sbase & 1023u) __trap();  // the 128B swizzle pattern repeats every 1024 bytes
   const unsigned bar0 = smaddr(bars);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int lr = lane >> 2, lc = lane & 3;
-  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
+  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN_;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min(K, kbeg + kchunk);
   const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
@@ -136,8 +141,8 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
         const unsigned fb = bar0 + 8 * s, dst = sbase + s * STAGE_BYTES;
         const int k0 = (int)(kbeg + (int64_t)s * BK);
         mbar_expect_tx(fb, STAGE_BYTES);
-        issue_tile<A_KMAJOR>(dst, &tmA, (int)m0, k0, fb);
-        issue_tile<B_KMAJOR>(dst + TILE_BYTES, &tmB, (int)n0, k0, fb);
+        issue_tile<A_KMAJOR, BM>(dst, &tmA, (int)m0, k0, fb);
+        issue_tile<B_KMAJOR, BN_>(dst + TILE_BYTES, &tmB, (int)n0, k0, fb);
       }
   }
 
@@ -151,18 +156,23 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
   // (kq has bits 0 and 2 only and mu >> 1 bits 0.. of the chunk index, so +2 in k, +4 in
   // k >> 1 and +8 in m are XORs of single chunk-index bits) — four base registers per operand.
   const int baseA = tile_off<A_KMAJOR>(wm * 32 + mu, kq);
-  const int baseB = tile_off<B_KMAJOR>(wn * 32 + mu, kq);
+  const int baseB = tile_off<B_KMAJOR>(wn * WN_COLS + mu, kq);
+  // (K-major B with 40-column warp tiles: 8 j + 40 wn crosses the 16-wide boxes irregularly, so
+  // every fragment keeps its own base offset; + 2 in k is still the XOR of byte-offset bit 5)
+  int oB[FN];
+#pragma unroll
+  for (int j = 0; j < FN; j++) oB[j] = tile_off<B_KMAJOR>(wn * WN_COLS + 8 * j + mu, kq);
   int vA[4], vB[4];
 #pragma unroll
   for (int v = 0; v < 4; v++) {
     vA[v] = baseA ^ (A_KMAJOR ? (((v & 1) << 5) ^ ((v >> 1) << 6)) : (((v & 1) << 4) ^ ((v >> 1) << 6)));
     vB[v] = baseB ^ (B_KMAJOR ? (((v & 1) << 5) ^ ((v >> 1) << 6)) : (((v & 1) << 4) ^ ((v >> 1) << 6)));
   }
-  double acc[4][4][2];
+  double acc[4][FN][2];
 #pragma unroll
   for (int i = 0; i < 4; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const char* sgen = (const char*)__cvta_shared_to_generic((size_t)sbase);
   for (int t = 0; t < ntiles; t++) {
@@ -176,8 +186,8 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
       const unsigned fb = bar0 + 8 * sp, dst = sbase + sp * STAGE_BYTES;
       const int k0 = (int)(kbeg + (int64_t)(t - 1 + STAGES) * BK);
       mbar_expect_tx(fb, STAGE_BYTES);
-      issue_tile<A_KMAJOR>(dst, &tmA, (int)m0, k0, fb);
-      issue_tile<B_KMAJOR>(dst + TILE_BYTES, &tmB, (int)n0, k0, fb);
+      issue_tile<A_KMAJOR, BM>(dst, &tmA, (int)m0, k0, fb);
+      issue_tile<B_KMAJOR, BN_>(dst + TILE_BYTES, &tmB, (int)n0, k0, fb);
     }
     __syncwarp();
     mbar_wait(bar0 + 8 * s, ph);
@@ -185,7 +195,7 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
     const char* bs = as + TILE_BYTES;
 #pragma unroll
     for (int st = 0; st < 4; st++) {
-      double a[4], b[4];
+      double a[4], b[FN];
       const int g = st >> 1, j2 = st & 1;
 #pragma unroll
       for (int i = 0; i < 4; i++) {
@@ -194,15 +204,19 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
         a[i] = *(const double*)(as + off);
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int off = B_KMAJOR ? vB[j2 | ((j & 1) << 1)] + 2048 * (j >> 1) + 1024 * g + 256 * j2
-                                 : vB[j2 | (g << 1)] + 1024 * j;
+      for (int j = 0; j < FN; j++) {
+        int off;
+        if (B_KMAJOR && BN_ != 64)
+          off = (oB[j] ^ (j2 << 5)) + 1024 * g + 256 * j2;
+        else
+          off = B_KMAJOR ? vB[j2 | ((j & 1) << 1)] + 2048 * (j >> 1) + 1024 * g + 256 * j2
+                         : vB[j2 | (g << 1)] + 1024 * j;
         b[j] = *(const double*)(bs + off);
       }
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < FN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     // The stage is about to be overwritten by the TMA (async proxy) while it was read through
     // the generic proxy: the release needs a cross-proxy fence.  Without it a warp's fragment
@@ -223,8 +237,8 @@ __global__ void __launch_bounds__(NT) dgemm_tma_kernel(const __grid_constant__ C
     const int64_t gm = m0 + wm * 32 + i * 8 + mu;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int64_t gn = n0 + wn * 32 + j * 8 + nc;
+    for (int j = 0; j < FN; j++) {
+      const int64_t gn = n0 + wn * WN_COLS + j * 8 + nc;
       if (vec_out) {
         if (gn >= N) continue;
         if (partial)
@@ -271,7 +285,7 @@ EncodeFn encode_fn() {
 
 // rows x K operand: kmajor = stored [K][rows] (rows contiguous), else [rows][K] (K contiguous)
 bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t rows, int64_t K,
-              int64_t ld) {
+              int64_t ld, int tile_rows) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2], strides[1] = {(cuuint64_t)ld * 8};
@@ -285,28 +299,37 @@ bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t rows, i
     dims[0] = (cuuint64_t)K;
     dims[1] = (cuuint64_t)rows;
     box[0] = 16;
-    box[1] = BM;
+    box[1] = (cuuint32_t)tile_rows;
   }
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool AK, bool BKm>
+template <bool AK, bool BKm, int BN_>
 int launch(tk_ctx* ctx, dim3 grid, const CUtensorMap& ta, const CUtensorMap& tb, int64_t M,
            int64_t N, int64_t K, double* C, int64_t ldc, double alpha, int64_t kchunk, int sym,
            double* partial, const int* skip) {
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
+  const size_t smem = (size_t)STAGES * (TILE_BYTES + BN_ * BK * 8);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_tma_kernel<AK, BKm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(dgemm_tma_kernel<AK, BKm, BN_>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  dgemm_tma_kernel<AK, BKm><<<grid, NT, smem, ctx->stream>>>(ta, tb, M, N, K, C, ldc, alpha, kchunk,
-                                                             sym, partial, skip);
+  dgemm_tma_kernel<AK, BKm, BN_><<<grid, NT, smem, ctx->stream>>>(ta, tb, M, N, K, C, ldc, alpha,
+                                                                  kchunk, sym, partial, skip);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
+}
+template <int BN_>
+int launch_bn(tk_ctx* ctx, bool AK, bool BKm, dim3 grid, const CUtensorMap& ta,
+              const CUtensorMap& tb, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
+              double alpha, int64_t kchunk, int sym, double* partial, const int* skip) {
+  if (AK && BKm) return launch<true, true, BN_>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
+  if (AK && !BKm) return launch<true, false, BN_>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
+  if (!AK && BKm) return launch<false, true, BN_>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
+  return launch<false, false, BN_>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
 }
 
 }  // namespace
@@ -321,22 +344,22 @@ bool tk_dgemm_tma_eligible(bool transA, bool transB, int64_t M, int64_t N, int64
   return true;
 }
 
-// The TMA-fed kernel proper (grid and split-K decided by tk_dgemm).  sym: symmetric Gram flag.
+// The TMA-fed kernel proper (split-K decided by tk_dgemm).  sym: symmetric Gram flag; bn: tile
+// columns (64, or 80 for N = 80 j).
 int tk_dgemm_tma_launch(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
                         double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                         double* C, int64_t ldc, int64_t kchunk, int splits, int sym,
-                        double* partial, const int* skip) {
+                        double* partial, const int* skip, int bn) {
   CUtensorMap ta, tb;
   const bool AK = transA, BKm = !transB;
-  if (!make_map(&ta, A, AK, M, K, lda) || !make_map(&tb, B, BKm, N, K, ldb)) {
+  if (!make_map(&ta, A, AK, M, K, lda, BM) || !make_map(&tb, B, BKm, N, K, ldb, bn)) {
     ctx->err = "tk_dgemm: cuTensorMapEncodeTiled failed";
     return TK_ECUDA;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
-  if (AK && BKm) return launch<true, true>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
-  if (AK && !BKm) return launch<true, false>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
-  if (!AK && BKm) return launch<false, true>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
-  return launch<false, false>(ctx, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
+  dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
+  if (bn == 80)
+    return launch_bn<80>(ctx, AK, BKm, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
+  return launch_bn<64>(ctx, AK, BKm, grid, ta, tb, M, N, K, C, ldc, alpha, kchunk, sym, partial, skip);
 }
 
 __global__ void tk_anchor_k_gemm_tma_k() {}

@@ -313,7 +313,7 @@ bool tk_dgemm_tma_eligible(bool transA, bool transB, int64_t M, int64_t N, int64
 int tk_dgemm_tma_launch(tk_ctx* ctx, bool transA, bool transB, int64_t M, int64_t N, int64_t K,
                         double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                         double* C, int64_t ldc, int64_t kchunk, int splits, int sym,
-                        double* partial, const int* skip);
+                        double* partial, const int* skip, int bn = 64);
 
 // Symmetric eigen-decomposition by parallel cyclic two-sided Jacobi.
 //   A: n x n symmetric (device, row-major, ld = n), destroyed.

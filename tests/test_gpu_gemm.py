@@ -80,6 +80,17 @@ def test_gemm_all_layouts(feed, ta, tb, M, N, K):
 
 
 @pytest.mark.parametrize("feed", [1, 0])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_n80_tile(feed, ta, tb):
+    """N = 80 j with a tall M (the c4 reconstruction shape class): the 64 x 80 TMA tile / the
+    128 x 80 cp.async tile, ragged M and K."""
+    rng = np.random.default_rng([80, int(ta), int(tb)])
+    ctx = ttk.Context()
+    ctx.set_gemm_feed(feed)
+    _run(ctx, 75802, 160, 322, ta, tb, pad=2, rng=rng, alpha=1.25)
+
+
+@pytest.mark.parametrize("feed", [1, 0])
 def test_gemm_split_k_and_gram(feed):
     """Small output with a long K (split-K partials + fixed-order reduction), symmetric mode."""
     rng = np.random.default_rng(7)

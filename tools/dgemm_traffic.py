@@ -15,7 +15,8 @@ for r in rows:
     d = per.setdefault(int(r[ii]), {})
     d[r[mi]] = float(r[vi].replace(",", ""))
 launches = [per[k] for k in sorted(per)]
-steps = 3  # the timed step, the untimed fully profiled step and the e2e step
+# ops captured = number of form_W launches (the only dgemm launch longer than 15 ms at c4)
+steps = max(1, sum(1 for d in launches if d.get("gpu__time_duration.sum", 0) > 15e6))
 # the bench's heavy set is the launches with >= 1e8 algorithmic flops or bytes (46 per c4 step):
 # here the 46 longest per step
 TOP = int(sys.argv[2]) if len(sys.argv) > 2 else 46
@@ -23,8 +24,9 @@ heavy = sorted(launches, key=lambda d: -d.get("gpu__time_duration.sum", 0))[: TO
 byts = [d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in heavy]
 out = {
     "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-              "-k regex:dgemm_kernel over `bench.py --steps 1 --warmup 0 --no-cpu-baseline` on "
-              "c4 (3 apply+round ops: timed, profiled, e2e)",
+              "-k regex:dgemm (dgemm_tma_kernel + dgemm_kernel) over `bench.py --steps 1 --warmup 0 "
+              f"--no-cpu-baseline` on c4 ({steps} apply+round ops captured)",
+    "csv": os.path.basename(sys.argv[1]),
     "launches_per_step": len(launches) / steps,
     "heavy_launches_per_step": len(heavy) / steps,
     "heavy_rule": f"the {TOP} longest dgemm launches per step (bench.py's heavy set)",
