@@ -98,6 +98,17 @@ int tk_ctx_profile_dump(tk_ctx* ctx, char* buf, size_t len);
  * tk_sync_ranks: block until every queued rounding has finished and published its ranks (x may
  * be NULL; all TTs are published).  A no-op in synchronous mode. */
 int tk_ctx_set_async(tk_ctx* ctx, int on);
+/* Copy-window gate for pipelined host <-> device transfers.  The latency-bound phases of a
+ * rounding (thousands of short kernels) slow down when bulk PCIe copies run beside them, the
+ * DMMA-bound phase in the middle (the big-core Gram pass) does not.  After this
+ * call, work enqueued on `cuda_stream` (a cudaStream_t of the caller: its copy stream) waits —
+ * on the device, without a host synchronisation — until the NEXT tk_round / tk_apply_round of
+ * this context reaches that phase, and at the latest until that rounding has finished (also
+ * when it fails).  Several streams may be gated on the same rounding.  The caller must follow
+ * up with a rounding on this context (tk_ctx_destroy releases a gate that was never opened).
+ * Returns 1 if the stream is gated, 0 if the driver has no stream memory operations (the
+ * stream is not gated: transfers simply start at once), or a negative error. */
+int tk_ctx_gate_stream(tk_ctx* ctx, void* cuda_stream);
 int tk_sync_ranks(tk_ctx* ctx, tk_tt* x);
 /* Upper bound (bytes) of the library scratch of one tk_round on ranks (R1, R2), or one
  * tk_apply_round whose grown ranks are (R1, R2), with these mode sizes; the caller-owned cores

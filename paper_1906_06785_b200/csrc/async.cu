@@ -269,6 +269,61 @@ extern "C" int tk_ctx_set_async(tk_ctx* ctx, int on) {
   return 1;
 }
 
+// ---------------------------------------------------------------------------- copy-window gate
+// The latency-bound phases of a rounding (the small-core chain before the big Gram pass, and the
+// pass-2 / bond-2 chain after it) launch ~1500 short kernels whose command fetches share the
+// PCIe link with bulk host <-> device copies: a concurrent 7 ms H2D copy at the start of a c4 op
+// costs the op 6.5 ms (profiles/r02/e2e_diag.txt).  The DMMA-bound phase in between (form_W,
+// gram_W: 35 ms at c4) is insensitive to it.  tk_ctx_gate_stream makes a user stream wait (a
+// device-side wait on a flag, no host synchronisation) until the NEXT rounding of the context
+// reaches that phase, so pipelined transfers of the neighbouring steps land inside the window.
+extern "C" int tk_ctx_gate_stream(tk_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return TK_EARG;
+  if (!memops_available()) return 0;  // no stream memory operations: the stream is not gated
+  if (!ctx->gate_flag) {
+    if (cudaMalloc(&ctx->gate_flag, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(ctx->gate_flag, 0, sizeof(uint32_t)) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->gate_flag = nullptr;
+      ctx->err = "tk_ctx_gate_stream: flag allocation failed";
+      return TK_ECUDA;
+    }
+  }
+  if (!ctx->gate_armed) {
+    ctx->gate_seq++;
+    ctx->gate_armed = true;
+  }
+  if (g_wait((CUstream)cuda_stream, (CUdeviceptr)ctx->gate_flag, ctx->gate_seq,
+             CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+    ctx->err = "tk_ctx_gate_stream: cuStreamWaitValue32 failed";
+    return TK_ECUDA;
+  }
+  return 1;
+}
+
+uint32_t tk_gate_claim(tk_ctx* ctx) {
+  if (!ctx->gate_armed) return 0;
+  ctx->gate_armed = false;
+  return ctx->gate_seq;
+}
+
+void tk_gate_open(tk_ctx* ctx) {
+  if (!ctx->gate_job || !ctx->gate_flag) return;
+  g_write((CUstream)ctx->stream, (CUdeviceptr)ctx->gate_flag, ctx->gate_job, 0);
+  ctx->gate_job = 0;
+}
+
+void tk_gate_destroy(tk_ctx* ctx) {
+  if (!ctx->gate_flag) return;
+  if (ctx->gate_armed) {  // a gate nobody will open: release the waiting streams
+    const uint32_t v = ctx->gate_seq;
+    cudaMemcpy(ctx->gate_flag, &v, sizeof(v), cudaMemcpyHostToDevice);
+    cudaDeviceSynchronize();
+  }
+  cudaFree(ctx->gate_flag);
+  ctx->gate_flag = nullptr;
+}
+
 void tk_async_destroy(tk_ctx* ctx) {
   tk_async_drain(ctx);
   async_stop(ctx);

@@ -145,6 +145,7 @@ int tk_side_join(tk_ctx* ctx) {
 extern "C" int tk_ctx_destroy(tk_ctx* ctx) {
   if (!ctx) return TK_OK;
   tk_async_destroy(ctx);
+  tk_gate_destroy(ctx);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
@@ -999,6 +1000,7 @@ int svd_two_pass(tk_ctx* ctx, int64_t M, int64_t R, const double* Y, const doubl
   TK_TRY(W.get(ctx, M * k));
   {
     TagScope t(ctx, Lm ? "bond1.form_W" : "bond2.form_W");
+    if (Lm) tk_gate_open(ctx);  // the DMMA-bound phase starts: open the copy-window gate
     TK_TRY(tk_dgemm(ctx, false, false, M, k, R, 1.0, Y, R, PV, k, 0.0, W.p, k));
   }
   TK_TRY(GW.get(ctx, k * k));
@@ -1175,8 +1177,10 @@ int tk_round_now(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
   if (!ctx || !x) return TK_EARG;
+  const uint32_t gate = tk_gate_claim(ctx);  // copy-window gate requested for this rounding
   if (ctx->async && !tk_async_on_worker(ctx))  // queued: *x is read when the job runs
     return tk_async_submit(ctx, [=]() {
+      GateGuard gg(ctx, gate);
       tk_tt xc = *x;
       const int st = tk_round_now(ctx, &xc, tol, rmax, sigma1_out, sigma2_out, discarded_out,
                                   norm_out);
@@ -1186,6 +1190,7 @@ extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double*
       }
       return st;
     });
+  GateGuard gg(ctx, gate);
   return tk_round_now(ctx, x, tol, rmax, sigma1_out, sigma2_out, discarded_out, norm_out);
 }
 
@@ -1193,8 +1198,10 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
                               int64_t rmax, double* sigma1_out, double* sigma2_out,
                               double* discarded_out, double* norm_out) {
   if (!ctx || !op || !x || !y) return TK_EARG;
+  const uint32_t gate = tk_gate_claim(ctx);
   if (ctx->async && !tk_async_on_worker(ctx))
     return tk_async_submit(ctx, [=]() {
+      GateGuard gg(ctx, gate);
       const tk_tt xc = *x;
       tk_tt yc = *y;
       const int st = tk_apply_round_now(ctx, op, &xc, &yc, tol, rmax, sigma1_out, sigma2_out,
@@ -1205,6 +1212,7 @@ extern "C" int tk_apply_round(tk_ctx* ctx, const tk_op* op, const tk_tt* x, tk_t
       }
       return st;
     });
+  GateGuard gg(ctx, gate);
   return tk_apply_round_now(ctx, op, x, y, tol, rmax, sigma1_out, sigma2_out, discarded_out,
                             norm_out);
 }

@@ -64,6 +64,23 @@ struct tk_ctx {
   // schedule of the block-Jacobi eigensolver: 1 = dataflow (pair CTAs and tile CTAs one round
   // apart, no grid barriers; default), 0 = grid barriers (k_jacobi.cu); tk_ctx_set_jacobi_schedule
   int jacobi_flow = 1;
+  // copy-window gate (tk_ctx_gate_stream, async.cu): user streams wait on gate_flag >= gate_seq,
+  // which the next rounding writes when it reaches its DMMA-bound phase (and at its end at the
+  // latest).  gate_armed: a gate was requested since the last rounding was submitted; gate_job:
+  // the sequence number the RUNNING rounding still has to publish (0: none).
+  uint32_t* gate_flag = nullptr;
+  uint32_t gate_seq = 0, gate_job = 0;
+  bool gate_armed = false;
+};
+// Copy-window gate: claim (caller thread, when a rounding is submitted), open (on the stream the
+// rounding runs on; idempotent), destroy.
+uint32_t tk_gate_claim(tk_ctx* ctx);
+void tk_gate_open(tk_ctx* ctx);
+void tk_gate_destroy(tk_ctx* ctx);
+struct GateGuard {  // opens the gate on every exit path of a rounding
+  tk_ctx* c;
+  GateGuard(tk_ctx* ctx, uint32_t job) : c(ctx) { c->gate_job = job; }
+  ~GateGuard() { tk_gate_open(c); }
 };
 // Async mode (async.cu).  drain: wait until the queued jobs ran (returns their first error);
 // submit: queue body() for the worker, ordered after (and gating) the caller's stream.

@@ -30,7 +30,7 @@ EXPORTED = ["tk_version", "tk_ctx_create", "tk_ctx_destroy", "tk_last_error", "t
             "tk_gmres_cycle_p", "tk_gmres_solve_p", "tk_picard",
             "tk_ctx_set_async", "tk_sync_ranks", "tk_round_workspace_bytes", "tk_ctx_reserve",
             "tk_ctx_scratch_high_water", "tk_gemm", "tk_ctx_set_gemm_feed",
-            "tk_ctx_set_jacobi_schedule"]
+            "tk_ctx_set_jacobi_schedule", "tk_ctx_gate_stream"]
 
 
 class TkError(RuntimeError):
@@ -115,6 +115,7 @@ def lib():
     L.tk_gemm.argtypes = [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64, I]
     L.tk_ctx_set_gemm_feed.argtypes = [P, I]
     L.tk_ctx_set_jacobi_schedule.argtypes = [P, I]
+    L.tk_ctx_gate_stream.argtypes = [P, P]
     L.tk_ctx_profile.argtypes = [P, I]
     L.tk_ctx_profile_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t]
     for name in EXPORTED:
@@ -168,6 +169,15 @@ class Context:
         """0 = cp.async, 1 = TMA tensor tiles (default) for the heavy DMMA products."""
         self.check(lib().tk_ctx_set_gemm_feed(self._h, int(mode)))
 
+    def gate_stream(self, stream: torch.cuda.Stream) -> bool:
+        """Work enqueued on `stream` from now on waits (on the device) until the next rounding of
+        this context reaches its DMMA-bound phase (tk_ctx_gate_stream): the window for pipelined
+        bulk copies.  Returns False when the driver cannot gate (the stream then runs at once)."""
+        rc = lib().tk_ctx_gate_stream(self._h, ctypes.c_void_p(stream.cuda_stream))
+        if rc < 0:
+            self.check(rc)
+        return rc == 1
+
     def set_jacobi_schedule(self, mode: int):
         """1 = dataflow (default), 0 = grid barriers for the block-Jacobi eigensolver."""
         self.check(lib().tk_ctx_set_jacobi_schedule(self._h, int(mode)))
@@ -198,10 +208,15 @@ class Context:
     def launches(self) -> int:
         return int(lib().tk_ctx_launch_count(self._h))
 
+    def close(self):
+        """tk_ctx_destroy now (drains the async queue, releases an unused copy-window gate)."""
+        if self._h:
+            h, self._h = self._h, None
+            lib().tk_ctx_destroy(h)
+
     def __del__(self):
         try:
-            if self._h:
-                lib().tk_ctx_destroy(self._h)
+            self.close()
         except Exception:
             pass
 

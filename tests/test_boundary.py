@@ -121,3 +121,5 @@ def test_gemm_and_schedule_entry_points_reject_null_arguments(so):
     assert so.tk_ctx_set_gemm_feed(None, 1) == -3
     so.tk_ctx_set_jacobi_schedule.argtypes = [P, I]
     assert so.tk_ctx_set_jacobi_schedule(None, 1) == -3
+    so.tk_ctx_gate_stream.argtypes = [P, P]
+    assert so.tk_ctx_gate_stream(None, None) == -3

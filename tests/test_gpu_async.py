@@ -137,3 +137,62 @@ def test_round_workspace_bound_random(seed):
     ctx.scratch_high_water(reset=True)
     ttk.tt_round(x, 1e-8, ctx=ctx)
     assert ctx.scratch_high_water() <= ttk.round_workspace_bytes(*n, r1, r2)
+
+
+def _wait_idle(stream, seconds=10.0):
+    t0 = time.perf_counter()
+    while not stream.query():
+        if time.perf_counter() - t0 > seconds:
+            return False
+        time.sleep(0.001)
+    return True
+
+
+@pytest.mark.parametrize("use_async", [False, True])
+def test_copy_window_gate(use_async):
+    """tk_ctx_gate_stream: work on a gated stream waits for the next rounding of the context and
+    is released by it — also when that rounding fails — without any host synchronisation."""
+    cfg = CONFIGS["c2"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    ctx = ttk.Context()
+    if use_async and not ctx.set_async(True):
+        pytest.skip("no stream memory operations on this driver")
+    gop = ttk.Operator.from_kronsum(op, ctx)
+    xg = ttk.TT.from_cores(*x)
+    side = torch.cuda.Stream()
+    src = torch.arange(1 << 20, dtype=torch.float64, device="cuda")
+    dst = torch.zeros_like(src)
+    torch.cuda.synchronize()
+    if not ctx.gate_stream(side):
+        pytest.skip("driver cannot gate streams")
+    with torch.cuda.stream(side):
+        dst.copy_(src, non_blocking=True)
+    time.sleep(0.05)
+    assert not side.query()           # still waiting for a rounding
+    assert float(dst[-1]) == 0.0      # (default stream is independent of `side`)
+    y = ttk.tt_apply_round(gop, xg, cfg.tol, cfg.rmax)
+    ctx.sync()
+    assert _wait_idle(side)
+    assert torch.equal(dst, src)
+    ref = otT.round_tt(otT.apply_op(op, x), cfg.tol, cfg.rmax)
+    assert y.ranks == (ref[0].shape[1], ref[2].shape[0])
+    # a rounding that fails validation still opens the gate
+    dst.zero_()
+    torch.cuda.synchronize()
+    assert ctx.gate_stream(side)
+    with torch.cuda.stream(side):
+        dst.copy_(src, non_blocking=True)
+    bad = ttk.TT.from_cores(*random_tt(np.random.default_rng(1), 11, 3, 4, 2, 2))
+    with pytest.raises(ttk.TkError):
+        ttk.tt_apply_round(gop, bad, cfg.tol, cfg.rmax)
+        ctx.sync()
+    assert _wait_idle(side)
+    assert torch.equal(dst, src)
+    # an unused gate is released when the context goes away
+    assert ctx.gate_stream(side)
+    with torch.cuda.stream(side):
+        dst.copy_(src, non_blocking=True)
+    del gop, y
+    ctx.close()
+    assert _wait_idle(side)
