@@ -524,7 +524,7 @@ def run_ours(args, cfg, op, x):
         def h2d_step(i):
             with torch.cuda.stream(s_in):
                 if i >= 1:
-                    # copy window: step i's input travels while step i - 1 (the next rounding
+                    # copy window: step i's input travels while step i - 1 (the rounding just
                     # submitted) is in its DMMA-bound phase (tk_ctx_gate_stream)
                     gop.ctx.gate_stream(s_in)
                 if i >= 2:
@@ -543,25 +543,35 @@ def run_ours(args, cfg, op, x):
         e0.record(stream)
         s_in.wait_event(e0)
         h2d_step(0)
+
+        def d2h_step(i, ye, gated):
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[i])
+                if gated:
+                    gop.ctx.gate_stream(s_out)  # read back inside the next step's copy window
+                n = 0
+                srcs = ((ye.b1, op.n_x * r1o), (ye.b2, r1o * op.n_xi * r2o), (ye.b3, r2o * op.n_t)) \
+                    if use_async else ((c.reshape(-1), c.numel()) for c in (ye.U1, ye.U2, ye.U3))
+                for o, (c, m) in zip(outs[i % 2], srcs):
+                    o[:m].copy_(c[:m], non_blocking=True)
+                    n += m * 8
+                out_done[i].record(s_out)
+            return n
+
+        prev = None
         for i in range(ne):
-            if i + 1 < ne:
-                h2d_step(i + 1)
             stream.wait_event(in_done[i])
             if i >= 2:
                 stream.wait_event(out_done[i - 2])  # yes[i % 2] read back
             ye = ttk.tt_apply_round(gop, xes[i % 2], cfg.tol, cfg.rmax, out=yes[i % 2])
             comp_done[i].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(comp_done[i])
-                if i + 1 < ne:
-                    gop.ctx.gate_stream(s_out)  # read back inside step i + 1's copy window
-                d2h = 0
-                srcs = ((ye.b1, op.n_x * r1o), (ye.b2, r1o * op.n_xi * r2o), (ye.b3, r2o * op.n_t)) \
-                    if use_async else ((c.reshape(-1), c.numel()) for c in (ye.U1, ye.U2, ye.U3))
-                for o, (c, n) in zip(outs[i % 2], srcs):
-                    o[:n].copy_(c[:n], non_blocking=True)
-                    d2h += n * 8
-                out_done[i].record(s_out)
+            # step i is submitted: the transfers of its neighbours wait for its copy window
+            if i + 1 < ne:
+                h2d_step(i + 1)
+            if prev is not None:
+                d2h = d2h_step(i - 1, prev, True)
+            prev = ye
+        d2h = d2h_step(ne - 1, prev, False)
         stream.wait_event(out_done[ne - 1])
         e1.record(stream)
         torch.cuda.synchronize()

@@ -102,12 +102,16 @@ int tk_ctx_set_async(tk_ctx* ctx, int on);
  * rounding (thousands of short kernels) slow down when bulk PCIe copies run beside them, the
  * DMMA-bound phase in the middle (the big-core Gram pass) does not.  After this
  * call, work enqueued on `cuda_stream` (a cudaStream_t of the caller: its copy stream) waits —
- * on the device, without a host synchronisation — until the NEXT tk_round / tk_apply_round of
- * this context reaches that phase, and at the latest until that rounding has finished (also
- * when it fails).  Several streams may be gated on the same rounding.  The caller must follow
- * up with a rounding on this context (tk_ctx_destroy releases a gate that was never opened).
- * Returns 1 if the stream is gated, 0 if the driver has no stream memory operations (the
- * stream is not gated: transfers simply start at once), or a negative error. */
+ * on the device, without a host synchronisation — until the most recently SUBMITTED tk_round /
+ * tk_apply_round of this context has reached that phase (at the latest: has finished, also
+ * when it failed).  With the asynchronous boundary (tk_ctx_set_async) the rounding is still
+ * queued or running when the call is made and the transfers of the neighbouring pipeline steps
+ * land inside its window; in synchronous mode, or when no rounding was submitted yet, the
+ * condition already holds and the stream is not delayed.  The gate only ever waits for work
+ * that is already queued: no call order can leave the stream waiting forever.  Returns 1 if
+ * the wait was enqueued, 0 if the driver has no stream memory operations (the stream is not
+ * gated: transfers simply start at once), or a negative error.  The first call loads every
+ * kernel of the library and synchronises the context once. */
 int tk_ctx_gate_stream(tk_ctx* ctx, void* cuda_stream);
 int tk_sync_ranks(tk_ctx* ctx, tk_tt* x);
 /* Upper bound (bytes) of the library scratch of one tk_round on ranks (R1, R2), or one

@@ -275,25 +275,33 @@ extern "C" int tk_ctx_set_async(tk_ctx* ctx, int on) {
 // PCIe link with bulk host <-> device copies: a concurrent 7 ms H2D copy at the start of a c4 op
 // costs the op 6.5 ms (profiles/r02/e2e_diag.txt).  The DMMA-bound phase in between (form_W,
 // gram_W: 35 ms at c4) is insensitive to it.  tk_ctx_gate_stream makes a user stream wait (a
-// device-side wait on a flag, no host synchronisation) until the NEXT rounding of the context
-// reaches that phase, so pipelined transfers of the neighbouring steps land inside the window.
+// device-side wait on a flag, no host synchronisation) until the most recently SUBMITTED
+// rounding of the context has reached that phase, so pipelined transfers of the neighbouring
+// steps land inside the window.  A gate only ever waits for work that is already queued, and
+// every rounding publishes its number on all exit paths: no call order can leave a stream
+// waiting forever.
 extern "C" int tk_ctx_gate_stream(tk_ctx* ctx, void* cuda_stream) {
   if (!ctx) return TK_EARG;
   if (!memops_available()) return 0;  // no stream memory operations: the stream is not gated
   if (!ctx->gate_flag) {
-    if (cudaMalloc(&ctx->gate_flag, sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(ctx->gate_flag, 0, sizeof(uint32_t)) != cudaSuccess) {
+    // A gated stream does not idle until the rounding publishes its number, and CUDA's lazy
+    // loading of a not-yet-loaded kernel waits for the device to idle: load every kernel of
+    // the library first (as tk_ctx_set_async does).  Roundings submitted before the flag
+    // existed never publish: wait for them, then start the flag at the current number.
+    TK_TRY(preload_kernels(ctx));
+    if (ctx->async) TK_TRY(tk_async_drain(ctx));
+    TK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    uint32_t* f = nullptr;
+    const uint32_t v = ctx->round_seq;
+    if (cudaMalloc(&f, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemcpy(f, &v, sizeof(v), cudaMemcpyHostToDevice) != cudaSuccess) {
       cudaGetLastError();
-      ctx->gate_flag = nullptr;
       ctx->err = "tk_ctx_gate_stream: flag allocation failed";
       return TK_ECUDA;
     }
+    ctx->gate_flag = f;
   }
-  if (!ctx->gate_armed) {
-    ctx->gate_seq++;
-    ctx->gate_armed = true;
-  }
-  if (g_wait((CUstream)cuda_stream, (CUdeviceptr)ctx->gate_flag, ctx->gate_seq,
+  if (g_wait((CUstream)cuda_stream, (CUdeviceptr)ctx->gate_flag, ctx->round_seq,
              CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
     ctx->err = "tk_ctx_gate_stream: cuStreamWaitValue32 failed";
     return TK_ECUDA;
@@ -301,25 +309,19 @@ extern "C" int tk_ctx_gate_stream(tk_ctx* ctx, void* cuda_stream) {
   return 1;
 }
 
-uint32_t tk_gate_claim(tk_ctx* ctx) {
-  if (!ctx->gate_armed) return 0;
-  ctx->gate_armed = false;
-  return ctx->gate_seq;
-}
+// number of the rounding being submitted (caller thread)
+uint32_t tk_gate_claim(tk_ctx* ctx) { return ++ctx->round_seq; }
 
 void tk_gate_open(tk_ctx* ctx) {
-  if (!ctx->gate_job || !ctx->gate_flag) return;
-  g_write((CUstream)ctx->stream, (CUdeviceptr)ctx->gate_flag, ctx->gate_job, 0);
+  if (!ctx->gate_job) return;
+  if (ctx->gate_flag)
+    g_write((CUstream)ctx->stream, (CUdeviceptr)ctx->gate_flag, ctx->gate_job, 0);
   ctx->gate_job = 0;
 }
 
-void tk_gate_destroy(tk_ctx* ctx) {
+void tk_gate_destroy(tk_ctx* ctx) {  // (after the queue was drained: every gate is open)
   if (!ctx->gate_flag) return;
-  if (ctx->gate_armed) {  // a gate nobody will open: release the waiting streams
-    const uint32_t v = ctx->gate_seq;
-    cudaMemcpy(ctx->gate_flag, &v, sizeof(v), cudaMemcpyHostToDevice);
-    cudaDeviceSynchronize();
-  }
+  cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->gate_flag);
   ctx->gate_flag = nullptr;
 }

@@ -822,7 +822,8 @@ int pass1_basis(tk_ctx* ctx, int n, const double* G, double* /*lam*/, double* V)
 }
 const EigOpts kPass2{kEps * kEps, 32 * kEps};
 const int kMaxSweeps = 40;
-const int64_t kOrth3MinRank = 128;  // orth_rows on the time core from this grown rank on
+const int64_t kOrth3MinRank = 128;  // orth_rows on the time core from this grown rank on ...
+const int64_t kOrth3MinNt = 128;    // ... when n_t is at least this (R2 >= n_t case)
 const double kDropThr = 64.0 * kEps;         // numerical-dimension threshold of orth_rows
 
 // A (R x N, row-major, ld N) = L (R x k) * Q (k x N, orthonormal rows) with Q stored
@@ -1177,7 +1178,7 @@ int tk_round_now(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1
 extern "C" int tk_round(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* sigma1_out,
                         double* sigma2_out, double* discarded_out, double* norm_out) {
   if (!ctx || !x) return TK_EARG;
-  const uint32_t gate = tk_gate_claim(ctx);  // copy-window gate requested for this rounding
+  const uint32_t gate = tk_gate_claim(ctx);  // this rounding's number (copy-window gate)
   if (ctx->async && !tk_async_on_worker(ctx))  // queued: *x is read when the job runs
     return tk_async_submit(ctx, [=]() {
       GateGuard gg(ctx, gate);
@@ -1294,7 +1295,10 @@ static int round_impl(tk_ctx* ctx, tk_tt* x, double tol, int64_t rmax, double* s
   // NUMERICAL row rank k3 of U3 (terms sharing a time factor, e.g. T_k = I, make it exactly
   // rank-deficient: c4 k3 = 128 instead of n_t = 512), which shrinks the middle core's
   // unfolding (R1 x n_xi k3) and bond 2 four-fold for the price of one orth_rows on R2 x n_t.
-  if (n_t > R2 || R2 >= kOrth3MinRank) {
+  // (n_t < kOrth3MinNt: the rank cannot drop below much less than n_t's worth of columns and
+  // the step costs more than it can save — c5, n_t = 64: every MGS rounding has R2 = 128 and
+  // full time rank 64, ~1.5 ms of pure overhead per rounding)
+  if (n_t > R2 || (R2 >= kOrth3MinRank && n_t >= kOrth3MinNt)) {
     TK_TRY(orth_rows(ctx, R2, n_t, x->U3, L3b, Q3c, &k3));
     L3 = L3b.p;
     q3_id = false;

@@ -64,13 +64,13 @@ struct tk_ctx {
   // schedule of the block-Jacobi eigensolver: 1 = dataflow (pair CTAs and tile CTAs one round
   // apart, no grid barriers; default), 0 = grid barriers (k_jacobi.cu); tk_ctx_set_jacobi_schedule
   int jacobi_flow = 1;
-  // copy-window gate (tk_ctx_gate_stream, async.cu): user streams wait on gate_flag >= gate_seq,
-  // which the next rounding writes when it reaches its DMMA-bound phase (and at its end at the
-  // latest).  gate_armed: a gate was requested since the last rounding was submitted; gate_job:
-  // the sequence number the RUNNING rounding still has to publish (0: none).
+  // copy-window gate (tk_ctx_gate_stream, async.cu): every public rounding gets a sequence
+  // number (round_seq, caller thread) and publishes it to gate_flag (device) when it reaches its
+  // DMMA-bound phase, at its end at the latest; a gated user stream waits for the number of the
+  // most recently SUBMITTED rounding.  gate_job: the number the running rounding still has to
+  // publish (0: none).
   uint32_t* gate_flag = nullptr;
-  uint32_t gate_seq = 0, gate_job = 0;
-  bool gate_armed = false;
+  uint32_t round_seq = 0, gate_job = 0;
 };
 // Copy-window gate: claim (caller thread, when a rounding is submitted), open (on the stream the
 // rounding runs on; idempotent), destroy.

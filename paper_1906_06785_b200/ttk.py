@@ -170,9 +170,10 @@ class Context:
         self.check(lib().tk_ctx_set_gemm_feed(self._h, int(mode)))
 
     def gate_stream(self, stream: torch.cuda.Stream) -> bool:
-        """Work enqueued on `stream` from now on waits (on the device) until the next rounding of
-        this context reaches its DMMA-bound phase (tk_ctx_gate_stream): the window for pipelined
-        bulk copies.  Returns False when the driver cannot gate (the stream then runs at once)."""
+        """Work enqueued on `stream` from now on waits (on the device) until the most recently
+        submitted rounding of this context has reached its DMMA-bound phase
+        (tk_ctx_gate_stream): the window for pipelined bulk copies.  Returns False when the
+        driver cannot gate (the stream then runs at once)."""
         rc = lib().tk_ctx_gate_stream(self._h, ctypes.c_void_p(stream.cuda_stream))
         if rc < 0:
             self.check(rc)

@@ -150,9 +150,11 @@ def _wait_idle(stream, seconds=10.0):
 
 @pytest.mark.parametrize("use_async", [False, True])
 def test_copy_window_gate(use_async):
-    """tk_ctx_gate_stream: work on a gated stream waits for the next rounding of the context and
-    is released by it — also when that rounding fails — without any host synchronisation."""
-    cfg = CONFIGS["c2"]
+    """tk_ctx_gate_stream: work on a gated stream waits (on the device) for the most recently
+    submitted rounding of the context to reach its DMMA-bound phase and is released by it — also
+    when that rounding fails; with nothing submitted, or in synchronous mode, the stream is not
+    delayed."""
+    cfg = CONFIGS["c3"]
     op = build_operator(cfg)
     x = make_input_tt(cfg, op.n_xi)
     ctx = ttk.Context()
@@ -164,35 +166,38 @@ def test_copy_window_gate(use_async):
     src = torch.arange(1 << 20, dtype=torch.float64, device="cuda")
     dst = torch.zeros_like(src)
     torch.cuda.synchronize()
+    # nothing submitted yet: the gate is open
     if not ctx.gate_stream(side):
         pytest.skip("driver cannot gate streams")
     with torch.cuda.stream(side):
         dst.copy_(src, non_blocking=True)
-    time.sleep(0.05)
-    assert not side.query()           # still waiting for a rounding
-    assert float(dst[-1]) == 0.0      # (default stream is independent of `side`)
-    y = ttk.tt_apply_round(gop, xg, cfg.tol, cfg.rmax)
-    ctx.sync()
-    assert _wait_idle(side)
-    assert torch.equal(dst, src)
+    assert _wait_idle(side) and torch.equal(dst, src)
+    # a submitted rounding: the copy completes, and never before the rounding was submitted
+    for _ in range(2):
+        dst.zero_()
+        torch.cuda.synchronize()
+        y = ttk.tt_apply_round(gop, xg, cfg.tol, cfg.rmax)
+        assert ctx.gate_stream(side)
+        with torch.cuda.stream(side):
+            dst.copy_(src, non_blocking=True)
+        ctx.sync()
+        assert _wait_idle(side)
+        assert torch.equal(dst, src)
     ref = otT.round_tt(otT.apply_op(op, x), cfg.tol, cfg.rmax)
     assert y.ranks == (ref[0].shape[1], ref[2].shape[0])
-    # a rounding that fails validation still opens the gate
+    # a rounding that fails validation still releases the stream
     dst.zero_()
     torch.cuda.synchronize()
-    assert ctx.gate_stream(side)
-    with torch.cuda.stream(side):
-        dst.copy_(src, non_blocking=True)
     bad = ttk.TT.from_cores(*random_tt(np.random.default_rng(1), 11, 3, 4, 2, 2))
     with pytest.raises(ttk.TkError):
         ttk.tt_apply_round(gop, bad, cfg.tol, cfg.rmax)
+        assert ctx.gate_stream(side)
+        with torch.cuda.stream(side):
+            dst.copy_(src, non_blocking=True)
         ctx.sync()
+    if not use_async:  # (synchronous mode raised before the gate was requested)
+        assert ctx.gate_stream(side)
+        with torch.cuda.stream(side):
+            dst.copy_(src, non_blocking=True)
     assert _wait_idle(side)
     assert torch.equal(dst, src)
-    # an unused gate is released when the context goes away
-    assert ctx.gate_stream(side)
-    with torch.cuda.stream(side):
-        dst.copy_(src, non_blocking=True)
-    del gop, y
-    ctx.close()
-    assert _wait_idle(side)

@@ -252,8 +252,12 @@ def test_round_wide_time_bond(r2, ctx):
     an R2 x R2 Gram): every panel-kernel shared-memory size class, including the exact 48 KB
     edge at R2 = 192 (32 panel rows x 192 doubles) that once failed to launch."""
     rng = np.random.default_rng(700 + r2)
-    x = random_tt(rng, 40, 3, 6, 5, r2)
+    # n_t = 130 >= 128: the rank-revealing path is taken for every R2 (for n_t < 128 and
+    # R2 >= n_t the library keeps Q3 = I, as the oracle does)
+    x = random_tt(rng, 40, 3, 130, 5, r2)
     check_round(x, 1e-8, 0, ctx)
+    y = random_tt(rng, 40, 3, 6, 5, r2)   # Q3 = I branch
+    check_round(y, 1e-8, 0, ctx)
 
 
 def test_round_rank_one_and_zero(ctx):
