@@ -70,3 +70,24 @@ def test_schedule_argument_error():
     ctx = ttk.Context()
     with pytest.raises(ttk.TkError):
         ctx.set_jacobi_schedule(3)
+
+
+@pytest.mark.parametrize("feed,schedule", [(0, 0), (0, 1), (1, 0)])
+def test_non_default_feed_and_schedule_match_the_oracle(feed, schedule):
+    """The non-default combinations (cp.async GEMM feed, grid-barrier Jacobi) through the whole
+    fused apply+round at c2 against the CPU oracle: ranks, kept singular values (1e-10 s_1) and
+    the reconstructed tensor (1e-10)."""
+    cfg = CONFIGS["c2"]
+    op = build_operator(cfg)
+    x = make_input_tt(cfg, op.n_xi)
+    ctx = ttk.Context()
+    ctx.set_gemm_feed(feed)
+    ctx.set_jacobi_schedule(schedule)
+    gop = ttk.Operator.from_kronsum(op, ctx)
+    y, info = ttk.tt_apply_round(gop, ttk.TT.from_cores(*x), cfg.tol, cfg.rmax, want_info=True)
+    torch.cuda.synchronize()
+    ref, rinfo = otT.round_tt(otT.apply_op(op, x), cfg.tol, cfg.rmax, return_info=True)
+    assert y.ranks == (ref[0].shape[1], ref[2].shape[0])
+    s1 = np.asarray(info.sigma1)[: y.ranks[0]]
+    assert np.abs(s1 - np.asarray(rinfo["sigma1"])[: y.ranks[0]]).max() <= 1e-10 * s1[0]
+    assert tt_diff_rel(y.cores_numpy(), ref) <= 1e-10
