@@ -521,12 +521,19 @@ def run_ours(args, cfg, op, x):
         in_done, comp_done, out_done = ([ev() for _ in range(ne)] for _ in range(3))
         d2h = 0
 
+        def gate(s_):
+            # copy-window gate; a driver without the needed entry points just runs ungated
+            try:
+                return gop.ctx.gate_stream(s_)
+            except ttk.TkError:
+                return False
+
         def h2d_step(i):
             with torch.cuda.stream(s_in):
                 if i >= 1:
                     # copy window: step i's input travels while step i - 1 (the rounding just
                     # submitted) is in its DMMA-bound phase (tk_ctx_gate_stream)
-                    gop.ctx.gate_stream(s_in)
+                    gate(s_in)
                 if i >= 2:
                     s_in.wait_event(comp_done[i - 2])  # xes[i % 2] free again
                 for buf_, src in zip((xes[i % 2].b1, xes[i % 2].b2, xes[i % 2].b3), pinned):
@@ -541,8 +548,8 @@ def run_ours(args, cfg, op, x):
         # one-time setup of the copy-window gate outside the timed region (its first call loads
         # the library's kernels and synchronises the context once; nothing is pending here, so
         # the streams are not delayed)
-        gop.ctx.gate_stream(s_in)
-        gop.ctx.gate_stream(s_out)
+        gate(s_in)
+        gate(s_out)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(stream)
@@ -553,7 +560,7 @@ def run_ours(args, cfg, op, x):
             with torch.cuda.stream(s_out):
                 s_out.wait_event(comp_done[i])
                 if gated:
-                    gop.ctx.gate_stream(s_out)  # read back inside the next step's copy window
+                    gate(s_out)  # read back inside the next step's copy window
                 n = 0
                 srcs = ((ye.b1, op.n_x * r1o), (ye.b2, r1o * op.n_xi * r2o), (ye.b3, r2o * op.n_t)) \
                     if use_async else ((c.reshape(-1), c.numel()) for c in (ye.U1, ye.U2, ye.U3))
