@@ -487,36 +487,49 @@ __global__ void __launch_bounds__(UCT) chol_unpiv_panel_k(int n, int j0, const d
 constexpr int TS_H = 64;
 
 // Inverse of every 64 x 64 (or smaller, last) diagonal block of the upper triangular R,
-// written into the matching diagonal blocks of X: one CTA per block, thread c computes column
-// c of the block inverse by back substitution (block of R and the columns in shared memory).
-__global__ void __launch_bounds__(TS_H) diag_inv_k(int k, const double* __restrict__ R,
+// written into the matching diagonal blocks of X: one CTA per block.  All DI_T threads load the
+// block (unrolled: the former 64-thread loop was a chain of 64 dependent L2 loads per thread)
+// and store the result; thread c < h computes column c of the block inverse by back
+// substitution with reciprocal diagonals (no division on the chain) and four partial sums.
+constexpr int DI_T = 256;
+__global__ void __launch_bounds__(DI_T) diag_inv_k(int k, const double* __restrict__ R,
                                                    int64_t ldr, double* __restrict__ X,
                                                    int64_t ldx) {
   extern __shared__ double dsm[];
   double(*Rs)[TS_H + 1] = reinterpret_cast<double(*)[TS_H + 1]>(dsm);
   double(*xs)[TS_H + 1] = reinterpret_cast<double(*)[TS_H + 1]>(dsm + TS_H * (TS_H + 1));
+  __shared__ double rdiag[TS_H];
   const int i0 = blockIdx.x * TS_H, h = min(TS_H, k - i0), c = threadIdx.x;
-  for (int e = c; e < h * h; e += blockDim.x) {
-    const int i = e / h, l = e % h;
-    Rs[i][l] = (l >= i) ? R[(int64_t)(i0 + i) * ldr + i0 + l] : 0.0;
+#pragma unroll 4
+  for (int e = c; e < TS_H * TS_H; e += DI_T) {
+    const int i = e / TS_H, l = e % TS_H;
+    Rs[i][l] = (i < h && l < h && l >= i) ? R[(int64_t)(i0 + i) * ldr + i0 + l] : 0.0;
   }
+  __syncthreads();
+  if (c < h) rdiag[c] = 1.0 / Rs[c][c];
   __syncthreads();
   if (c < h) {
     for (int i = h - 1; i >= 0; i--) {
       double s = (i == c) ? 1.0 : 0.0;
       if (i < c) {
-        double s0 = 0.0, s1 = 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int l = i + 1;
-        for (; l + 1 <= c; l += 2) {
+        for (; l + 3 <= c; l += 4) {
           s0 = fma(Rs[i][l], xs[l][c], s0);
           s1 = fma(Rs[i][l + 1], xs[l + 1][c], s1);
+          s2 = fma(Rs[i][l + 2], xs[l + 2][c], s2);
+          s3 = fma(Rs[i][l + 3], xs[l + 3][c], s3);
         }
-        if (l <= c) s0 = fma(Rs[i][l], xs[l][c], s0);
-        s -= s0 + s1;
+        for (; l <= c; l++) s0 = fma(Rs[i][l], xs[l][c], s0);
+        s -= (s0 + s1) + (s2 + s3);
       }
-      xs[i][c] = (i <= c) ? s / Rs[i][i] : 0.0;
+      xs[i][c] = (i <= c) ? s * rdiag[i] : 0.0;
     }
-    for (int i = 0; i < h; i++) X[(int64_t)(i0 + i) * ldx + i0 + c] = xs[i][c];
+  }
+  __syncthreads();
+  for (int e = c; e < h * h; e += DI_T) {
+    const int i = e / h, l = e % h;
+    X[(int64_t)(i0 + i) * ldx + i0 + l] = xs[i][l];
   }
 }
 
@@ -713,7 +726,7 @@ int tk_tri_inv(tk_ctx* ctx, int k, const double* R, int64_t ldr, double* X, int6
       cudaFuncSetAttribute(diag_inv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
       attr = true;
     }
-    diag_inv_k<<<nbk, TS_H, dsm, ctx->stream>>>(k, R, ldr, X, ldx);
+    diag_inv_k<<<nbk, DI_T, dsm, ctx->stream>>>(k, R, ldr, X, ldx);
     TK_LAUNCH_CHECK(ctx);
     tk_prof_end(ctx, pid);
   }
