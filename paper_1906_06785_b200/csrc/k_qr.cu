@@ -948,24 +948,40 @@ __global__ void __launch_bounds__(256) apply_reflector_right_k(int n, int m,
   }
 }
 
-// thr2[0] = (64 eps ||A||_F)^2 and stop_at[0] = INT_MAX (one CTA, fixed-order reduction)
-__global__ void __launch_bounds__(1024) qr_stop_init_k(int64_t nn, const double* __restrict__ A,
-                                                       double* __restrict__ thr2,
-                                                       int* __restrict__ stop_at) {
-  __shared__ double red[1024];
-  double s = 0.0;
-  for (int64_t e = threadIdx.x; e < nn; e += blockDim.x) s = fma(A[e], A[e], s);
-  red[threadIdx.x] = s;
+// thr2[0] = (64 eps ||A||_F)^2 and stop_at[0] = INT_MAX, in two small launches: per-CTA partial
+// sums of squares (fixed-order tree), then their sum in CTA order — deterministic, and ~5 us
+// instead of the ~70 us a single CTA needed for n = 896 (a chain of ~200 L2 round trips per
+// thread at the start of every pass-1 QR).
+constexpr int SQ_T = 256, SQ_MAXG = 148;
+__global__ void __launch_bounds__(SQ_T) qr_sq_partial_k(int64_t nn, const double* __restrict__ A,
+                                                        double* __restrict__ part) {
+  __shared__ double red[SQ_T];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * SQ_T;
+  int64_t e = (int64_t)blockIdx.x * SQ_T + threadIdx.x;
+  for (; e + 3 * stride < nn; e += 4 * stride) {
+    const double a0 = A[e], a1 = A[e + stride], a2 = A[e + 2 * stride], a3 = A[e + 3 * stride];
+    s0 = fma(a0, a0, s0);
+    s1 = fma(a1, a1, s1);
+    s2 = fma(a2, a2, s2);
+    s3 = fma(a3, a3, s3);
+  }
+  for (; e < nn; e += stride) s0 = fma(A[e], A[e], s0);
+  red[threadIdx.x] = (s0 + s1) + (s2 + s3);
   __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+  for (int st = SQ_T / 2; st > 0; st >>= 1) {
     if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const double e64 = 64.0 * 2.220446049250313e-16;
-    thr2[0] = e64 * e64 * red[0];
-    stop_at[0] = 0x7fffffff;
-  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void qr_stop_fin_k(int g, const double* __restrict__ part, double* __restrict__ thr2,
+                              int* __restrict__ stop_at) {
+  double t = 0.0;
+  for (int i = 0; i < g; i++) t += part[i];
+  const double e64 = 64.0 * 2.220446049250313e-16;
+  thr2[0] = e64 * e64 * t;
+  stop_at[0] = 0x7fffffff;
 }
 
 }  // namespace
@@ -988,13 +1004,19 @@ int tk_householder_q(tk_ctx* ctx, int n, const double* A, double* Q) {
   // basis; sqpart[p]: per-CTA squared norms written by the trailing update of panel p
   const int sq_stride = (n + AR_W - 1) / AR_W + 1;
   DevBuf qst, sqpart;
-  TK_TRY(qst.get(ctx, 2));
+  TK_TRY(qst.get(ctx, 2 + SQ_MAXG));
   TK_TRY(sqpart.get(ctx, (size_t)np * sq_stride));
   double* thr2 = qst.p;
   int* stop_at = (int*)(qst.p + 1);
   const bool no_stop = false;
-  qr_stop_init_k<<<1, 1024, 0, ctx->stream>>>((int64_t)n * n, A, thr2, stop_at);
-  TK_LAUNCH_CHECK(ctx);
+  {
+    const int64_t nn = (int64_t)n * n;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(SQ_MAXG, nn / (8 * SQ_T)));
+    qr_sq_partial_k<<<g, SQ_T, 0, ctx->stream>>>(nn, A, qst.p + 2);
+    TK_LAUNCH_CHECK(ctx);
+    qr_stop_fin_k<<<1, 1, 0, ctx->stream>>>(g, qst.p + 2, thr2, stop_at);
+    TK_LAUNCH_CHECK(ctx);
+  }
   DevBuf dbgb;  // (per-panel clock stamps of the panel kernels: not allocated = off)
   // global tail of the tall panel kernel (rows beyond BIG_M: QB columns + two reflector tails)
   DevBuf gtail;
