@@ -190,28 +190,52 @@ __global__ void dot_final_k(int64_t n, const double* __restrict__ a, const doubl
 
 __global__ void set_scalar_k(double* dst, double v) { dst[0] = v; }
 
-// trace of an n x n matrix (row-major) and ||P||_F^2 (nP entries), then the noise floor
+// per-CTA partial sums of squares of P (fixed-order tree; summed in CTA order by noise_floor_k:
+// deterministic).  One CTA took ~160 us for the 896 x 640 P of c4's bond 1, right before form_W.
+constexpr int NF_T = 256, NF_MAXG = 148;
+__global__ void __launch_bounds__(NF_T) sumsq_partial_k(int64_t nP, const double* __restrict__ P,
+                                                        double* __restrict__ part) {
+  __shared__ double red[NF_T];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * NF_T;
+  int64_t e = (int64_t)blockIdx.x * NF_T + threadIdx.x;
+  for (; e + 3 * stride < nP; e += 4 * stride) {
+    const double a0 = P[e], a1 = P[e + stride], a2 = P[e + 2 * stride], a3 = P[e + 3 * stride];
+    s0 = fma(a0, a0, s0);
+    s1 = fma(a1, a1, s1);
+    s2 = fma(a2, a2, s2);
+    s3 = fma(a3, a3, s3);
+  }
+  for (; e < nP; e += stride) s0 = fma(P[e], P[e], s0);
+  red[threadIdx.x] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  for (int st = NF_T / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// trace of an n x n matrix (row-major) and ||P||_F^2 (npart partial sums), then the noise floor
 __global__ void noise_floor_k(const double* __restrict__ G, int64_t n, double gscale,
-                              const double* __restrict__ P, int64_t nP, int64_t K, int64_t k,
+                              const double* __restrict__ part, int npart, int64_t K, int64_t k,
                               double* out) {
-  __shared__ double r1[256], r2[256];
-  double a = 0.0, b = 0.0;
+  __shared__ double r1[256];
+  double a = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += G[i * n + i];
-  if (P)
-    for (int64_t i = threadIdx.x; i < nP; i += blockDim.x) b += P[i] * P[i];
   r1[threadIdx.x] = a;
-  r2[threadIdx.x] = b;
   __syncthreads();
   for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st) {
-      r1[threadIdx.x] += r1[threadIdx.x + st];
-      r2[threadIdx.x] += r2[threadIdx.x + st];
-    }
+    if (threadIdx.x < st) r1[threadIdx.x] += r1[threadIdx.x + st];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     const double eps = 2.220446049250313e-16;
-    const double pf2 = P ? r2[0] : (double)k;
+    double pf2 = (double)k;
+    if (part) {
+      pf2 = 0.0;
+      for (int i = 0; i < npart; i++) pf2 += part[i];
+    }
     out[0] = 16.0 * eps * eps * (double)K * (gscale * r1[0]) * pf2 / (double)k;
   }
 }
@@ -252,7 +276,16 @@ __global__ void symmetrize_k(int64_t n, double* A) {
 
 int tk_noise_floor(tk_ctx* ctx, const double* trG_src, int64_t n_trG, double trG_scale,
                    const double* P, int64_t nP, int64_t K, int64_t k, double* out) {
-  noise_floor_k<<<1, 256, 0, ctx->stream>>>(trG_src, n_trG, trG_scale, P, nP, K, k, out);
+  DevBuf part;
+  int g = 0;
+  if (P) {
+    g = (int)std::max<int64_t>(1, std::min<int64_t>(NF_MAXG, nP / (8 * NF_T)));
+    TK_TRY(part.get(ctx, (size_t)g));
+    sumsq_partial_k<<<g, NF_T, 0, ctx->stream>>>(nP, P, part.p);
+    TK_LAUNCH_CHECK(ctx);
+  }
+  noise_floor_k<<<1, 256, 0, ctx->stream>>>(trG_src, n_trG, trG_scale, P ? part.p : nullptr, g, K, k,
+                                            out);
   TK_LAUNCH_CHECK(ctx);
   return TK_OK;
 }
